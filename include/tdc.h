@@ -1,0 +1,130 @@
+/*
+ * tdc.h -- C-ABI of the B200-native Tucker-format (TKD) convolution library
+ * (libtdc.so, built from paper_2211_03715_b200/csrc for sm_100a).
+ *
+ * The operation (BASELINE.json north_star): a TKD convolution
+ * layer, the Tucker-2 format of a K x K convolution ("truncates ...
+ * mode-1 and mode-2 matricization"; Eq. tkd2 referenced there), evaluated as
+ * three stages
+ *
+ *   stage 1  X'[b,h,w,a] = sum_c U_in[c,a] X[b,c,h,w]                 (1x1, C -> D1)
+ *   stage 2  Z[b,q,i,j]  = sum_a sum_r sum_t core[q,a,r,t]
+ *                              X'[b, i*s-p+r, j*s-p+t, a]              (K x K, D1 -> D2)
+ *   stage 3  Y[b,n,i,j]  = sum_q U_out[n,q] Z[b,q,i,j] (+ bias[n])      (1x1, D2 -> N)
+ *
+ * which equals one convolution with the reconstructed kernel
+ * W[n,c,r,t] = sum_{a,q} U_out[n,q] core[q,a,r,t] U_in[c,a] (Eq. tkd2).
+ * Stage 2 is the paper's "core convolution" (§5).  Conventions
+ * (DESIGN.md readings): cross-correlation (R4); stride and zero padding act on
+ * the core stage only (R5, R6); H' = floor((H + 2p - K)/s) + 1; B is batch and
+ * N output channels (R3).
+ *
+ * Threading: all calls are thread-safe on distinct plans.  A plan is immutable
+ * after creation; tdc_conv_forward may run concurrently on different streams
+ * only when tdc_plan_info.concurrent_forward is 1 (NHWC plans; NCHW plans use
+ * a plan-owned conversion workspace).
+ *
+ * Errors: every call returns a tdc_status; nothing throws or aborts across the
+ * ABI.  On failure tdc_last_error() (thread-local) holds a one-line message.
+ * Asynchronous device faults surface at the caller's next synchronisation.
+ */
+#ifndef TDC_H
+#define TDC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TDC_OK = 0,
+    TDC_ERR_INVALID_ARGUMENT = 1, /* bad size, rank bound, null pointer, batch > plan  */
+    TDC_ERR_UNSUPPORTED = 2,      /* device is not sm_100 / math mode not available    */
+    TDC_ERR_CUDA = 3,             /* a CUDA runtime/driver call or launch failed        */
+    TDC_ERR_OUT_OF_MEMORY = 4,    /* device or host allocation failed                   */
+    TDC_ERR_INTERNAL = 5
+} tdc_status;
+
+typedef enum {
+    TDC_LAYOUT_NCHW = 0, /* the paper's statement; converted on device    */
+    TDC_LAYOUT_NHWC = 1  /* fast path: channel-fastest, what the kernels read/write */
+} tdc_layout;
+
+typedef enum {
+    TDC_MATH_FP32 = 0,   /* fp32 FFMA on CUDA cores (the paper's precision); tol 1e-4 */
+    TDC_MATH_3XTF32 = 1, /* tcgen05 TF32 with hi/lo split (3 products); tol 1e-4            */
+    TDC_MATH_TF32 = 2    /* tcgen05 TF32, one product; tol 1e-2 (north_star)                */
+} tdc_math;
+
+/* Layer descriptor.  All sizes > 0; 1 <= rank_in <= c_in and
+ * 1 <= rank_out <= c_out; kernel <= height + 2*pad and
+ * kernel <= width + 2*pad; stride >= 1; pad >= 0. */
+typedef struct {
+    int32_t batch;             /* B: maximum batch this plan serves                 */
+    int32_t c_in, height, width; /* C, H, W of the input                            */
+    int32_t c_out;             /* N: output channels                                 */
+    int32_t rank_in, rank_out; /* D1, D2: Tucker ranks                               */
+    int32_t kernel;            /* K: core filter is K x K                            */
+    int32_t stride, pad;       /* of the core convolution (stage 2)                  */
+    int32_t layout;            /* tdc_layout of x and y                              */
+    int32_t math;              /* tdc_math                                           */
+} tdc_conv_desc;
+
+typedef struct tdc_conv_plan_s *tdc_conv_plan_t;
+
+/* Read-only description of what a plan will launch (for benches and tests). */
+typedef struct {
+    int32_t h_out, w_out;          /* H', W'                                          */
+    int32_t variant;               /* 1 = fused fp32 SIMT, 2 = fused tcgen05          */
+    char variant_name[48];
+    int32_t launches_per_forward;  /* kernels tdc_conv_forward enqueues                */
+    int32_t concurrent_forward;    /* 1 if forwards on distinct streams may overlap    */
+    int32_t tile_h, tile_w;        /* output pixels per CTA tile                       */
+    int32_t threads_per_cta;
+    int32_t smem_bytes_per_cta;
+    int64_t ctas_per_image;        /* CTAs launched per image by the main kernel       */
+    int64_t workspace_bytes;       /* device bytes owned by the plan beyond weights    */
+    int64_t weight_bytes;          /* packed device weight bytes                       */
+} tdc_plan_info;
+
+const char *tdc_version(void);
+const char *tdc_status_string(tdc_status s);
+/* Thread-local one-line message for the last failing call on this thread. */
+const char *tdc_last_error(void);
+
+/* H' and W' for a descriptor; validates it first. */
+tdc_status tdc_conv_output_shape(const tdc_conv_desc *desc, int32_t *h_out, int32_t *w_out);
+
+/* Plan a layer on CUDA device `device` (§8(a) row a0).  core (D2 x D1 x K x K),
+ * u_in (C x D1), u_out (N x D2) and bias (N, or NULL) are HOST fp32 arrays,
+ * row-major; they are copied and re-laid out (the CRSN idea, P:L338-340:
+ * "format conversion can be completely done offline once") so the caller may
+ * free them on return.  No kernel runs.  Returns UNSUPPORTED if the device is
+ * not compute capability 10.0 or the math mode is not built. */
+tdc_status tdc_conv_plan(const tdc_conv_desc *desc, const float *core,
+                         const float *u_in, const float *u_out,
+                         const float *bias, int32_t device, tdc_conv_plan_t *out);
+
+tdc_status tdc_conv_plan_query(tdc_conv_plan_t plan, tdc_plan_info *info);
+
+/* Forward (§8(a) rows a1-a4), asynchronous on `stream` (a cudaStream_t; NULL =
+ * legacy default stream).  x: DEVICE fp32, batch x C x H x W in desc.layout;
+ * y: DEVICE fp32, batch x N x H' x W' in the same layout, fully overwritten.
+ * 1 <= batch <= desc.batch; x and y must not alias.  The caller owns x, y and
+ * the stream. */
+tdc_status tdc_conv_forward(tdc_conv_plan_t plan, const float *x, float *y,
+                            int32_t batch, void *stream);
+
+/* End-to-end forward with HOST buffers: copies x to the device, runs
+ * tdc_conv_forward on plan-owned device buffers, copies y back and waits for
+ * the stream.  Host buffers should be pinned for asynchronous copies. */
+tdc_status tdc_conv_forward_host(tdc_conv_plan_t plan, const float *x_host,
+                                 float *y_host, int32_t batch, void *stream);
+
+tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TDC_H */

@@ -1,0 +1,164 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle.
+
+Error metric (reading R13): max_i |y_i - y_ref_i| / max_i |y_ref_i|.
+Tolerances (north_star): 1e-4 for FP32 and 3xTF32 math, 1e-2 for TF32.
+Integer-valued layers (every partial sum an integer < 2^24) must be bit-exact
+in FP32 math whatever the reduction order.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import LayerShape
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-4, "3xtf32": 1e-4, "tf32": 1e-2}
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2211_03715_b200 import tdc
+    return torch, tdc
+
+
+def run_layer(env, shape, d, layout="nhwc", math="fp32", batch=None):
+    torch, tdc = env
+    lay = tdc.TDC_LAYOUT_NHWC if layout == "nhwc" else tdc.TDC_LAYOUT_NCHW
+    plan = tdc.ConvPlan(shape, d, layout=lay, math=tdc.MATH_NAMES[math])
+    b = shape.B if batch is None else batch
+    x_np = d["x"][:b]
+    if layout == "nhwc":
+        x = torch.from_numpy(synth.nchw_to_nhwc(x_np)).cuda()
+        y = torch.full((b, shape.Ho, shape.Wo, shape.N), float("nan"), device="cuda")
+    else:
+        x = torch.from_numpy(np.ascontiguousarray(x_np)).cuda()
+        y = torch.full((b, shape.N, shape.Ho, shape.Wo), float("nan"), device="cuda")
+    plan.forward(x, y, batch=b)
+    torch.cuda.synchronize()
+    out = y.cpu().numpy()
+    info = plan.info()
+    plan.close()
+    if layout == "nhwc":
+        out = synth.nhwc_to_nchw(out)
+    return out, info
+
+
+def err(got, ref):
+    return float(np.max(np.abs(got.astype(np.float64) - ref)) / np.max(np.abs(ref)))
+
+
+def ref_of(shape, d, b=None):
+    x = d["x"] if b is None else d["x"][:b]
+    return oracle.tkd_stages(x, d["core"], d["u_in"], d["u_out"], d["bias"], shape.stride, shape.pad)
+
+
+MATHS = ["fp32"]
+
+
+@pytest.mark.parametrize("math", MATHS)
+@pytest.mark.parametrize("layout", ["nhwc", "nchw"])
+def test_config1(env, layout, math):
+    s = synth.CONFIG1
+    d = synth.make_layer(s)
+    got, _ = run_layer(env, s, d, layout, math)
+    assert np.all(np.isfinite(got))
+    assert err(got, ref_of(s, d)) <= TOL[math]
+
+
+@pytest.mark.parametrize("layout", ["nhwc", "nchw"])
+def test_integer_layer_is_bit_exact(env, layout):
+    s = LayerShape(2, 16, 16, 8, 8, 4, 4, 3, 1, 1)
+    d = synth.make_layer(s, integer=True, bias=True)
+    got, _ = run_layer(env, s, d, layout, "fp32")
+    assert np.array_equal(got.astype(np.float64), ref_of(s, d))
+
+
+@pytest.mark.parametrize("shape", [
+    LayerShape(3, 37, 29, 13, 11, 7, 5, 3, 1, 1),     # ragged C, N, D, H, W
+    LayerShape(2, 33, 18, 15, 9, 6, 3, 3, 2, 1),      # stride 2, odd sizes
+    LayerShape(1, 8, 12, 10, 10, 3, 5, 5, 1, 2),      # 5x5 core
+    LayerShape(2, 12, 8, 9, 7, 4, 4, 1, 1, 0),        # 1x1 core
+    LayerShape(1, 16, 16, 9, 9, 4, 4, 3, 3, 0),       # stride 3, no pad
+    LayerShape(1, 5, 3, 3, 3, 2, 2, 3, 1, 1),         # smaller than a tile
+    LayerShape(1, 64, 64, 1, 1, 16, 16, 3, 1, 1),     # 1x1 image, all padding
+    LayerShape(2, 64, 96, 20, 17, 64, 96, 3, 1, 1),   # full ranks
+])
+@pytest.mark.parametrize("math", MATHS)
+def test_ragged_and_edge_shapes(env, shape, math):
+    d = synth.make_layer(shape, seed=7, bias=True)
+    got, _ = run_layer(env, shape, d, "nhwc", math)
+    assert err(got, ref_of(shape, d)) <= TOL[math]
+
+
+@pytest.mark.parametrize("shape,count", synth.R18_SHAPES, ids=[s.name for s, _ in synth.R18_SHAPES])
+@pytest.mark.parametrize("math", MATHS)
+def test_r18_shapes_batch1_full(env, shape, count, math):
+    d = synth.make_layer(shape, seed=synth.BASE_SEED)
+    got, _ = run_layer(env, shape, d, "nhwc", math)
+    assert err(got, ref_of(shape, d)) <= TOL[math]
+
+
+@pytest.mark.parametrize("shape,count", synth.R18_SHAPES, ids=[s.name for s, _ in synth.R18_SHAPES])
+@pytest.mark.parametrize("math", MATHS)
+def test_r18_shapes_batch32_sampled(env, shape, count, math):
+    """Full benchmark size (B=32, the bench's launch configuration), checked on
+    sampled outputs the oracle evaluates one by one."""
+    s = shape.with_batch(32)
+    d = synth.make_layer(s, seed=synth.BASE_SEED)
+    got, _ = run_layer(env, s, d, "nhwc", math)
+    assert np.all(np.isfinite(got))
+    pts = synth.sample_points(s, 200)
+    ref = oracle.tkd_points(d["x"], d["core"], d["u_in"], d["u_out"], pts, None, s.stride, s.pad)
+    vals = np.array([got[p] for p in pts], dtype=np.float64)
+    scale = np.max(np.abs(ref))
+    assert np.max(np.abs(vals - ref)) / scale <= TOL[math]
+
+
+def test_partial_batch_and_batch_independence(env):
+    s = LayerShape(8, 32, 32, 14, 14, 16, 16, 3, 1, 1)
+    d = synth.make_layer(s, seed=3)
+    full, _ = run_layer(env, s, d)
+    part, _ = run_layer(env, s, d, batch=3)
+    one, _ = run_layer(env, s.with_batch(1), {**d, "x": d["x"][:1]})
+    assert np.array_equal(part, full[:3])
+    assert np.array_equal(one[0], full[0])
+
+
+def test_deterministic(env):
+    s = LayerShape(4, 64, 64, 28, 28, 32, 32, 3, 1, 1)
+    d = synth.make_layer(s, seed=5)
+    a, _ = run_layer(env, s, d)
+    b, _ = run_layer(env, s, d)
+    assert np.array_equal(a, b)
+
+
+def test_forward_host_matches_device(env):
+    torch, tdc = env
+    s = LayerShape(4, 32, 48, 12, 12, 8, 12, 3, 2, 1)
+    d = synth.make_layer(s, seed=9, bias=True)
+    plan = tdc.ConvPlan(s, d, layout=tdc.TDC_LAYOUT_NHWC)
+    xh = torch.from_numpy(synth.nchw_to_nhwc(d["x"])).pin_memory()
+    yh = torch.empty((s.B, s.Ho, s.Wo, s.N)).pin_memory()
+    plan.forward_host(xh, yh)
+    dev, _ = run_layer(env, s, d)
+    assert np.array_equal(synth.nhwc_to_nchw(yh.numpy()), dev)
+    plan.close()
+
+
+def test_forward_rejects_bad_calls(env):
+    torch, tdc = env
+    s = synth.CONFIG1
+    d = synth.make_layer(s)
+    plan = tdc.ConvPlan(s, d)
+    x = torch.zeros((1, 8, 8, 16), device="cuda")
+    with pytest.raises(tdc.TdcError):
+        plan.forward(x, x)  # aliasing
+    y = torch.zeros((2, 8, 8, 16), device="cuda")
+    with pytest.raises(tdc.TdcError):
+        tdc.tdc_conv_forward(plan._h, x.data_ptr(), y.data_ptr(), 2)  # batch > plan
+    plan.close()
