@@ -1,0 +1,365 @@
+#!/usr/bin/env python3
+"""Benchmark of the TKD-layer hot path (BASELINE.json configs[1]).
+
+Workload (one "step"): the 16 Tucker-format 3x3 layers of ResNet-18 (7
+distinct shapes x their multiplicity, paper-style ranks D = C/2, reading R15),
+each applied to its own batch-32 synthetic input, NHWC fp32, through the C-ABI
+(tdc_conv_forward).  Every layer instance owns distinct input/output buffers
+(~424 MB per step in total, > the 126 MB L2), so each launch reads its input
+from HBM; weights are a few MB and legitimately L2-resident.
+
+value  = algorithmic HBM bytes of all layers on all ranks / max-over-ranks time
+         (GB/s; bytes = input once + output once + weights once per layer).
+e2e    = the same metric through tdc_conv_forward_host with pinned host buffers
+         (H2D of every input and D2H of every output inside the timed region).
+roofline = the dominant layer's kernel: achieved bytes (or FLOPs) per launch /
+         its mean CUDA-event duration on the launching stream.
+cpu_baseline / --impl reference = the fp64 CPU oracle (oracle/) on a bounded
+         sample of the same workload.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; for N>1 under
+torchrun, one process per GPU, each running the full per-GPU workload (weak
+scaling: the layer is independent per image, no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2211_03715_b200 import roofline as rl  # noqa: E402
+
+METRIC = "TKD-layer µs & HBM GB/s vs peak"
+UNIT = "GB/s"
+WORKLOAD = "tucker_resnet18_3x3_tkd_layers"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["tdc", "reference"], default="tdc")
+    ap.add_argument("--math", choices=["fp32", "tf32", "3xtf32"], default="fp32")
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def layer_instances(batch: int):
+    """(layer_id, shape) for the 16 TKD layers of Tucker ResNet-18."""
+    out = []
+    lid = 0
+    for shape, count in synth.R18_SHAPES:
+        for _ in range(count):
+            out.append((lid, shape.with_batch(batch)))
+            lid += 1
+    return out
+
+
+def config_dict(args, n_gpus):
+    return {"workload": WORKLOAD,
+            "layers": [f"{s.name} x{c}" for s, c in synth.R18_SHAPES],
+            "batch_per_gpu": args.batch, "global_batch": args.batch * n_gpus,
+            "ranks": "paper-style D1=C/2, D2=N/2 (DESIGN.md R15)",
+            "layout": "NHWC", "math": args.math,
+            "l2": "inputs larger than L2: 16 distinct input/output buffer sets (~424 MB/step at B=32) rotate each step",
+            "parallelism": f"dp{n_gpus} (batch-sharded, no data-path collective)"}
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.nv = None
+            self.err = str(e)
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- oracle arm
+def run_oracle_sample(insts, budget_s: float):
+    """Time the fp64 oracle on images of the workload, layer by layer, until the
+    budget is spent (at least one full image through all 16 layers)."""
+    import oracle
+    total_bytes, n_img, t0 = 0, 0, time.perf_counter()
+    data = {lid: synth.make_layer(s.with_batch(1), seed=synth.BASE_SEED, layer_id=lid)
+            for lid, s in insts}
+    elapsed = 0.0
+    while True:
+        t1 = time.perf_counter()
+        for lid, s in insts:
+            d = data[lid]
+            oracle.tkd_stages(d["x"], d["core"], d["u_in"], d["u_out"], None, s.stride, s.pad)
+            total_bytes += rl.tkd_bytes(s, B=1)
+        elapsed += time.perf_counter() - t1
+        n_img += 1
+        if elapsed >= budget_s or n_img >= insts[0][1].B:
+            break
+    del t0
+    return total_bytes, n_img, elapsed
+
+
+def impl_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return  # rank 0 alone runs the CPU oracle arm
+    import oracle
+    insts = layer_instances(args.batch)
+    threads = oracle.max_threads()
+    for _ in range(args.warmup):
+        run_oracle_sample(insts, 0.0)
+    tb, ti = 0, 0.0
+    for _ in range(args.steps):
+        b, n, t = run_oracle_sample(insts, 0.0)
+        tb += b
+        ti += t
+    value = tb / ti / 1e9
+    sample = "1 image (batch 1) through all 16 Tucker ResNet-18 3x3 TKD layers per step"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ti / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, 1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ tdc arm
+def impl_tdc(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2211_03715_b200 import tdc
+
+    math = tdc.MATH_NAMES[args.math]
+    insts = layer_instances(args.batch)
+    stream = torch.cuda.Stream()
+    layers = []
+    for lid, s in insts:
+        d = synth.make_layer(s, seed=synth.BASE_SEED + 1000 * rank, layer_id=lid)
+        plan = tdc.ConvPlan(s, d, layout=tdc.TDC_LAYOUT_NHWC, math=math, device=local)
+        x = torch.from_numpy(synth.nchw_to_nhwc(d["x"])).cuda()
+        y = torch.empty((s.B, s.Ho, s.Wo, s.N), device="cuda")
+        layers.append({"lid": lid, "shape": s, "plan": plan, "x": x, "y": y, "xnp": d["x"]})
+    launches_per_step = sum(L["plan"].info().launches_per_forward for L in layers)
+    torch.cuda.synchronize()
+
+    def step(events=None):
+        for i, L in enumerate(layers):
+            if events is not None:
+                events[i][0].record(stream)
+            L["plan"].forward(L["x"], L["y"], stream=stream)
+            if events is not None:
+                events[i][1].record(stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    torch.cuda.synchronize()
+
+    ev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+           for _ in layers] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(ev[k])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # per-layer mean durations (events on the launching stream)
+    per_layer_ms = [statistics.mean(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps))
+                    for i in range(len(layers))]
+    step_bytes = sum(rl.tkd_bytes(L["shape"]) for L in layers)
+    value = step_bytes * args.steps * world / (total_ms * 1e-3) / 1e9
+
+    # ---- per distinct shape summary and the dominant kernel's roofline ----
+    peaks = rl.measured_peaks()
+    eng = rl.engine_peak_tflops(args.math, peaks)
+    shapes = {}
+    for L, ms in zip(layers, per_layer_ms):
+        s = L["shape"]
+        e = shapes.setdefault(s.name, {"shape": s, "ms": [], "info": L["plan"].info()})
+        e["ms"].append(ms)
+    layer_rows = []
+    dominant, dom_share = None, -1.0
+    for name, e in shapes.items():
+        s = e["shape"]
+        us = statistics.mean(e["ms"]) * 1e3
+        by, fl = rl.tkd_bytes(s), rl.tkd_flops(s)
+        row = {"layer": name, "count": len(e["ms"]), "us": round(us, 3),
+               "gbs": round(by / (us * 1e-6) / 1e9, 1),
+               "hbm_frac": round(by / (us * 1e-6) / 1e9 / peaks["hbm_gbs"], 4),
+               "tflops": round(fl / (us * 1e-6) / 1e12, 2),
+               "engine_frac": round(fl / (us * 1e-6) / 1e12 / eng, 4),
+               "bytes": by, "flops": fl, "ai_flop_per_byte": round(fl / by, 1),
+               "variant": e["info"].variant_name, "tile": [e["info"].tile_h, e["info"].tile_w],
+               "ctas": e["info"].ctas_per_image * s.B}
+        layer_rows.append(row)
+        share = us * len(e["ms"])
+        if share > dom_share:
+            dom_share, dominant = share, (row, s)
+    row, s = dominant
+    ridge = eng * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    compute_bound = row["ai_flop_per_byte"] > ridge
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(args.math, {}).get(row["layer"])
+    if compute_bound:
+        bound = "alu" if args.math == "fp32" else "tensor"
+        roof = {"bound": bound, "achieved": row["tflops"], "peak": round(eng, 1), "unit": "TFLOP/s",
+                "frac": round(row["tflops"] / eng, 4)}
+        peak_src = ("FP32 FFMA: 148 SMs x 128 lanes x 2 x sm_max_mhz (DESIGN.md)" if args.math == "fp32"
+                    else f"TF32 = measured bf16 burst x 1.1/2.25 ({peaks['source']})")
+    else:
+        roof = {"bound": "hbm", "achieved": row["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(row["gbs"] / peaks["hbm_gbs"], 4)}
+        peak_src = f"HBM copy {peaks['source']}"
+    roof.update({"traffic": traffic, "kernel": row["variant"], "layer": row["layer"],
+                 "peak_source": peak_src,
+                 "hbm": {"achieved": row["gbs"], "peak": peaks["hbm_gbs"], "frac": row["hbm_frac"]},
+                 "share_of_step": round(dom_share * 1e-3 / (total_ms / args.steps), 3)})
+
+    # ---- end to end through the host-buffer C-ABI call ----
+    e2e = None
+    if not args.no_e2e:
+        host = []
+        for L in layers:
+            s = L["shape"]
+            xh = torch.from_numpy(synth.nchw_to_nhwc(L["xnp"])).pin_memory()
+            yh = torch.empty((s.B, s.Ho, s.Wo, s.N)).pin_memory()
+            host.append((xh, yh))
+        for L, (xh, yh) in zip(layers, host):
+            L["plan"].forward_host(xh, yh, stream=stream)
+        e2e_steps = max(1, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            for L, (xh, yh) in zip(layers, host):
+                L["plan"].forward_host(xh, yh, stream=stream)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": step_bytes * e2e_steps * world / el / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": sum(int(h[0].numel()) * 4 for h in host),
+               "d2h_bytes_per_step": sum(int(h[1].numel()) * 4 for h in host),
+               "steps": e2e_steps, "api": "tdc_conv_forward_host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        b, n, t = run_oracle_sample(insts, args.cpu_budget_s)
+        cpu = {"value": b / t / 1e9, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+               "sample": f"{n} image(s) (batch 1) through all 16 TKD layers, fp64, {t:.1f} s"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": max(args.warmup, 3),
+                "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": {"fp32": "f32", "tf32": "tf32", "3xtf32": "3xtf32"}[args.math],
+                "data": "synthetic", "config": config_dict(args, world),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches_per_step * args.steps,
+                "clocks": sampler.summary(), "layers": layer_rows,
+                "step_bytes": step_bytes, "step_flops": sum(rl.tkd_flops(L["shape"]) for L in layers)}
+        print(json.dumps(line), flush=True)
+    for L in layers:
+        L["plan"].close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        impl_reference(args)
+    else:
+        impl_tdc(args)
+
+
+if __name__ == "__main__":
+    main()

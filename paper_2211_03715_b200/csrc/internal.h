@@ -1,6 +1,7 @@
 // internal.h -- device-side parameter blocks and launchers shared by the
 // C-ABI (tdc_api.cu) and the kernels.  Not part of the public ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -33,6 +34,25 @@ bool simt_choose_tile(const LayerDims &d, int D1p, int D2p, int max_smem, SimtTi
 // x, y NHWC.  Launches one kernel.
 cudaError_t simt_fused_launch(const LayerDims &d, const SimtWeights &w, const SimtTile &t,
                               const float *x, float *y, int batch, cudaStream_t st);
+
+// ---- tensor-core (tcgen05) GEMM with taps: see tkd_tc.cu ----
+constexpr int kMaxTaps = 49;
+struct TcGemmArgs {
+    int M, Nn, kchunks, taps, BN, stages;
+    int a_off[kMaxTaps], b_off[kMaxTaps];
+    float *out;
+    int ldo;
+    const float *bias;
+    int remap;  // 0 identity, 1 pixel -> phase grid, 2 output grid -> compact
+    int H, W, s, p, Hq, Wq, Ho, Wo;
+    long long phase_rows;
+};
+int tc_smem_bytes(int BN, int stages);
+int tc_pick_stages(int BN, int iters, int max_smem);
+bool make_tma_2d(CUtensorMap *map, const float *base, long long rows, int k_extent, int pitch,
+                 int box_rows);
+cudaError_t tc_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapB, const TcGemmArgs &g,
+                           int grid_n, cudaStream_t st);
 
 // NCHW <-> NHWC for the NCHW API layout.
 cudaError_t nchw_to_nhwc(const float *src, float *dst, int B, int C, int H, int W,

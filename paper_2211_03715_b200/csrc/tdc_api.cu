@@ -95,7 +95,159 @@ struct tdc_conv_plan_s {
     float *d_ws_in = nullptr, *d_ws_out = nullptr;
     size_t ws_bytes = 0;
     float *d_stage_x = nullptr, *d_stage_y = nullptr;
+    // tensor-core variant (variant 2): three tcgen05 GEMM-with-taps launches
+    struct TcStage {
+        tdc::TcGemmArgs args;
+        CUtensorMap mapA, mapB;
+        int grid_n = 1;
+    } tc[3];
+    float *d_tc_w = nullptr;       // Bt1 | Bt2 | Bt3 | bias
+    float *d_xg = nullptr;         // X' phase grids (zero borders)
+    float *d_z = nullptr;          // Z compact
+    size_t tc_ws_bytes = 0;
+    const float *tc_last_x = nullptr;
+    int max_smem = 0;
 };
+
+namespace {
+
+int pick_bn(int nn, long long mtiles) {
+    int bn = 256;
+    while (bn > 32 && bn / 2 >= nn) bn /= 2;          // do not exceed the output width
+    while (bn > 64 && mtiles * ((nn + bn - 1) / bn) < 2 * 148) bn /= 2;  // fill the SMs
+    return bn;
+}
+
+int div_up(int a, int b) { return (a + b - 1) / b; }
+
+// Plan the tcgen05 variant: weight re-layout (a0), workspaces, tensor maps.
+tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, const float *u_out,
+                   const float *bias) {
+    const tdc_conv_desc &d = p->desc;
+    const int C = d.c_in, N = d.c_out, D1 = d.rank_in, D2 = d.rank_out, K = d.kernel;
+    const int s = d.stride, pad = d.pad, H = d.height, W = d.width;
+    const int Ho = p->dims.Ho, Wo = p->dims.Wo, Bm = d.batch;
+    const int Cs = round_up(C, 32), D1s = round_up(D1, 32), D2s = round_up(D2, 32);
+    const int Hq = div_up(H + 2 * pad, s), Wq = div_up(W + 2 * pad, s);
+    const long long phase_rows = (long long)Bm * Hq * Wq;
+    const long long M1 = (long long)Bm * H * W, M2 = phase_rows, M3 = (long long)Bm * Ho * Wo;
+    if (M1 > (1LL << 31) - 256 || M2 * s * s > (1LL << 31) - 256)
+        return fail(TDC_ERR_UNSUPPORTED, "batch too large for the tensor-core variant");
+    const int BN1 = pick_bn(D1s, div_up((int)M1, 128));
+    const int BN2 = pick_bn(D2s, div_up((int)M2, 128));
+    const int BN3 = pick_bn(N, div_up((int)M3, 128));
+    const int R1 = round_up(D1s, BN1), R2 = round_up(D2s, BN2), R3 = round_up(N, BN3);
+    const int KK = K * K;
+
+    // ---- a0: K-major weight panels, zero padded (CRSN idea) ----
+    const size_t n1 = (size_t)R1 * Cs, n2 = (size_t)KK * R2 * D1s, n3 = (size_t)R3 * D2s,
+                 nb = (size_t)round_up(N, 4);
+    std::vector<float> h(n1 + n2 + n3 + nb, 0.f);
+    float *b1 = h.data(), *b2 = b1 + n1, *b3 = b2 + n2, *hb = b3 + n3;
+    for (int a = 0; a < D1; ++a)
+        for (int c = 0; c < C; ++c) b1[(size_t)a * Cs + c] = u_in[(size_t)c * D1 + a];
+    for (int r = 0; r < K; ++r)
+        for (int t = 0; t < K; ++t)
+            for (int q = 0; q < D2; ++q)
+                for (int a = 0; a < D1; ++a)
+                    b2[((size_t)(r * K + t) * R2 + q) * D1s + a] =
+                        core[(((size_t)q * D1 + a) * K + r) * K + t];
+    for (int n = 0; n < N; ++n)
+        for (int q = 0; q < D2; ++q) b3[(size_t)n * D2s + q] = u_out[(size_t)n * D2 + q];
+    if (bias)
+        for (int n = 0; n < N; ++n) hb[n] = bias[n];
+    cudaError_t e = cudaMalloc(&p->d_tc_w, h.size() * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(tc weights)");
+    e = cudaMemcpy(p->d_tc_w, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(tc weights)");
+    p->weight_bytes += h.size() * sizeof(float);
+
+    // ---- workspaces: X' phase grids (zero borders, never written there) and Z ----
+    const size_t xg_elems = (size_t)s * s * phase_rows * D1s;
+    const size_t z_elems = (size_t)M3 * D2s;
+    e = cudaMalloc(&p->d_xg, xg_elems * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_z, z_elems * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(tc workspace)");
+    e = cudaMemset(p->d_xg, 0, xg_elems * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(X' grid)");
+    p->tc_ws_bytes = (xg_elems + z_elems) * sizeof(float);
+
+    auto base_args = [&](tdc::TcGemmArgs &g) {
+        std::memset(&g, 0, sizeof g);
+        g.H = H; g.W = W; g.s = s; g.p = pad; g.Hq = Hq; g.Wq = Wq; g.Ho = Ho; g.Wo = Wo;
+        g.phase_rows = phase_rows;
+    };
+    const float *dB1 = p->d_tc_w, *dB2 = dB1 + n1, *dB3 = dB2 + n2, *dbias = dB3 + n3;
+    // stage 1: A = X (per forward), Bt1; out = X' grid
+    {
+        auto &st = p->tc[0];
+        base_args(st.args);
+        st.args.M = (int)M1; st.args.Nn = D1s; st.args.kchunks = Cs / 32; st.args.taps = 1;
+        st.args.BN = BN1; st.args.out = p->d_xg; st.args.ldo = D1s; st.args.remap = 1;
+        st.args.stages = tdc::tc_pick_stages(BN1, Cs / 32, p->max_smem);
+        st.grid_n = R1 / BN1;
+        if (!tdc::make_tma_2d(&st.mapB, dB1, R1, Cs, Cs, BN1))
+            return fail(TDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (stage-1 weights)");
+    }
+    // stage 2: A = X' grid, Bt2 (K*K taps); out = Z compact
+    {
+        auto &st = p->tc[1];
+        base_args(st.args);
+        st.args.M = (int)M2; st.args.Nn = D2s; st.args.kchunks = D1s / 32; st.args.taps = KK;
+        st.args.BN = BN2; st.args.out = p->d_z; st.args.ldo = D2s; st.args.remap = 2;
+        for (int r = 0; r < K; ++r)
+            for (int t = 0; t < K; ++t) {
+                const int ph = (r % s) * s + (t % s);
+                st.args.a_off[r * K + t] = (int)(ph * phase_rows + (r / s) * Wq + (t / s));
+                st.args.b_off[r * K + t] = (r * K + t) * R2;
+            }
+        st.args.stages = tdc::tc_pick_stages(BN2, KK * D1s / 32, p->max_smem);
+        st.grid_n = R2 / BN2;
+        if (!tdc::make_tma_2d(&st.mapA, p->d_xg, (long long)s * s * phase_rows, D1s, D1s, 128) ||
+            !tdc::make_tma_2d(&st.mapB, dB2, (long long)KK * R2, D1s, D1s, BN2))
+            return fail(TDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (stage 2)");
+    }
+    // stage 3: A = Z, Bt3 = U_out; out = Y (per forward), bias
+    {
+        auto &st = p->tc[2];
+        base_args(st.args);
+        st.args.M = (int)M3; st.args.Nn = N; st.args.kchunks = D2s / 32; st.args.taps = 1;
+        st.args.BN = BN3; st.args.ldo = N; st.args.remap = 0; st.args.bias = bias ? dbias : nullptr;
+        st.args.stages = tdc::tc_pick_stages(BN3, D2s / 32, p->max_smem);
+        st.grid_n = R3 / BN3;
+        if (!tdc::make_tma_2d(&st.mapA, p->d_z, M3, D2s, D2s, 128) ||
+            !tdc::make_tma_2d(&st.mapB, dB3, R3, D2s, D2s, BN3))
+            return fail(TDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (stage 3)");
+    }
+    p->variant = 2;
+    return TDC_OK;
+}
+
+tdc_status forward_tc(tdc_conv_plan_s *p, const float *x, float *y, int batch, cudaStream_t st) {
+    const tdc::LayerDims &d = p->dims;
+    auto &s1 = p->tc[0], &s2 = p->tc[1], &s3 = p->tc[2];
+    if (x != p->tc_last_x) {
+        if (!tdc::make_tma_2d(&s1.mapA, x, (long long)p->desc.batch * d.H * d.W, d.C, d.C, 128))
+            return fail(TDC_ERR_INVALID_ARGUMENT,
+                        "cuTensorMapEncodeTiled rejected x (needs 16-byte aligned pointer)");
+        p->tc_last_x = x;
+    }
+    tdc::TcGemmArgs a1 = s1.args, a2 = s2.args, a3 = s3.args;
+    a1.M = batch * d.H * d.W;
+    const int Hq = a2.Hq, Wq = a2.Wq;
+    a2.M = batch * Hq * Wq;
+    a3.M = batch * d.Ho * d.Wo;
+    a3.out = y;
+    cudaError_t e = tdc::tc_gemm_launch(s1.mapA, s1.mapB, a1, s1.grid_n, st);
+    if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-1 launch");
+    e = tdc::tc_gemm_launch(s2.mapA, s2.mapB, a2, s2.grid_n, st);
+    if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-2 launch");
+    e = tdc::tc_gemm_launch(s3.mapA, s3.mapB, a3, s3.grid_n, st);
+    if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-3 launch");
+    return TDC_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -146,8 +298,8 @@ tdc_status tdc_conv_plan(const tdc_conv_desc *desc, const float *core, const flo
     if (prop.major != 10 || prop.minor != 0)
         return fail(TDC_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a only",
                     device, prop.major, prop.minor);
-    if (desc->math != TDC_MATH_FP32)
-        return fail(TDC_ERR_UNSUPPORTED, "math mode %d is not available in this build", desc->math);
+    if (desc->math == TDC_MATH_3XTF32)
+        return fail(TDC_ERR_UNSUPPORTED, "math mode 3XTF32 is not available in this build");
 
     DeviceGuard guard(device);
     if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
@@ -202,12 +354,22 @@ tdc_status tdc_conv_plan(const tdc_conv_desc *desc, const float *core, const flo
 
     // ---- variant selection ----
     const int max_smem = (int)prop.sharedMemPerBlockOptin;
+    p->max_smem = max_smem;
     if (!tdc::simt_choose_tile(p->dims, D1p, D2p, max_smem, &p->simt_tile)) {
         tdc_conv_plan_destroy(p);
         return fail(TDC_ERR_UNSUPPORTED, "ranks D1=%d D2=%d too large for the fused kernel's "
                     "shared-memory budget (%d bytes)", D1, D2, max_smem);
     }
     p->variant = 1;
+    // Tensor-core variant: TMA needs 16-byte row pitches (C % 4 == 0) and at most
+    // kMaxTaps taps; otherwise the plan keeps the (more accurate) fp32 variant.
+    if (d.math == TDC_MATH_TF32 && C % 4 == 0 && K * K <= tdc::kMaxTaps) {
+        s = plan_tc(p, core, u_in, u_out, bias);
+        if (s != TDC_OK) {
+            tdc_conv_plan_destroy(p);
+            return s;
+        }
+    }
 
     if (d.layout == TDC_LAYOUT_NCHW) {
         const size_t in_b = (size_t)d.batch * C * d.height * d.width * sizeof(float);
@@ -230,15 +392,24 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
     info->h_out = p->dims.Ho;
     info->w_out = p->dims.Wo;
     info->variant = p->variant;
-    std::snprintf(info->variant_name, sizeof info->variant_name, "%s", "fused_simt_fp32");
-    info->launches_per_forward = p->desc.layout == TDC_LAYOUT_NCHW ? 3 : 1;
-    info->concurrent_forward = p->desc.layout == TDC_LAYOUT_NHWC ? 1 : 0;
+    const bool tc = p->variant == 2;
+    std::snprintf(info->variant_name, sizeof info->variant_name, "%s",
+                  tc ? "tc3_tf32" : "fused_simt_fp32");
+    info->launches_per_forward = (tc ? 3 : 1) + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
+    info->concurrent_forward = (p->desc.layout == TDC_LAYOUT_NHWC && !tc) ? 1 : 0;
     info->tile_h = p->simt_tile.oth;
     info->tile_w = p->simt_tile.otw;
     info->threads_per_cta = 256;
     info->smem_bytes_per_cta = p->simt_tile.smem_bytes;
     info->ctas_per_image = (int64_t)p->simt_tile.tiles_h * p->simt_tile.tiles_w;
-    info->workspace_bytes = (int64_t)p->ws_bytes;
+    info->workspace_bytes = (int64_t)(p->ws_bytes + p->tc_ws_bytes);
+    if (tc) {
+        info->tile_h = 128;
+        info->tile_w = p->tc[1].args.BN;
+        info->threads_per_cta = 192;
+        info->smem_bytes_per_cta = tdc::tc_smem_bytes(p->tc[1].args.BN, p->tc[1].args.stages);
+        info->ctas_per_image = 0;
+    }
     info->weight_bytes = (int64_t)p->weight_bytes;
     return TDC_OK;
 }
@@ -261,14 +432,20 @@ tdc_status tdc_conv_forward(tdc_conv_plan_t p, const float *x, float *y, int32_t
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
     if (p->desc.layout == TDC_LAYOUT_NHWC) {
+        if (p->variant == 2) return forward_tc(p, x, y, batch, st);
         e = tdc::simt_fused_launch(d, p->simt, p->simt_tile, x, y, batch, st);
         if (e != cudaSuccess) return cuda_fail(e, "fused SIMT kernel launch");
         return TDC_OK;
     }
     e = tdc::nchw_to_nhwc(x, p->d_ws_in, batch, d.C, d.H, d.W, st);
     if (e != cudaSuccess) return cuda_fail(e, "NCHW->NHWC launch");
-    e = tdc::simt_fused_launch(d, p->simt, p->simt_tile, p->d_ws_in, p->d_ws_out, batch, st);
-    if (e != cudaSuccess) return cuda_fail(e, "fused SIMT kernel launch");
+    if (p->variant == 2) {
+        tdc_status s = forward_tc(p, p->d_ws_in, p->d_ws_out, batch, st);
+        if (s != TDC_OK) return s;
+    } else {
+        e = tdc::simt_fused_launch(d, p->simt, p->simt_tile, p->d_ws_in, p->d_ws_out, batch, st);
+        if (e != cudaSuccess) return cuda_fail(e, "fused SIMT kernel launch");
+    }
     e = tdc::nhwc_to_nchw(p->d_ws_out, y, batch, d.N, d.Ho, d.Wo, st);
     if (e != cudaSuccess) return cuda_fail(e, "NHWC->NCHW launch");
     return TDC_OK;
@@ -314,6 +491,9 @@ tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t p) {
     cudaFree(p->d_ws_out);
     cudaFree(p->d_stage_x);
     cudaFree(p->d_stage_y);
+    cudaFree(p->d_tc_w);
+    cudaFree(p->d_xg);
+    cudaFree(p->d_z);
     delete p;
     return TDC_OK;
 }

@@ -57,7 +57,7 @@ def ref_of(shape, d, b=None):
     return oracle.tkd_stages(x, d["core"], d["u_in"], d["u_out"], d["bias"], shape.stride, shape.pad)
 
 
-MATHS = ["fp32"]
+MATHS = ["fp32", "tf32"]
 
 
 @pytest.mark.parametrize("math", MATHS)
@@ -119,21 +119,32 @@ def test_r18_shapes_batch32_sampled(env, shape, count, math):
     assert np.max(np.abs(vals - ref)) / scale <= TOL[math]
 
 
-def test_partial_batch_and_batch_independence(env):
+@pytest.mark.parametrize("shape,count", synth.R18_SHAPES, ids=[s.name for s, _ in synth.R18_SHAPES])
+def test_tensor_core_variant_is_selected(env, shape, count):
+    torch, tdc = env
+    d = synth.make_layer(shape)
+    plan = tdc.ConvPlan(shape.with_batch(32), d, math=tdc.TDC_MATH_TF32)
+    assert plan.info().variant_name.startswith("tc")
+    plan.close()
+
+
+@pytest.mark.parametrize("math", MATHS)
+def test_partial_batch_and_batch_independence(env, math):
     s = LayerShape(8, 32, 32, 14, 14, 16, 16, 3, 1, 1)
     d = synth.make_layer(s, seed=3)
-    full, _ = run_layer(env, s, d)
-    part, _ = run_layer(env, s, d, batch=3)
-    one, _ = run_layer(env, s.with_batch(1), {**d, "x": d["x"][:1]})
+    full, _ = run_layer(env, s, d, math=math)
+    part, _ = run_layer(env, s, d, batch=3, math=math)
+    one, _ = run_layer(env, s.with_batch(1), {**d, "x": d["x"][:1]}, math=math)
     assert np.array_equal(part, full[:3])
     assert np.array_equal(one[0], full[0])
 
 
-def test_deterministic(env):
+@pytest.mark.parametrize("math", MATHS)
+def test_deterministic(env, math):
     s = LayerShape(4, 64, 64, 28, 28, 32, 32, 3, 1, 1)
     d = synth.make_layer(s, seed=5)
-    a, _ = run_layer(env, s, d)
-    b, _ = run_layer(env, s, d)
+    a, _ = run_layer(env, s, d, math=math)
+    b, _ = run_layer(env, s, d, math=math)
     assert np.array_equal(a, b)
 
 
