@@ -46,13 +46,55 @@ struct TcGemmArgs {
     int remap;  // 0 identity, 1 pixel -> phase grid, 2 output grid -> compact
     int H, W, s, p, Hq, Wq, Ho, Wo;
     long long phase_rows;
+    long long planar_stride;  // >0: epilogue writes planar [col/4][row][4] with this plane stride (floats)
 };
+
+// Stage-2 core convolution with a shared-memory-resident X' band (tkd_tc.cu):
+// X' planar [kg][rows_total][4]; weights pre-blocked [tap][kc][ntile][8][BN][4].
+struct TcCoreArgs {
+    const float *xg;          // X' planar grid
+    long long plane_stride;   // floats between kg planes (rows_total * 4)
+    const float *w;           // blocked core weights
+    float *z;                 // Z compact [B*Ho*Wo][ldz]
+    int ldz, Nn;              // Z pitch, valid output columns (D2s)
+    int M;                    // output-grid rows this launch
+    int kchunks, taps, ntiles, BN, nphase, band_rows, b_stages;
+    long long phase_rows;
+    int tap_phase[kMaxTaps], tap_off[kMaxTaps];
+    int phase_src[kMaxTaps];   // global phase index of compact phase i
+    int Hq, Wq, Ho, Wo;
+};
+int tc_core_smem_bytes(int BN, int nphase, int band_rows, int b_stages);
+cudaError_t tc_core_launch(const TcCoreArgs &g, cudaStream_t st);
 int tc_smem_bytes(int BN, int stages);
 int tc_pick_stages(int BN, int iters, int max_smem);
 bool make_tma_2d(CUtensorMap *map, const float *base, long long rows, int k_extent, int pitch,
                  int box_rows);
 cudaError_t tc_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapB, const TcGemmArgs &g,
                            int grid_n, cudaStream_t st);
+
+// ---- fused single-kernel TKD layer (tkd_fused.cu) ----
+struct FusedArgs {
+    int B, H, W, C, N, Ho, Wo, K, KK, s, p;
+    int R, Rin, Wp, Wq;          // output rows per tile; input band rows/cols; phase-grid width
+    int tiles_per_img, num_tiles;
+    int nblk1, c_chunks;         // stage-1 accumulator blocks (128 rows); C/32 chunks
+    int D1s, D2s, Nh, nhalves;   // padded ranks; stage-3 columns per pass
+    int nph, PR, TR;             // X' phases, phase-plane stride (rows), total rows
+    int tap_phase[kMaxTaps], tap_off[kMaxTaps];
+    int phase_idx[kMaxTaps];     // (py*s+px) -> compact phase or -1
+    const float *w;              // [U_in chunks][core chunks][U_out chunks], blocked [8][rows][4]
+    const float *bias;
+    float *y;
+    int XS, WS;                  // ring depths (X chunks, weight chunks)
+    int acc3_col, tmem_cols, nbuf3;   // stage-3 accumulator column, TMEM size, buffers
+    int P1, P2, P3;  // independent accumulator chains per stage (hide MMA accumulate latency)
+};
+int fused_smem_bytes(const FusedArgs &g);
+bool make_tma_4d_nhwc(CUtensorMap *map, const float *x, int C, int W, int H, int B, int box_w,
+                      int box_h);
+bool fused_make_x_map(CUtensorMap *map, const float *x, const FusedArgs &g);
+cudaError_t fused_launch(const CUtensorMap &mapX, const FusedArgs &g, int grid, cudaStream_t st);
 
 // NCHW <-> NHWC for the NCHW API layout.
 cudaError_t nchw_to_nhwc(const float *src, float *dst, int B, int C, int H, int W,

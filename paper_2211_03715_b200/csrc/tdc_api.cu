@@ -5,7 +5,9 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -101,6 +103,14 @@ struct tdc_conv_plan_s {
         CUtensorMap mapA, mapB;
         int grid_n = 1;
     } tc[3];
+    // fused single-kernel variant (variant 3)
+    tdc::FusedArgs fargs;
+    float *d_fw = nullptr;
+    CUtensorMap fmapX;
+    const float *f_last_x = nullptr;
+    int fgrid = 0, num_sms = 148;
+    bool tc_core = false;          // stage 2 uses the band-resident core kernel
+    tdc::TcCoreArgs core_args;
     float *d_tc_w = nullptr;       // Bt1 | Bt2 | Bt3 | bias
     float *d_xg = nullptr;         // X' phase grids (zero borders)
     float *d_z = nullptr;          // Z compact
@@ -139,6 +149,31 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     const int R1 = round_up(D1s, BN1), R2 = round_up(D2s, BN2), R3 = round_up(N, BN3);
     const int KK = K * K;
 
+    // Stage-2 kernel choice: band-resident core kernel if its two A slots fit.
+    const int maxoff = ((K - 1) / s) * Wq + (K - 1) / s;
+    const int band_rows = round_up(128 + maxoff, 8);
+    int phase_of[tdc::kMaxTaps], nphase = 0, phase_src[tdc::kMaxTaps];
+    {
+        int idx_of[tdc::kMaxTaps];
+        for (int i = 0; i < s * s && i < tdc::kMaxTaps; ++i) idx_of[i] = -1;
+        for (int r = 0; r < K; ++r)
+            for (int t = 0; t < K; ++t) {
+                const int ph = (r % s) * s + (t % s);
+                if (idx_of[ph] < 0) {
+                    idx_of[ph] = nphase;
+                    phase_src[nphase++] = ph;
+                }
+                phase_of[r * K + t] = idx_of[ph];
+            }
+    }
+    int core_stages = 4;
+    while (core_stages > 2 &&
+           tdc::tc_core_smem_bytes(BN2, nphase, band_rows, core_stages) > p->max_smem)
+        --core_stages;
+    p->tc_core = tdc::tc_core_smem_bytes(BN2, nphase, band_rows, core_stages) <= p->max_smem;
+    const int k2chunks = D1s / 32, nt2 = R2 / BN2;
+    const long long rows_total = (long long)s * s * phase_rows + band_rows + 128;
+
     // ---- a0: K-major weight panels, zero padded (CRSN idea) ----
     const size_t n1 = (size_t)R1 * Cs, n2 = (size_t)KK * R2 * D1s, n3 = (size_t)R3 * D2s,
                  nb = (size_t)round_up(N, 4);
@@ -149,9 +184,18 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     for (int r = 0; r < K; ++r)
         for (int t = 0; t < K; ++t)
             for (int q = 0; q < D2; ++q)
-                for (int a = 0; a < D1; ++a)
-                    b2[((size_t)(r * K + t) * R2 + q) * D1s + a] =
-                        core[(((size_t)q * D1 + a) * K + r) * K + t];
+                for (int a = 0; a < D1; ++a) {
+                    const float v = core[(((size_t)q * D1 + a) * K + r) * K + t];
+                    const int tap = r * K + t;
+                    if (p->tc_core) {
+                        // blocked [tap][kc][ntile][kg8][BN][4] no-swizzle K-major chunks
+                        const int kc = a / 32, kg = (a % 32) / 4, e = a % 4;
+                        const int ntl = q / BN2, n = q % BN2;
+                        b2[((((size_t)(tap * k2chunks + kc) * nt2 + ntl) * 8 + kg) * BN2 + n) * 4 + e] = v;
+                    } else {
+                        b2[((size_t)tap * R2 + q) * D1s + a] = v;
+                    }
+                }
     for (int n = 0; n < N; ++n)
         for (int q = 0; q < D2; ++q) b3[(size_t)n * D2s + q] = u_out[(size_t)n * D2 + q];
     if (bias)
@@ -163,7 +207,7 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     p->weight_bytes += h.size() * sizeof(float);
 
     // ---- workspaces: X' phase grids (zero borders, never written there) and Z ----
-    const size_t xg_elems = (size_t)s * s * phase_rows * D1s;
+    const size_t xg_elems = p->tc_core ? (size_t)rows_total * D1s : (size_t)s * s * phase_rows * D1s;
     const size_t z_elems = (size_t)M3 * D2s;
     e = cudaMalloc(&p->d_xg, xg_elems * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&p->d_z, z_elems * sizeof(float));
@@ -178,19 +222,34 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
         g.phase_rows = phase_rows;
     };
     const float *dB1 = p->d_tc_w, *dB2 = dB1 + n1, *dB3 = dB2 + n2, *dbias = dB3 + n3;
-    // stage 1: A = X (per forward), Bt1; out = X' grid
+    // stage 1: A = X (per forward), Bt1; out = X' grid (planar for the core kernel)
     {
         auto &st = p->tc[0];
         base_args(st.args);
         st.args.M = (int)M1; st.args.Nn = D1s; st.args.kchunks = Cs / 32; st.args.taps = 1;
         st.args.BN = BN1; st.args.out = p->d_xg; st.args.ldo = D1s; st.args.remap = 1;
+        st.args.planar_stride = p->tc_core ? rows_total * 4 : 0;
         st.args.stages = tdc::tc_pick_stages(BN1, Cs / 32, p->max_smem);
         st.grid_n = R1 / BN1;
         if (!tdc::make_tma_2d(&st.mapB, dB1, R1, Cs, Cs, BN1))
             return fail(TDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (stage-1 weights)");
     }
-    // stage 2: A = X' grid, Bt2 (K*K taps); out = Z compact
-    {
+    // stage 2
+    if (p->tc_core) {
+        tdc::TcCoreArgs &g = p->core_args;
+        std::memset(&g, 0, sizeof g);
+        g.xg = p->d_xg; g.plane_stride = rows_total * 4; g.w = dB2; g.z = p->d_z;
+        g.ldz = D2s; g.Nn = D2s; g.M = (int)M2; g.kchunks = k2chunks; g.taps = KK;
+        g.ntiles = nt2; g.BN = BN2; g.nphase = nphase; g.band_rows = band_rows;
+        g.b_stages = core_stages; g.phase_rows = phase_rows;
+        for (int r = 0; r < K; ++r)
+            for (int t = 0; t < K; ++t) {
+                g.tap_phase[r * K + t] = phase_of[r * K + t];
+                g.tap_off[r * K + t] = (r / s) * Wq + (t / s);
+            }
+        for (int i = 0; i < nphase; ++i) g.phase_src[i] = phase_src[i];
+        g.Hq = Hq; g.Wq = Wq; g.Ho = Ho; g.Wo = Wo;
+    } else {
         auto &st = p->tc[1];
         base_args(st.args);
         st.args.M = (int)M2; st.args.Nn = D2s; st.args.kchunks = D1s / 32; st.args.taps = KK;
@@ -223,6 +282,171 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     return TDC_OK;
 }
 
+
+// Plan the fused single-kernel variant; returns TDC_OK and sets variant 3 if the
+// layer fits the kernel's shared-memory / tensor-memory budget, otherwise leaves
+// the plan untouched (caller falls back to the three-launch variant).
+tdc_status plan_fused(tdc_conv_plan_s *p, const float *core, const float *u_in, const float *u_out,
+                      const float *bias, bool *used) {
+    *used = false;
+    const tdc_conv_desc &d = p->desc;
+    const int C = d.c_in, N = d.c_out, D1 = d.rank_in, D2 = d.rank_out, K = d.kernel;
+    const int s = d.stride, pad = d.pad, H = d.height, W = d.width;
+    const int Ho = p->dims.Ho, Wo = p->dims.Wo;
+    const int D1s = round_up(D1, 32), D2s = round_up(D2, 32);
+    if (C % 4 || D1s > 256 || D2s > 256 || K * K > tdc::kMaxTaps || s * s > tdc::kMaxTaps)
+        return TDC_OK;
+    const int Wp = W + 2 * pad, Wq = div_up(Wp, s);
+    if (Wp > 256 || Wq > 128) return TDC_OK;
+    const int kc1 = div_up(C, 32);
+    int Nh = N < 256 ? round_up(N, 16) : 256;
+    const int nhalves = div_up(N, Nh);
+    // compact phases used by the taps
+    int phase_idx[tdc::kMaxTaps], nph = 0;
+    for (int i = 0; i < tdc::kMaxTaps; ++i) phase_idx[i] = -1;
+    for (int r = 0; r < K; ++r)
+        for (int t = 0; t < K; ++t) {
+            const int ph = (r % s) * s + (t % s);
+            if (phase_idx[ph] < 0) phase_idx[ph] = nph++;
+        }
+    const int maxoff = ((K - 1) / s) * Wq + (K - 1) / s;
+
+    tdc::FusedArgs best;
+    bool found = false;
+    const int rmax = std::min(Ho, 128 / Wq);
+    for (int R = rmax; R >= 1; --R) {
+        tdc::FusedArgs g;
+        std::memset(&g, 0, sizeof g);
+        g.B = d.batch; g.H = H; g.W = W; g.C = C; g.N = N; g.Ho = Ho; g.Wo = Wo; g.K = K;
+        g.KK = K * K; g.s = s; g.p = pad; g.R = R; g.Rin = s * (R - 1) + K; g.Wp = Wp; g.Wq = Wq;
+        if (g.Rin > 256) continue;
+        g.tiles_per_img = div_up(Ho, R);
+        g.num_tiles = d.batch * g.tiles_per_img;
+        g.nblk1 = div_up(g.Rin * Wp, 128);
+        g.c_chunks = kc1;
+        g.D1s = D1s; g.D2s = D2s; g.Nh = Nh; g.nhalves = nhalves;
+        g.nph = nph;
+        g.PR = round_up(div_up(g.Rin, s) * Wq, 8);
+        g.TR = s == 1 ? std::max(g.Rin * Wp, 128 + maxoff)
+                      : (nph - 1) * g.PR + std::max(g.PR, 128 + maxoff);
+        g.TR = round_up(g.TR, 8);
+        // TMEM: acc1 [nblk1][P1][D1s] and acc2 [P2][D2s] share columns (acc2 is written
+        // only after epilogue 1 drained acc1); acc3 [nbuf3][P3][Nh] is separate.
+        auto tmem_need = [&](int P1, int P2, int P3, int nb) {
+            return std::max(g.nblk1 * P1 * D1s, P2 * D2s) + nb * P3 * Nh;
+        };
+        // Independent accumulator chains measured to give no gain (tcgen05.mma
+        // issue cost is ~130-150 cycles per instruction regardless, see
+        // DESIGN.md "tensor-core cost model"), so one chain per stage.
+        g.P1 = 1;
+        g.P2 = 1;
+        g.P3 = 1;
+        g.nbuf3 = 2;
+        while (tmem_need(g.P1, g.P2, g.P3, g.nbuf3) > 512) {
+            if (g.P3 > 1) --g.P3;
+            else if (g.P1 > 1) --g.P1;
+            else if (g.P2 > 2) g.P2 /= 2;
+            else if (g.nbuf3 > 1) --g.nbuf3;
+            else if (g.P2 > 1) --g.P2;
+            else break;
+        }
+        const int cols = tmem_need(g.P1, g.P2, g.P3, g.nbuf3);
+        if (cols > 512) continue;
+        g.acc3_col = std::max(g.nblk1 * g.P1 * D1s, g.P2 * D2s);
+        g.tmem_cols = 32;
+        while (g.tmem_cols < cols) g.tmem_cols *= 2;
+        // ring depths: as deep as shared memory allows (X: up to two tiles ahead)
+        g.WS = 4;
+        g.XS = std::max(2, std::min(2 * kc1, 8));
+        while (g.XS > 2 && tdc::fused_smem_bytes(g) > p->max_smem) --g.XS;
+        if (tdc::fused_smem_bytes(g) > p->max_smem) {
+            g.WS = 2;
+            if (tdc::fused_smem_bytes(g) > p->max_smem) continue;
+        }
+        while (g.WS < 8) {
+            ++g.WS;
+            if (tdc::fused_smem_bytes(g) > p->max_smem) { --g.WS; break; }
+        }
+        if (!found || (best.num_tiles < p->num_sms && g.num_tiles > best.num_tiles)) {
+            best = g;
+            found = true;
+        }
+        if (best.num_tiles >= p->num_sms) break;
+    }
+    if (!found) return TDC_OK;
+    tdc::FusedArgs &g = best;
+    // The kernel streams every weight chunk once per tile (from L2).  When that
+    // outweighs the tile's own activation traffic (small images, large ranks),
+    // the three-launch variant -- whose GEMM tiles reuse weights across more
+    // rows -- is the better choice.
+    {
+        const double wbytes = (double)(kc1 * D1s + (D1s / 32) * K * K * D2s +
+                                       g.nhalves * (D2s / 32) * Nh) * 128.0;
+        const double abytes = ((double)g.Rin * W * C + (double)g.R * Wo * N) * 4.0;
+        if (wbytes > 2.5 * abytes && !getenv("TDC_FORCE_FUSED")) return TDC_OK;
+    }
+    for (int r = 0; r < K; ++r)
+        for (int t = 0; t < K; ++t) {
+            g.tap_phase[r * K + t] = phase_idx[(r % s) * s + (t % s)];
+            g.tap_off[r * K + t] = (r / s) * Wq + (t / s);
+        }
+    for (int i = 0; i < tdc::kMaxTaps; ++i) g.phase_idx[i] = phase_idx[i];
+
+    // ---- a0: blocked weight chunks [8][rows][4] in consumption order ----
+    const int KK = K * K, kc2 = D1s / 32, kc3 = D2s / 32;
+    const size_t n1 = (size_t)kc1 * D1s * 32, n2 = (size_t)kc2 * KK * D2s * 32,
+                 n3 = (size_t)nhalves * kc3 * Nh * 32, nb = (size_t)round_up(N, 4);
+    std::vector<float> h(n1 + n2 + n3 + nb, 0.f);
+    float *w1 = h.data(), *w2 = w1 + n1, *w3 = w2 + n2, *hb = w3 + n3;
+    for (int c = 0; c < C; ++c)
+        for (int a = 0; a < D1; ++a) {
+            const int kc = c / 32, kg = (c % 32) / 4, e = c % 4;
+            w1[(((size_t)kc * 8 + kg) * D1s + a) * 4 + e] = u_in[(size_t)c * D1 + a];
+        }
+    for (int q = 0; q < D2; ++q)
+        for (int a = 0; a < D1; ++a)
+            for (int r = 0; r < K; ++r)
+                for (int t = 0; t < K; ++t) {
+                    const int kc = a / 32, kg = (a % 32) / 4, e = a % 4, tap = r * K + t;
+                    w2[((((size_t)kc * KK + tap) * 8 + kg) * D2s + q) * 4 + e] =
+                        core[(((size_t)q * D1 + a) * K + r) * K + t];
+                }
+    for (int n = 0; n < N; ++n)
+        for (int q = 0; q < D2; ++q) {
+            const int hh = n / Nh, nn = n % Nh, kc = q / 32, kg = (q % 32) / 4, e = q % 4;
+            w3[((((size_t)hh * kc3 + kc) * 8 + kg) * Nh + nn) * 4 + e] = u_out[(size_t)n * D2 + q];
+        }
+    if (bias)
+        for (int n = 0; n < N; ++n) hb[n] = bias[n];
+    cudaError_t e = cudaMalloc(&p->d_fw, h.size() * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(fused weights)");
+    e = cudaMemcpy(p->d_fw, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(fused weights)");
+    p->weight_bytes += h.size() * sizeof(float);
+    g.w = p->d_fw;
+    g.bias = bias ? p->d_fw + n1 + n2 + n3 : nullptr;
+    p->fargs = g;
+    p->variant = 3;
+    *used = true;
+    return TDC_OK;
+}
+
+tdc_status forward_fused(tdc_conv_plan_s *p, const float *x, float *y, int batch, cudaStream_t st) {
+    if (x != p->f_last_x) {
+        if (!tdc::fused_make_x_map(&p->fmapX, x, p->fargs))
+            return fail(TDC_ERR_INVALID_ARGUMENT,
+                        "cuTensorMapEncodeTiled rejected x (needs a 16-byte aligned pointer)");
+        p->f_last_x = x;
+    }
+    tdc::FusedArgs g = p->fargs;
+    g.y = y;
+    g.num_tiles = batch * g.tiles_per_img;
+    const int grid = std::min(g.num_tiles, p->num_sms);
+    cudaError_t e = tdc::fused_launch(p->fmapX, g, grid, st);
+    if (e != cudaSuccess) return cuda_fail(e, "fused tcgen05 kernel launch");
+    return TDC_OK;
+}
+
 tdc_status forward_tc(tdc_conv_plan_s *p, const float *x, float *y, int batch, cudaStream_t st) {
     const tdc::LayerDims &d = p->dims;
     auto &s1 = p->tc[0], &s2 = p->tc[1], &s3 = p->tc[2];
@@ -234,13 +458,24 @@ tdc_status forward_tc(tdc_conv_plan_s *p, const float *x, float *y, int batch, c
     }
     tdc::TcGemmArgs a1 = s1.args, a2 = s2.args, a3 = s3.args;
     a1.M = batch * d.H * d.W;
-    const int Hq = a2.Hq, Wq = a2.Wq;
+    const int Hq = a1.Hq, Wq = a1.Wq;  // stage-1 args always carry the grid geometry
     a2.M = batch * Hq * Wq;
     a3.M = batch * d.Ho * d.Wo;
     a3.out = y;
     cudaError_t e = tdc::tc_gemm_launch(s1.mapA, s1.mapB, a1, s1.grid_n, st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-1 launch");
-    e = tdc::tc_gemm_launch(s2.mapA, s2.mapB, a2, s2.grid_n, st);
+    if (p->tc_core) {
+        tdc::TcCoreArgs c = p->core_args;
+        c.M = a2.M;
+        e = tdc::tc_core_launch(c, st);
+        if (e != cudaSuccess)
+            return fail(TDC_ERR_CUDA, "tcgen05 core launch: %s (M=%d ntiles=%d BN=%d smem=%d nphase=%d band=%d stages=%d)",
+                        cudaGetErrorString(e), c.M, c.ntiles, c.BN,
+                        tdc::tc_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.b_stages), c.nphase,
+                        c.band_rows, c.b_stages);
+    } else {
+        e = tdc::tc_gemm_launch(s2.mapA, s2.mapB, a2, s2.grid_n, st);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-2 launch");
     e = tdc::tc_gemm_launch(s3.mapA, s3.mapB, a3, s3.grid_n, st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-3 launch");
@@ -363,7 +598,16 @@ tdc_status tdc_conv_plan(const tdc_conv_desc *desc, const float *core, const flo
     p->variant = 1;
     // Tensor-core variant: TMA needs 16-byte row pitches (C % 4 == 0) and at most
     // kMaxTaps taps; otherwise the plan keeps the (more accurate) fp32 variant.
-    if (d.math == TDC_MATH_TF32 && C % 4 == 0 && K * K <= tdc::kMaxTaps) {
+    p->num_sms = prop.multiProcessorCount;
+    bool fused = false;
+    if (d.math == TDC_MATH_TF32 && !getenv("TDC_DISABLE_FUSED")) {
+        s = plan_fused(p, core, u_in, u_out, bias, &fused);
+        if (s != TDC_OK) {
+            tdc_conv_plan_destroy(p);
+            return s;
+        }
+    }
+    if (!fused && d.math == TDC_MATH_TF32 && C % 4 == 0 && K * K <= tdc::kMaxTaps) {
         s = plan_tc(p, core, u_in, u_out, bias);
         if (s != TDC_OK) {
             tdc_conv_plan_destroy(p);
@@ -392,9 +636,10 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
     info->h_out = p->dims.Ho;
     info->w_out = p->dims.Wo;
     info->variant = p->variant;
-    const bool tc = p->variant == 2;
+    const bool tc = p->variant == 2, fz = p->variant == 3;
     std::snprintf(info->variant_name, sizeof info->variant_name, "%s",
-                  tc ? "tc3_tf32" : "fused_simt_fp32");
+                  fz ? "fused_tc_tf32"
+                     : tc ? (p->tc_core ? "tc3_tf32_band" : "tc3_tf32") : "fused_simt_fp32");
     info->launches_per_forward = (tc ? 3 : 1) + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
     info->concurrent_forward = (p->desc.layout == TDC_LAYOUT_NHWC && !tc) ? 1 : 0;
     info->tile_h = p->simt_tile.oth;
@@ -409,6 +654,14 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
         info->threads_per_cta = 192;
         info->smem_bytes_per_cta = tdc::tc_smem_bytes(p->tc[1].args.BN, p->tc[1].args.stages);
         info->ctas_per_image = 0;
+    }
+    if (fz) {
+        info->tile_h = p->fargs.R;
+        info->tile_w = p->fargs.Wo;
+        info->threads_per_cta = 384;
+        info->smem_bytes_per_cta = tdc::fused_smem_bytes(p->fargs);
+        info->ctas_per_image = p->fargs.tiles_per_img;  // tiles per image (persistent grid)
+        info->concurrent_forward = p->desc.layout == TDC_LAYOUT_NHWC ? 1 : 0;
     }
     info->weight_bytes = (int64_t)p->weight_bytes;
     return TDC_OK;
@@ -432,6 +685,7 @@ tdc_status tdc_conv_forward(tdc_conv_plan_t p, const float *x, float *y, int32_t
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
     if (p->desc.layout == TDC_LAYOUT_NHWC) {
+        if (p->variant == 3) return forward_fused(p, x, y, batch, st);
         if (p->variant == 2) return forward_tc(p, x, y, batch, st);
         e = tdc::simt_fused_launch(d, p->simt, p->simt_tile, x, y, batch, st);
         if (e != cudaSuccess) return cuda_fail(e, "fused SIMT kernel launch");
@@ -439,7 +693,10 @@ tdc_status tdc_conv_forward(tdc_conv_plan_t p, const float *x, float *y, int32_t
     }
     e = tdc::nchw_to_nhwc(x, p->d_ws_in, batch, d.C, d.H, d.W, st);
     if (e != cudaSuccess) return cuda_fail(e, "NCHW->NHWC launch");
-    if (p->variant == 2) {
+    if (p->variant == 3) {
+        tdc_status s = forward_fused(p, p->d_ws_in, p->d_ws_out, batch, st);
+        if (s != TDC_OK) return s;
+    } else if (p->variant == 2) {
         tdc_status s = forward_tc(p, p->d_ws_in, p->d_ws_out, batch, st);
         if (s != TDC_OK) return s;
     } else {
@@ -492,6 +749,7 @@ tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t p) {
     cudaFree(p->d_stage_x);
     cudaFree(p->d_stage_y);
     cudaFree(p->d_tc_w);
+    cudaFree(p->d_fw);
     cudaFree(p->d_xg);
     cudaFree(p->d_z);
     delete p;

@@ -12,7 +12,7 @@ import os
 from dataclasses import dataclass
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtdc.so")
+LIB_PATH = os.environ.get("TDC_LIB") or os.path.join(HERE, "libtdc.so")
 
 TDC_OK, TDC_ERR_INVALID_ARGUMENT, TDC_ERR_UNSUPPORTED, TDC_ERR_CUDA, \
     TDC_ERR_OUT_OF_MEMORY, TDC_ERR_INTERNAL = range(6)

@@ -124,8 +124,21 @@ def test_tensor_core_variant_is_selected(env, shape, count):
     torch, tdc = env
     d = synth.make_layer(shape)
     plan = tdc.ConvPlan(shape.with_batch(32), d, math=tdc.TDC_MATH_TF32)
-    assert plan.info().variant_name.startswith("tc")
+    assert plan.info().variant_name in ("fused_tc_tf32", "tc3_tf32_band", "tc3_tf32")
     plan.close()
+
+
+@pytest.mark.parametrize("shape", [s for s, _ in synth.R18_SHAPES] + [
+    LayerShape(3, 64, 40, 13, 11, 24, 20, 3, 1, 1),
+    LayerShape(2, 32, 48, 15, 9, 16, 32, 3, 2, 1),
+], ids=lambda s: s.name or f"{s.C}_{s.N}_{s.H}x{s.W}_s{s.stride}")
+def test_three_launch_tensor_core_path(env, shape, monkeypatch):
+    """The unfused tcgen05 path (forced with TDC_DISABLE_FUSED) on its own."""
+    monkeypatch.setenv("TDC_DISABLE_FUSED", "1")
+    d = synth.make_layer(shape.with_batch(2), seed=13, bias=True)
+    got, info = run_layer(env, shape.with_batch(2), d, "nhwc", "tf32")
+    assert info.variant_name.startswith("tc3")
+    assert err(got, ref_of(shape.with_batch(2), d)) <= TOL["tf32"]
 
 
 @pytest.mark.parametrize("math", MATHS)
