@@ -47,6 +47,9 @@ struct TcGemmArgs {
     int H, W, s, p, Hq, Wq, Ho, Wo;
     long long phase_rows;
     long long planar_stride;  // >0: epilogue writes planar [col/4][row][4] with this plane stride (floats)
+    int split;        // 1: 3xTF32 (hi*hi + hi*lo + lo*hi), fp32-grade accuracy
+    int a_convert;    // split only: 1 = A lo computed in-kernel from A (user input); 0 = loaded
+    float *out_lo;    // split only: epilogue also writes the lo part of the output (next stage's A lo)
 };
 
 // Stage-2 core convolution with a shared-memory-resident X' band (tkd_tc.cu):
@@ -63,14 +66,19 @@ struct TcCoreArgs {
     int tap_phase[kMaxTaps], tap_off[kMaxTaps];
     int phase_src[kMaxTaps];   // global phase index of compact phase i
     int Hq, Wq, Ho, Wo;
+    int split;                 // 3xTF32
+    const float *xg_lo;        // split: X' lo planes
+    const float *w_lo;         // split: blocked core weights, lo parts
+    float *z_lo;               // split: Z lo (next stage's A lo)
 };
-int tc_core_smem_bytes(int BN, int nphase, int band_rows, int b_stages);
+int tc_core_smem_bytes(int BN, int nphase, int band_rows, int b_stages, int split);
 cudaError_t tc_core_launch(const TcCoreArgs &g, cudaStream_t st);
-int tc_smem_bytes(int BN, int stages);
-int tc_pick_stages(int BN, int iters, int max_smem);
+int tc_smem_bytes(int BN, int stages, int split);
+int tc_pick_stages(int BN, int iters, int max_smem, int split);
 bool make_tma_2d(CUtensorMap *map, const float *base, long long rows, int k_extent, int pitch,
                  int box_rows);
-cudaError_t tc_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapB, const TcGemmArgs &g,
+cudaError_t tc_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo,
+                           const CUtensorMap &mapB, const CUtensorMap &mapBlo, const TcGemmArgs &g,
                            int grid_n, cudaStream_t st);
 
 // ---- fused single-kernel TKD layer (tkd_fused.cu) ----

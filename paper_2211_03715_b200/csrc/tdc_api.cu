@@ -100,7 +100,7 @@ struct tdc_conv_plan_s {
     // tensor-core variant (variant 2): three tcgen05 GEMM-with-taps launches
     struct TcStage {
         tdc::TcGemmArgs args;
-        CUtensorMap mapA, mapB;
+        CUtensorMap mapA, mapB, mapAlo, mapBlo;
         int grid_n = 1;
     } tc[3];
     // fused single-kernel variant (variant 3)
@@ -110,6 +110,7 @@ struct tdc_conv_plan_s {
     const float *f_last_x = nullptr;
     int fgrid = 0, num_sms = 148;
     bool tc_core = false;          // stage 2 uses the band-resident core kernel
+    bool split = false;            // 3xTF32
     tdc::TcCoreArgs core_args;
     float *d_tc_w = nullptr;       // Bt1 | Bt2 | Bt3 | bias
     float *d_xg = nullptr;         // X' phase grids (zero borders)
@@ -130,9 +131,20 @@ int pick_bn(int nn, long long mtiles) {
 
 int div_up(int a, int b) { return (a + b - 1) / b; }
 
-// Plan the tcgen05 variant: weight re-layout (a0), workspaces, tensor maps.
+// Round-to-nearest (ties away) to tf32: clear the low 13 mantissa bits.
+float tf32_round_host(float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & ~0x1fffu;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+}
+
+// Plan the tcgen05 3-launch variant: weight re-layout (a0), workspaces, tensor
+// maps.  split = 3xTF32 (hi/lo operands everywhere).
 tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, const float *u_out,
-                   const float *bias) {
+                   const float *bias, bool split) {
     const tdc_conv_desc &d = p->desc;
     const int C = d.c_in, N = d.c_out, D1 = d.rank_in, D2 = d.rank_out, K = d.kernel;
     const int s = d.stride, pad = d.pad, H = d.height, W = d.width;
@@ -143,6 +155,7 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     const long long M1 = (long long)Bm * H * W, M2 = phase_rows, M3 = (long long)Bm * Ho * Wo;
     if (M1 > (1LL << 31) - 256 || M2 * s * s > (1LL << 31) - 256)
         return fail(TDC_ERR_UNSUPPORTED, "batch too large for the tensor-core variant");
+    const int sp = split ? 1 : 0;
     const int BN1 = pick_bn(D1s, div_up((int)M1, 128));
     const int BN2 = pick_bn(D2s, div_up((int)M2, 128));
     const int BN3 = pick_bn(N, div_up((int)M3, 128));
@@ -155,7 +168,7 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     int phase_of[tdc::kMaxTaps], nphase = 0, phase_src[tdc::kMaxTaps];
     {
         int idx_of[tdc::kMaxTaps];
-        for (int i = 0; i < s * s && i < tdc::kMaxTaps; ++i) idx_of[i] = -1;
+        for (int i = 0; i < tdc::kMaxTaps; ++i) idx_of[i] = -1;
         for (int r = 0; r < K; ++r)
             for (int t = 0; t < K; ++t) {
                 const int ph = (r % s) * s + (t % s);
@@ -168,17 +181,19 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     }
     int core_stages = 4;
     while (core_stages > 2 &&
-           tdc::tc_core_smem_bytes(BN2, nphase, band_rows, core_stages) > p->max_smem)
+           tdc::tc_core_smem_bytes(BN2, nphase, band_rows, core_stages, sp) > p->max_smem)
         --core_stages;
-    p->tc_core = tdc::tc_core_smem_bytes(BN2, nphase, band_rows, core_stages) <= p->max_smem;
+    p->tc_core = tdc::tc_core_smem_bytes(BN2, nphase, band_rows, core_stages, sp) <= p->max_smem;
     const int k2chunks = D1s / 32, nt2 = R2 / BN2;
     const long long rows_total = (long long)s * s * phase_rows + band_rows + 128;
 
     // ---- a0: K-major weight panels, zero padded (CRSN idea) ----
     const size_t n1 = (size_t)R1 * Cs, n2 = (size_t)KK * R2 * D1s, n3 = (size_t)R3 * D2s,
                  nb = (size_t)round_up(N, 4);
-    std::vector<float> h(n1 + n2 + n3 + nb, 0.f);
-    float *b1 = h.data(), *b2 = b1 + n1, *b3 = b2 + n2, *hb = b3 + n3;
+    const size_t nw = n1 + n2 + n3;  // one copy (hi or plain)
+    std::vector<float> h(nw * (split ? 2 : 1) + nb, 0.f);
+    float *b1 = h.data(), *b2 = b1 + n1, *b3 = b2 + n2;
+    float *hb = h.data() + nw * (split ? 2 : 1);
     for (int a = 0; a < D1; ++a)
         for (int c = 0; c < C; ++c) b1[(size_t)a * Cs + c] = u_in[(size_t)c * D1 + a];
     for (int r = 0; r < K; ++r)
@@ -198,6 +213,12 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
                 }
     for (int n = 0; n < N; ++n)
         for (int q = 0; q < D2; ++q) b3[(size_t)n * D2s + q] = u_out[(size_t)n * D2 + q];
+    if (split)  // hi = RN-to-tf32 (low 13 mantissa bits cleared), lo = w - hi (exact)
+        for (size_t i = 0; i < nw; ++i) {
+            const float hi = tf32_round_host(h[i]);
+            h[nw + i] = h[i] - hi;
+            h[i] = hi;
+        }
     if (bias)
         for (int n = 0; n < N; ++n) hb[n] = bias[n];
     cudaError_t e = cudaMalloc(&p->d_tc_w, h.size() * sizeof(float));
@@ -209,19 +230,27 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     // ---- workspaces: X' phase grids (zero borders, never written there) and Z ----
     const size_t xg_elems = p->tc_core ? (size_t)rows_total * D1s : (size_t)s * s * phase_rows * D1s;
     const size_t z_elems = (size_t)M3 * D2s;
-    e = cudaMalloc(&p->d_xg, xg_elems * sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_z, z_elems * sizeof(float));
+    const int f = split ? 2 : 1;
+    e = cudaMalloc(&p->d_xg, f * xg_elems * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_z, f * z_elems * sizeof(float));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(tc workspace)");
-    e = cudaMemset(p->d_xg, 0, xg_elems * sizeof(float));
+    e = cudaMemset(p->d_xg, 0, f * xg_elems * sizeof(float));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(X' grid)");
-    p->tc_ws_bytes = (xg_elems + z_elems) * sizeof(float);
+    p->tc_ws_bytes = f * (xg_elems + z_elems) * sizeof(float);
+    float *xg_lo = split ? p->d_xg + xg_elems : nullptr;
+    float *z_lo = split ? p->d_z + z_elems : nullptr;
 
     auto base_args = [&](tdc::TcGemmArgs &g) {
         std::memset(&g, 0, sizeof g);
         g.H = H; g.W = W; g.s = s; g.p = pad; g.Hq = Hq; g.Wq = Wq; g.Ho = Ho; g.Wo = Wo;
         g.phase_rows = phase_rows;
+        g.split = sp;
     };
-    const float *dB1 = p->d_tc_w, *dB2 = dB1 + n1, *dB3 = dB2 + n2, *dbias = dB3 + n3;
+    const float *dB1 = p->d_tc_w, *dB2 = dB1 + n1, *dB3 = dB2 + n2;
+    const float *dB1lo = split ? dB1 + nw : nullptr, *dB2lo = split ? dB2 + nw : nullptr,
+                *dB3lo = split ? dB3 + nw : nullptr;
+    const float *dbias = p->d_tc_w + nw * f;
+    const char *enc_err = "cuTensorMapEncodeTiled failed";
     // stage 1: A = X (per forward), Bt1; out = X' grid (planar for the core kernel)
     {
         auto &st = p->tc[0];
@@ -229,10 +258,15 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
         st.args.M = (int)M1; st.args.Nn = D1s; st.args.kchunks = Cs / 32; st.args.taps = 1;
         st.args.BN = BN1; st.args.out = p->d_xg; st.args.ldo = D1s; st.args.remap = 1;
         st.args.planar_stride = p->tc_core ? rows_total * 4 : 0;
-        st.args.stages = tdc::tc_pick_stages(BN1, Cs / 32, p->max_smem);
+        st.args.a_convert = 1;
+        st.args.out_lo = xg_lo;
+        st.args.stages = tdc::tc_pick_stages(BN1, Cs / 32, p->max_smem, sp);
         st.grid_n = R1 / BN1;
-        if (!tdc::make_tma_2d(&st.mapB, dB1, R1, Cs, Cs, BN1))
-            return fail(TDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (stage-1 weights)");
+        if (!tdc::make_tma_2d(&st.mapB, dB1, R1, Cs, Cs, BN1) ||
+            (split && !tdc::make_tma_2d(&st.mapBlo, dB1lo, R1, Cs, Cs, BN1)))
+            return fail(TDC_ERR_CUDA, "%s (stage-1 weights)", enc_err);
+        st.mapAlo = st.mapB;  // unused (converter computes A lo)
+        if (!split) st.mapBlo = st.mapB;
     }
     // stage 2
     if (p->tc_core) {
@@ -249,22 +283,32 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
             }
         for (int i = 0; i < nphase; ++i) g.phase_src[i] = phase_src[i];
         g.Hq = Hq; g.Wq = Wq; g.Ho = Ho; g.Wo = Wo;
+        g.split = sp; g.xg_lo = xg_lo; g.w_lo = dB2lo; g.z_lo = z_lo;
     } else {
         auto &st = p->tc[1];
         base_args(st.args);
         st.args.M = (int)M2; st.args.Nn = D2s; st.args.kchunks = D1s / 32; st.args.taps = KK;
         st.args.BN = BN2; st.args.out = p->d_z; st.args.ldo = D2s; st.args.remap = 2;
+        st.args.out_lo = z_lo;
         for (int r = 0; r < K; ++r)
             for (int t = 0; t < K; ++t) {
                 const int ph = (r % s) * s + (t % s);
                 st.args.a_off[r * K + t] = (int)(ph * phase_rows + (r / s) * Wq + (t / s));
                 st.args.b_off[r * K + t] = (r * K + t) * R2;
             }
-        st.args.stages = tdc::tc_pick_stages(BN2, KK * D1s / 32, p->max_smem);
+        st.args.stages = tdc::tc_pick_stages(BN2, KK * D1s / 32, p->max_smem, sp);
         st.grid_n = R2 / BN2;
         if (!tdc::make_tma_2d(&st.mapA, p->d_xg, (long long)s * s * phase_rows, D1s, D1s, 128) ||
             !tdc::make_tma_2d(&st.mapB, dB2, (long long)KK * R2, D1s, D1s, BN2))
-            return fail(TDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (stage 2)");
+            return fail(TDC_ERR_CUDA, "%s (stage 2)", enc_err);
+        if (split) {
+            if (!tdc::make_tma_2d(&st.mapAlo, xg_lo, (long long)s * s * phase_rows, D1s, D1s, 128) ||
+                !tdc::make_tma_2d(&st.mapBlo, dB2lo, (long long)KK * R2, D1s, D1s, BN2))
+                return fail(TDC_ERR_CUDA, "%s (stage 2 lo)", enc_err);
+        } else {
+            st.mapAlo = st.mapA;
+            st.mapBlo = st.mapB;
+        }
     }
     // stage 3: A = Z, Bt3 = U_out; out = Y (per forward), bias
     {
@@ -272,16 +316,24 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
         base_args(st.args);
         st.args.M = (int)M3; st.args.Nn = N; st.args.kchunks = D2s / 32; st.args.taps = 1;
         st.args.BN = BN3; st.args.ldo = N; st.args.remap = 0; st.args.bias = bias ? dbias : nullptr;
-        st.args.stages = tdc::tc_pick_stages(BN3, D2s / 32, p->max_smem);
+        st.args.stages = tdc::tc_pick_stages(BN3, D2s / 32, p->max_smem, sp);
         st.grid_n = R3 / BN3;
         if (!tdc::make_tma_2d(&st.mapA, p->d_z, M3, D2s, D2s, 128) ||
             !tdc::make_tma_2d(&st.mapB, dB3, R3, D2s, D2s, BN3))
-            return fail(TDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (stage 3)");
+            return fail(TDC_ERR_CUDA, "%s (stage 3)", enc_err);
+        if (split) {
+            if (!tdc::make_tma_2d(&st.mapAlo, z_lo, M3, D2s, D2s, 128) ||
+                !tdc::make_tma_2d(&st.mapBlo, dB3lo, R3, D2s, D2s, BN3))
+                return fail(TDC_ERR_CUDA, "%s (stage 3 lo)", enc_err);
+        } else {
+            st.mapAlo = st.mapA;
+            st.mapBlo = st.mapB;
+        }
     }
     p->variant = 2;
+    p->split = split;
     return TDC_OK;
 }
-
 
 // Plan the fused single-kernel variant; returns TDC_OK and sets variant 3 if the
 // layer fits the kernel's shared-memory / tensor-memory budget, otherwise leaves
@@ -462,7 +514,8 @@ tdc_status forward_tc(tdc_conv_plan_s *p, const float *x, float *y, int batch, c
     a2.M = batch * Hq * Wq;
     a3.M = batch * d.Ho * d.Wo;
     a3.out = y;
-    cudaError_t e = tdc::tc_gemm_launch(s1.mapA, s1.mapB, a1, s1.grid_n, st);
+    if (p->split) s1.mapAlo = s1.mapA;  // unused by the converter path; any valid map
+    cudaError_t e = tdc::tc_gemm_launch(s1.mapA, s1.mapAlo, s1.mapB, s1.mapBlo, a1, s1.grid_n, st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-1 launch");
     if (p->tc_core) {
         tdc::TcCoreArgs c = p->core_args;
@@ -471,13 +524,13 @@ tdc_status forward_tc(tdc_conv_plan_s *p, const float *x, float *y, int batch, c
         if (e != cudaSuccess)
             return fail(TDC_ERR_CUDA, "tcgen05 core launch: %s (M=%d ntiles=%d BN=%d smem=%d nphase=%d band=%d stages=%d)",
                         cudaGetErrorString(e), c.M, c.ntiles, c.BN,
-                        tdc::tc_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.b_stages), c.nphase,
+                        tdc::tc_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.b_stages, c.split), c.nphase,
                         c.band_rows, c.b_stages);
     } else {
-        e = tdc::tc_gemm_launch(s2.mapA, s2.mapB, a2, s2.grid_n, st);
+        e = tdc::tc_gemm_launch(s2.mapA, s2.mapAlo, s2.mapB, s2.mapBlo, a2, s2.grid_n, st);
     }
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-2 launch");
-    e = tdc::tc_gemm_launch(s3.mapA, s3.mapB, a3, s3.grid_n, st);
+    e = tdc::tc_gemm_launch(s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, a3, s3.grid_n, st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-3 launch");
     return TDC_OK;
 }
@@ -533,8 +586,6 @@ tdc_status tdc_conv_plan(const tdc_conv_desc *desc, const float *core, const flo
     if (prop.major != 10 || prop.minor != 0)
         return fail(TDC_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a only",
                     device, prop.major, prop.minor);
-    if (desc->math == TDC_MATH_3XTF32)
-        return fail(TDC_ERR_UNSUPPORTED, "math mode 3XTF32 is not available in this build");
 
     DeviceGuard guard(device);
     if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
@@ -607,8 +658,8 @@ tdc_status tdc_conv_plan(const tdc_conv_desc *desc, const float *core, const flo
             return s;
         }
     }
-    if (!fused && d.math == TDC_MATH_TF32 && C % 4 == 0 && K * K <= tdc::kMaxTaps) {
-        s = plan_tc(p, core, u_in, u_out, bias);
+    if (!fused && d.math != TDC_MATH_FP32 && C % 4 == 0 && K * K <= tdc::kMaxTaps) {
+        s = plan_tc(p, core, u_in, u_out, bias, d.math == TDC_MATH_3XTF32);
         if (s != TDC_OK) {
             tdc_conv_plan_destroy(p);
             return s;
@@ -639,7 +690,9 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
     const bool tc = p->variant == 2, fz = p->variant == 3;
     std::snprintf(info->variant_name, sizeof info->variant_name, "%s",
                   fz ? "fused_tc_tf32"
-                     : tc ? (p->tc_core ? "tc3_tf32_band" : "tc3_tf32") : "fused_simt_fp32");
+                     : tc ? (p->split ? (p->tc_core ? "tc3_3xtf32_band" : "tc3_3xtf32")
+                                      : (p->tc_core ? "tc3_tf32_band" : "tc3_tf32"))
+                          : "fused_simt_fp32");
     info->launches_per_forward = (tc ? 3 : 1) + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
     info->concurrent_forward = (p->desc.layout == TDC_LAYOUT_NHWC && !tc) ? 1 : 0;
     info->tile_h = p->simt_tile.oth;
@@ -652,7 +705,7 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
         info->tile_h = 128;
         info->tile_w = p->tc[1].args.BN;
         info->threads_per_cta = 192;
-        info->smem_bytes_per_cta = tdc::tc_smem_bytes(p->tc[1].args.BN, p->tc[1].args.stages);
+        info->smem_bytes_per_cta = tdc::tc_smem_bytes(p->tc[1].args.BN, p->tc[1].args.stages, p->split);
         info->ctas_per_image = 0;
     }
     if (fz) {

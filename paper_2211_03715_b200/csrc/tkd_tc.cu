@@ -1,34 +1,33 @@
-// tkd_tc.cu -- the TKD layer on 5th-generation tensor cores (tcgen05, kind::tf32).
+// tkd_tc.cu -- the TKD layer as three tcgen05 launches (the "3-launch" path).
 //
-// One kernel, tdc_tc_gemm_kernel, computes a "GEMM with taps":
+// Used where the fused kernel (tkd_fused.cu) does not pay off -- small images
+// with large ranks, whose weights dwarf a tile's activations -- and for the
+// fp32-accurate 3xTF32 math mode on every shape.
 //
-//     Out[m][n] = sum_{tap} sum_k A[m + a_off[tap]][k] * Bt[b_off[tap] + n][k]   (+ bias[n])
+//   stage 1 (a1)  tdc_tc_gemm_kernel: A = X (NHWC rows = pixels, K = C) by TMA,
+//                 Bt = U_in^T; the epilogue scatters each pixel's D1 ranks into the
+//                 zero-bordered "phase grid" X'g, stored planar [kg][row][4] so
+//                 stage 2 can bulk-copy row bands (reading R6: zero padding).
+//   stage 2 (a2)  tdc_tc_core_kernel: per 32-channel chunk of D1 the X' band of a
+//                 128-row output tile is copied into shared memory ONCE; each of
+//                 the K*K taps is a descriptor whose start is shifted by the tap's
+//                 constant row offset (r/s)*Wq + t/s -- the core convolution
+//                  as an implicit GEMM without per-tap data movement.
+//   stage 3 (a3)  tdc_tc_gemm_kernel: A = Z, Bt = U_out (N x D2 is K-major), bias
+//                 in the epilogue, rows written straight to Y (NHWC).
 //
-// and the three stages of the layer (include/tdc.h) are three instances of it:
+// 3xTF32 (TDC_MATH_3XTF32): every operand is split x = hi + lo with
+// hi = cvt.rna.tf32(x) and lo = x - hi (exact in fp32), and each product is
+// hi*hi + hi*lo + lo*hi with fp32 accumulation in TMEM (~5e-7 max-normalized
+// error on the R18 shapes vs ~5e-4 for one TF32 product).  Weights are split at
+// plan time, X' and Z by the producing epilogue, and the user's X by a converter
+// warpgroup between the TMA landing and the MMA.
 //
-//   stage 1 (a1): A = X (NHWC rows = pixels, K = C), Bt = U_in^T, one tap; the
-//                 epilogue scatters each pixel's D1 ranks into a zero-bordered
-//                 "phase grid" X'g (below) -- zero padding for free (reading R6).
-//   stage 2 (a2): A = X'g, Bt = core re-laid out per tap, K*K taps whose row
-//                 offsets are constants on the phase grid, so the core
-//                 convolution is an implicit GEMM with pure TMA
-//                 row-shifted loads; the epilogue compacts valid rows into Z.
-//   stage 3 (a3): A = Z, Bt = U_out (N x D2 is already K-major), one tap,
-//                 bias in the epilogue, rows written straight to Y (NHWC).
-//
-// Phase grid (stride s, pad p): padded coordinate u = y + p splits into phase
-// u % s and position u / s; tap (r, t) of output (oy, ox) reads phase
-// (r % s, t % s) at (oy + r / s, ox + t / s).  With every image laid out as an
-// Hq x Wq block (Hq = ceil((H+2p)/s)), the read row is (output-grid row) +
-// constant, which is exactly what a TMA box at a shifted row coordinate loads.
-//
-// Kernel anatomy (one 128 x BN output tile per CTA, 6 warps):
-//   warp 0  TMA producer: A (128 rows x 32 fp32, 128B-swizzled) and Bt (BN x 32)
-//           per (tap, 32-wide K chunk) into an S-stage mbarrier ring;
-//   warp 1  TMEM allocation + single-thread tcgen05.mma issue (4 x K=8 per
-//           chunk), tcgen05.commit frees ring slots / signals the epilogue;
-//   warps 2-5  epilogue: tcgen05.ld 32x32b (one TMEM lane = one output row per
-//           thread), bias, row remap, vectorised global stores.
+// Kernel anatomy (one 128 x BN output tile per CTA):
+//   warp 0      producer (TMA / bulk copies) into an S-stage mbarrier ring;
+//   warp 1      TMEM owner + MMA issue (warp-uniform loop, one elected lane);
+//   warps 2-5   epilogue: tcgen05.ld 32x32b, one TMEM lane = one output row;
+//   warps 6-9   (3xTF32 stage 1 only) converter: hi in place, lo alongside.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -39,10 +38,15 @@ namespace tdc {
 
 using namespace sm100;
 
-constexpr int kTcThreads = 192;
 constexpr int kBM = 128;
-constexpr int kBK = 32;                      // fp32 elements per K chunk = one 128 B swizzle row
-constexpr int kATileBytes = kBM * kBK * 4;   // 16 KB
+constexpr int kBK = 32;                     // fp32 elements per K chunk = one 128 B swizzle row
+constexpr int kATileBytes = kBM * kBK * 4;  // 16 KB
+
+__device__ __forceinline__ float rna_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
 
 __device__ __forceinline__ bool remap_row(const TcGemmArgs &g, int m, long long *dst) {
     if (m >= g.M) return false;
@@ -70,29 +74,74 @@ __device__ __forceinline__ bool remap_row(const TcGemmArgs &g, int m, long long 
     return true;
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1)
-tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
-                   const __grid_constant__ CUtensorMap mapB, const TcGemmArgs g) {
+__device__ __forceinline__ void split4(const float *v, float4 *hi, float4 *lo) {
+    const float4 h = make_float4(rna_tf32(v[0]), rna_tf32(v[1]), rna_tf32(v[2]), rna_tf32(v[3]));
+    *hi = h;
+    *lo = make_float4(v[0] - h.x, v[1] - h.y, v[2] - h.z, v[3] - h.w);
+}
+
+// Store 32 consecutive output columns of one row (optionally split into hi/lo).
+__device__ __forceinline__ void store_row32(float *dst, float *dst_lo, long long planar, int n,
+                                            int Nn, bool ldo_vec, const float (&v)[32], bool split) {
+    if (planar) {  // [col/4][row][4]: lanes = consecutive rows -> coalesced
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+            const long long off = (long long)((n + j) >> 2) * planar;
+            if (split)
+                split4(v + j, reinterpret_cast<float4 *>(dst + off), reinterpret_cast<float4 *>(dst_lo + off));
+            else
+                *reinterpret_cast<float4 *>(dst + off) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+    } else if (n + 32 <= Nn && ldo_vec) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+            if (split)
+                split4(v + j, reinterpret_cast<float4 *>(dst + n + j),
+                       reinterpret_cast<float4 *>(dst_lo + n + j));
+            else
+                *reinterpret_cast<float4 *>(dst + n + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+    } else {
+        for (int j = 0; j < 32 && n + j < Nn; ++j) {
+            if (split) {
+                const float h = rna_tf32(v[j]);
+                dst[n + j] = h;
+                dst_lo[n + j] = v[j] - h;
+            } else {
+                dst[n + j] = v[j];
+            }
+        }
+    }
+}
+
+// ============================================================ GEMM with taps
+template <bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? 320 : 192, 1)
+tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
+                   const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo,
+                   const TcGemmArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-byte alignment for the 128B-swizzle atoms
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = g.stages, BN = g.BN;
-    const int b_tile_bytes = BN * kBK * 4;
-    uint8_t *a_tiles = smem;
-    uint8_t *b_tiles = smem + (size_t)S * kATileBytes;
-    uint64_t *full = reinterpret_cast<uint64_t *>(b_tiles + (size_t)S * b_tile_bytes);
-    uint64_t *empty = full + S;
+    const uint32_t b_tile = (uint32_t)BN * kBK * 4;
+    const uint32_t slot_bytes = (SPLIT ? 2 : 1) * (kATileBytes + b_tile);
+    // slot layout: A hi | B hi | [A lo | B lo]
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * slot_bytes);
+    uint64_t *conv = full + S;
+    uint64_t *empty = conv + S;
     uint64_t *tfull = empty + S;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfull + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
     const uint32_t ncols = BN < 32 ? 32 : BN;
+    const bool convert = SPLIT && g.a_convert;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
+            mbar_init(&conv[i], 128);
             mbar_init(&empty[i], 1);
         }
         mbar_init(tfull, 1);
@@ -109,49 +158,67 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
     const uint32_t tmem = *tmem_slot;
     const int iters = g.taps * g.kchunks;
 
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer
-            const uint32_t bytes = kATileBytes + b_tile_bytes;
-            for (int i = 0; i < iters; ++i) {
-                const int st = i % S;
-                const uint32_t ph = (i / S) & 1;
-                mbar_wait(&empty[st], ph ^ 1);
-                mbar_arrive_expect_tx(&full[st], bytes);
-                const int tap = i / g.kchunks, kc = i - tap * g.kchunks;
-                tma_load_2d(a_tiles + (size_t)st * kATileBytes, &mapA, &full[st], kc * kBK,
-                            m0 + g.a_off[tap]);
-                tma_load_2d(b_tiles + (size_t)st * b_tile_bytes, &mapB, &full[st], kc * kBK,
-                            g.b_off[tap] + n0);
+    if (warp == 0) {  // ------------------------------------- TMA producer
+        const uint32_t bytes = (SPLIT && !convert ? 2 : 1) * kATileBytes + (SPLIT ? 2 : 1) * b_tile;
+        Ring r(S);
+        int tap = 0, kc = 0;
+        for (int i = 0; i < iters; ++i, r.next()) {
+            mbar_wait(&empty[r.slot], r.phase ^ 1);
+            if (elect_one()) {
+                uint8_t *base = smem + (size_t)r.slot * slot_bytes;
+                mbar_arrive_expect_tx(&full[r.slot], bytes);
+                tma_load_2d(base, &mapA, &full[r.slot], kc * kBK, m0 + g.a_off[tap]);
+                tma_load_2d(base + kATileBytes, &mapB, &full[r.slot], kc * kBK, g.b_off[tap] + n0);
+                if (SPLIT) {
+                    if (!convert)
+                        tma_load_2d(base + kATileBytes + b_tile, &mapAlo, &full[r.slot], kc * kBK,
+                                    m0 + g.a_off[tap]);
+                    tma_load_2d(base + 2 * kATileBytes + b_tile, &mapBlo, &full[r.slot], kc * kBK,
+                                g.b_off[tap] + n0);
+                }
+            }
+            __syncwarp();
+            if (++kc == g.kchunks) {
+                kc = 0;
+                ++tap;
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer (single thread)
-            const uint32_t idesc = idesc_tf32(kBM, BN);
-            for (int i = 0; i < iters; ++i) {
-                const int st = i % S;
-                const uint32_t ph = (i / S) & 1;
-                mbar_wait(&full[st], ph);
-                tc_fence_after();
-                const uint32_t a0 = smem_u32(a_tiles + (size_t)st * kATileBytes);
-                const uint32_t b0 = smem_u32(b_tiles + (size_t)st * b_tile_bytes);
+    } else if (warp == 1) {  // ------------------------------ MMA issuer
+        const uint32_t idesc = idesc_tf32(kBM, BN);
+        const uint64_t da = sdesc_kmajor_sw128(smem_u32(smem));
+        const uint64_t db = sdesc_kmajor_sw128(smem_u32(smem + kATileBytes));
+        const uint32_t lo_off = (kATileBytes + b_tile) >> 4;  // hi -> lo, 16-byte units
+        Ring r(S);
+        for (int i = 0; i < iters; ++i, r.next()) {
+            mbar_wait(convert ? &conv[r.slot] : &full[r.slot], r.phase);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint64_t a = da + ((r.slot * slot_bytes) >> 4);
+                const uint64_t b = db + ((r.slot * slot_bytes) >> 4);
 #pragma unroll
                 for (int j = 0; j < kBK / 8; ++j) {  // K = 8 tf32 = 32 B per MMA
-                    mma_tf32(tmem, sdesc_kmajor_sw128(a0 + j * 32), sdesc_kmajor_sw128(b0 + j * 32),
-                             idesc, (i | j) != 0);
+                    mma_tf32(tmem, a + j * 2, b + j * 2, idesc, (i | j) != 0);
+                    if (SPLIT) {
+                        mma_tf32(tmem, a + j * 2, b + lo_off + j * 2, idesc, 1);  // hi * lo
+                        mma_tf32(tmem, a + lo_off + j * 2, b + j * 2, idesc, 1);  // lo * hi
+                    }
                 }
-                mma_commit(&empty[st]);
+                mma_commit(&empty[r.slot]);
             }
-            mma_commit(tfull);
+            __syncwarp();
         }
-    } else {  // ------------------------------ epilogue warps 2..5
+        if (elect_one()) mma_commit(tfull);
+        __syncwarp();
+    } else if (warp < 6) {  // --------------------------------- epilogue
         mbar_wait(tfull, 0);
         tc_fence_after();
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int row = q * 32 + lane;
-        long long dst_row;
+        long long dst_row = 0;
         const bool valid = remap_row(g, m0 + row, &dst_row);
-        float *dst = valid ? (g.planar_stride ? g.out + dst_row * 4 : g.out + dst_row * g.ldo)
-                           : nullptr;
+        const long long off = g.planar_stride ? dst_row * 4 : dst_row * g.ldo;
+        float *dst = g.out + off;
+        float *dst_lo = (SPLIT && g.out_lo) ? g.out_lo + off : nullptr;
         for (int c = 0; c < BN; c += 32) {
             uint32_t r[32];
             tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
@@ -166,19 +233,24 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                 for (int j = 0; j < 32; ++j)
                     if (n + j < g.Nn) v[j] += __ldg(&g.bias[n + j]);
             }
-            if (g.planar_stride) {  // [col/4][row][4]: lanes = consecutive rows -> coalesced
+            store_row32(dst, dst_lo, g.planar_stride, n, g.Nn, (g.ldo & 3) == 0, v, dst_lo != nullptr);
+        }
+    } else if (convert) {  // ------------------------ converter (3xTF32 stage 1)
+        const int t = threadIdx.x - 192;  // 0..127: each owns 128 contiguous bytes of A
+        Ring r(S);
+        for (int i = 0; i < iters; ++i, r.next()) {
+            mbar_wait(&full[r.slot], r.phase);
+            float4 *a = reinterpret_cast<float4 *>(smem + (size_t)r.slot * slot_bytes) + t * 8;
+            float4 *lo = reinterpret_cast<float4 *>(smem + (size_t)r.slot * slot_bytes +
+                                                    kATileBytes + b_tile) + t * 8;
 #pragma unroll
-                for (int j = 0; j < 32; j += 4)
-                    *reinterpret_cast<float4 *>(dst + (long long)((n + j) >> 2) * g.planar_stride) =
-                        make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            } else if (n + 32 <= g.Nn && (g.ldo & 3) == 0) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 4)
-                    *reinterpret_cast<float4 *>(dst + n + j) =
-                        make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-            } else {
-                for (int j = 0; j < 32 && n + j < g.Nn; ++j) dst[n + j] = v[j];
+            for (int j = 0; j < 8; ++j) {  // elementwise: the 128B swizzle is irrelevant
+                const float4 v = a[j];
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+                split4(vv, &a[j], &lo[j]);
             }
+            fence_proxy_async_smem();
+            mbar_arrive(&conv[r.slot]);
         }
     }
     tc_fence_before();
@@ -186,35 +258,41 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
     if (warp == 1) tmem_dealloc(tmem, ncols);
 }
 
+int tc_smem_bytes(int BN, int stages, int split) {
+    return 1024 /*align slack*/ + stages * (split ? 2 : 1) * (kATileBytes + BN * kBK * 4) +
+           (3 * stages + 1) * 8 + 16;
+}
 
-// ---------------------------------------------------------------------------
-// Stage 2 with a resident X' band: the core convolution as an
-// implicit GEMM whose A operand is never re-fetched per tap.  Per 32-channel
-// chunk kc of D1, the rows [m0, m0 + band_rows) of every phase plane are
-// bulk-copied once into shared memory in the no-swizzle K-major layout
-// [phase][kg][row][4 fp32] (a "core matrix" = 8 rows x 16 B); tap (r, t) is
-// then just a descriptor whose start address is shifted by the tap's constant
-// row offset (r/s)*Wq + t/s -- the 8-row groups stay 128 B apart (SBO) and the
-// K-adjacent 4-channel planes band_rows*16 B apart (LBO).  Weights arrive as
-// pre-blocked [8][BN][4] chunks (plan-time re-layout, the CRSN idea P:L338-340).
+int tc_pick_stages(int BN, int iters, int max_smem, int split) {
+    int s = 8;
+    while (s > 2 && tc_smem_bytes(BN, s, split) > max_smem) --s;
+    if (s > iters) s = iters < 2 ? 2 : iters;
+    return s;
+}
+
+// ============================================================ core conv (stage 2)
 constexpr int kCoreThreads = 192;
 
 __host__ __device__ inline int core_a_slot_bytes(int nphase, int band_rows) {
     return nphase * 8 * band_rows * 16;
 }
 
-int tc_core_smem_bytes(int BN, int nphase, int band_rows, int b_stages) {
-    return 1024 + 2 * core_a_slot_bytes(nphase, band_rows) + b_stages * BN * 128 +
+int tc_core_smem_bytes(int BN, int nphase, int band_rows, int b_stages, int split) {
+    const int f = split ? 2 : 1;
+    return 1024 + 2 * f * core_a_slot_bytes(nphase, band_rows) + b_stages * f * BN * 128 +
            (4 + 2 * b_stages + 1) * 8 + 16;
 }
 
+template <bool SPLIT>
 __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCoreArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int BN = g.BN, SB = g.b_stages;
-    const int a_bytes = core_a_slot_bytes(g.nphase, g.band_rows);
-    const int b_bytes = BN * 128;
+    const uint32_t a_half = core_a_slot_bytes(g.nphase, g.band_rows);  // hi -> lo
+    const uint32_t a_bytes = a_half * (SPLIT ? 2 : 1);
+    const uint32_t b_half = BN * 128;
+    const uint32_t b_bytes = b_half * (SPLIT ? 2 : 1);
     uint8_t *a_slots = smem;
     uint8_t *b_slots = smem + 2 * (size_t)a_bytes;
     uint64_t *a_full = reinterpret_cast<uint64_t *>(b_slots + (size_t)SB * b_bytes);
@@ -247,59 +325,73 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
     const uint32_t tmem = *tmem_slot;
     const uint32_t band_bytes = (uint32_t)g.band_rows * 16;
 
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- bulk-copy producer
-            int it = 0;
-            for (int kc = 0; kc < g.kchunks; ++kc) {
-                const int sa = kc & 1;
-                mbar_wait(&a_empty[sa], ((kc >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&a_full[sa], (uint32_t)a_bytes);
-                uint8_t *dst = a_slots + (size_t)sa * a_bytes;
+    if (warp == 0) {  // ---------------------------------- bulk-copy producer
+        Ring ra(2), rb(SB);
+        for (int kc = 0; kc < g.kchunks; ++kc, ra.next()) {
+            mbar_wait(&a_empty[ra.slot], ra.phase ^ 1);
+            if (elect_one()) {
+                mbar_arrive_expect_tx(&a_full[ra.slot], a_bytes);
+                uint8_t *dst = a_slots + (size_t)ra.slot * a_bytes;
                 for (int ph = 0; ph < g.nphase; ++ph)
                     for (int kg = 0; kg < 8; ++kg) {
-                        const float *src = g.xg + (long long)(kc * 8 + kg) * g.plane_stride +
-                                           ((long long)g.phase_src[ph] * g.phase_rows + m0) * 4;
-                        bulk_load(dst + (size_t)(ph * 8 + kg) * band_bytes, src, band_bytes,
-                                  &a_full[sa]);
+                        const long long off = (long long)(kc * 8 + kg) * g.plane_stride +
+                                              ((long long)g.phase_src[ph] * g.phase_rows + m0) * 4;
+                        bulk_load(dst + (size_t)(ph * 8 + kg) * band_bytes, g.xg + off, band_bytes,
+                                  &a_full[ra.slot]);
+                        if (SPLIT)
+                            bulk_load(dst + a_half + (size_t)(ph * 8 + kg) * band_bytes, g.xg_lo + off,
+                                      band_bytes, &a_full[ra.slot]);
                     }
-                for (int tap = 0; tap < g.taps; ++tap, ++it) {
-                    const int sb = it % SB;
-                    mbar_wait(&b_empty[sb], ((it / SB) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&b_full[sb], (uint32_t)b_bytes);
-                    const float *src =
-                        g.w + ((long long)(tap * g.kchunks + kc) * g.ntiles + nt) * BN * 32;
-                    bulk_load(b_slots + (size_t)sb * b_bytes, src, (uint32_t)b_bytes, &b_full[sb]);
+            }
+            __syncwarp();
+            for (int tap = 0; tap < g.taps; ++tap, rb.next()) {
+                mbar_wait(&b_empty[rb.slot], rb.phase ^ 1);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(&b_full[rb.slot], b_bytes);
+                    const long long woff = ((long long)(tap * g.kchunks + kc) * g.ntiles + nt) * BN * 32;
+                    uint8_t *dst = b_slots + (size_t)rb.slot * b_bytes;
+                    bulk_load(dst, g.w + woff, b_half, &b_full[rb.slot]);
+                    if (SPLIT) bulk_load(dst + b_half, g.w_lo + woff, b_half, &b_full[rb.slot]);
                 }
+                __syncwarp();
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            const uint32_t idesc = idesc_tf32(kBM, BN);
-            int it = 0;
-            for (int kc = 0; kc < g.kchunks; ++kc) {
-                const int sa = kc & 1;
-                mbar_wait(&a_full[sa], (kc >> 1) & 1);
-                const uint32_t a0 = smem_u32(a_slots + (size_t)sa * a_bytes);
-                for (int tap = 0; tap < g.taps; ++tap, ++it) {
-                    const int sb = it % SB;
-                    mbar_wait(&b_full[sb], (it / SB) & 1);
-                    tc_fence_after();
-                    const uint32_t b0 = smem_u32(b_slots + (size_t)sb * b_bytes);
-                    const uint32_t abase = a0 + (uint32_t)g.tap_phase[tap] * 8 * band_bytes +
-                                           (uint32_t)g.tap_off[tap] * 16;
+    } else if (warp == 1) {  // ------------------------------ MMA issuer
+        const uint32_t idesc = idesc_tf32(kBM, BN);
+        const uint64_t da = sdesc_kmajor_none(smem_u32(a_slots), band_bytes, 128);
+        const uint64_t db = sdesc_kmajor_none(smem_u32(b_slots), BN * 16, 128);
+        Ring ra(2), rb(SB);
+        bool first = true;
+        for (int kc = 0; kc < g.kchunks; ++kc, ra.next()) {
+            mbar_wait(&a_full[ra.slot], ra.phase);
+            for (int tap = 0; tap < g.taps; ++tap, rb.next()) {
+                mbar_wait(&b_full[rb.slot], rb.phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint64_t a = da + ((ra.slot * a_bytes + (uint32_t)g.tap_phase[tap] * 8 * band_bytes +
+                                              (uint32_t)g.tap_off[tap] * 16) >> 4);
+                    const uint64_t b = db + ((rb.slot * b_bytes) >> 4);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {  // K = 8 = two 4-channel planes
-                        const uint64_t ad = sdesc_kmajor_none(abase + j * 2 * band_bytes, band_bytes, 128);
-                        const uint64_t bd = sdesc_kmajor_none(b0 + j * 2 * BN * 16, BN * 16, 128);
-                        mma_tf32(tmem, ad, bd, idesc, (kc | tap | j) != 0);
+                        const uint64_t aj = a + ((j * 2 * band_bytes) >> 4);
+                        const uint64_t bj = b + ((j * 2 * BN * 16) >> 4);
+                        mma_tf32(tmem, aj, bj, idesc, !(first && j == 0));
+                        if (SPLIT) {
+                            mma_tf32(tmem, aj, bj + (b_half >> 4), idesc, 1);
+                            mma_tf32(tmem, aj + (a_half >> 4), bj, idesc, 1);
+                        }
                     }
-                    mma_commit(&b_empty[sb]);
+                    mma_commit(&b_empty[rb.slot]);
                 }
-                mma_commit(&a_empty[sa]);
+                __syncwarp();
+                first = false;
             }
-            mma_commit(tfull);
+            if (elect_one()) mma_commit(&a_empty[ra.slot]);
+            __syncwarp();
         }
-    } else {  // ------------------------------ epilogue warps 2..5: Z compact rows
+        if (elect_one()) mma_commit(tfull);
+        __syncwarp();
+    } else {  // --------------------------------- epilogue warps 2..5: Z compact
         mbar_wait(tfull, 0);
         tc_fence_after();
         const int q = warp & 3;
@@ -315,16 +407,16 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
             dst_row = ((long long)b * g.Ho + oy) * g.Wo + ox;
         }
         float *dst = g.z + dst_row * g.ldz;
+        float *dst_lo = SPLIT ? g.z_lo + dst_row * g.ldz : nullptr;
         for (int c = 0; c < BN; c += 32) {
             uint32_t r[32];
             tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
             tmem_ld_wait();
             if (!valid || n0 + c >= g.Nn) continue;
+            float v[32];
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4 *>(dst + n0 + c + j) =
-                    make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            store_row32(dst, dst_lo, 0, n0 + c, g.Nn, true, v, SPLIT);
         }
     }
     tc_fence_before();
@@ -333,24 +425,19 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
 }
 
 cudaError_t tc_core_launch(const TcCoreArgs &g, cudaStream_t st) {
-    const int smem = tc_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.b_stages);
-    cudaError_t e =
-        cudaFuncSetAttribute(tdc_tc_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
+    const int smem = tc_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.b_stages, g.split);
     dim3 grid((g.M + kBM - 1) / kBM, g.ntiles);
-    tdc_tc_core_kernel<<<grid, kCoreThreads, smem, st>>>(g);
+    cudaError_t e;
+    if (g.split) {
+        e = cudaFuncSetAttribute(tdc_tc_core_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        tdc_tc_core_kernel<true><<<grid, kCoreThreads, smem, st>>>(g);
+    } else {
+        e = cudaFuncSetAttribute(tdc_tc_core_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        tdc_tc_core_kernel<false><<<grid, kCoreThreads, smem, st>>>(g);
+    }
     return cudaGetLastError();
-}
-
-int tc_smem_bytes(int BN, int stages) {
-    return 1024 /*align slack*/ + stages * (kATileBytes + BN * kBK * 4) + (2 * stages + 1) * 8 + 16;
-}
-
-int tc_pick_stages(int BN, int iters, int max_smem) {
-    int s = 8;
-    while (s > 2 && tc_smem_bytes(BN, s) > max_smem) --s;
-    if (s > iters) s = iters < 2 ? 2 : iters;
-    return s;
 }
 
 // ----------------------------------------------------------------- host side
@@ -397,14 +484,21 @@ bool make_tma_4d_nhwc(CUtensorMap *map, const float *x, int C, int W, int H, int
     return r == CUDA_SUCCESS;
 }
 
-cudaError_t tc_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapB, const TcGemmArgs &g,
+cudaError_t tc_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo,
+                           const CUtensorMap &mapB, const CUtensorMap &mapBlo, const TcGemmArgs &g,
                            int grid_n, cudaStream_t st) {
-    const int smem = tc_smem_bytes(g.BN, g.stages);
-    cudaError_t e =
-        cudaFuncSetAttribute(tdc_tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
+    const int smem = tc_smem_bytes(g.BN, g.stages, g.split);
     dim3 grid((g.M + kBM - 1) / kBM, grid_n);
-    tdc_tc_gemm_kernel<<<grid, kTcThreads, smem, st>>>(mapA, mapB, g);
+    cudaError_t e;
+    if (g.split) {
+        e = cudaFuncSetAttribute(tdc_tc_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        tdc_tc_gemm_kernel<true><<<grid, 320, smem, st>>>(mapA, mapAlo, mapB, mapBlo, g);
+    } else {
+        e = cudaFuncSetAttribute(tdc_tc_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        tdc_tc_gemm_kernel<false><<<grid, 192, smem, st>>>(mapA, mapAlo, mapB, mapBlo, g);
+    }
     return cudaGetLastError();
 }
 

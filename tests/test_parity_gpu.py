@@ -57,7 +57,7 @@ def ref_of(shape, d, b=None):
     return oracle.tkd_stages(x, d["core"], d["u_in"], d["u_out"], d["bias"], shape.stride, shape.pad)
 
 
-MATHS = ["fp32", "tf32"]
+MATHS = ["fp32", "tf32", "3xtf32"]
 
 
 @pytest.mark.parametrize("math", MATHS)
@@ -70,11 +70,14 @@ def test_config1(env, layout, math):
     assert err(got, ref_of(s, d)) <= TOL[math]
 
 
+@pytest.mark.parametrize("math", ["fp32", "3xtf32"])
 @pytest.mark.parametrize("layout", ["nhwc", "nchw"])
-def test_integer_layer_is_bit_exact(env, layout):
+def test_integer_layer_is_bit_exact(env, layout, math):
+    """Every partial sum is an integer < 2^22: fp32 FFMA and the exact 3xTF32 split
+    (hi = value, lo = 0) must reproduce the oracle bit for bit."""
     s = LayerShape(2, 16, 16, 8, 8, 4, 4, 3, 1, 1)
     d = synth.make_layer(s, integer=True, bias=True)
-    got, _ = run_layer(env, s, d, layout, "fp32")
+    got, _ = run_layer(env, s, d, layout, math)
     assert np.array_equal(got.astype(np.float64), ref_of(s, d))
 
 
