@@ -50,7 +50,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["tdc", "reference"], default="tdc")
-    ap.add_argument("--math", choices=["fp32", "tf32", "3xtf32"], default="fp32")
+    ap.add_argument("--math", choices=["fp32", "tf32", "3xtf32"], default="3xtf32",
+                    help="3xtf32: fp32-accurate tensor-core split (default); tf32: 1e-2 mode; "
+                         "fp32: CUDA-core FFMA")
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -186,14 +188,12 @@ def impl_reference(args):
 # ------------------------------------------------------------------ tdc arm
 def impl_tdc(args):
     import torch
-    import torch.distributed as dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2211_03715_b200 import dist as tdist
+
+    rank, world, local = tdist.env_ranks()
     torch.cuda.set_device(local)
+    tdist.init("nccl", torch.device("cuda", local))
     from paper_2211_03715_b200 import tdc
 
     math = tdc.MATH_NAMES[args.math]
@@ -226,8 +226,7 @@ def impl_tdc(args):
            for _ in layers] for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
+    tdist.barrier()
     torch.cuda.synchronize()
     with sampler:
         t_start.record(stream)
@@ -235,13 +234,8 @@ def impl_tdc(args):
             step(ev[k])
         t_end.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    total_ms = t_start.elapsed_time(t_end)
-    if world > 1:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    tdist.barrier()
+    total_ms = tdist.max_over_ranks(t_start.elapsed_time(t_end), "cuda")
 
     # per-layer mean durations (events on the launching stream)
     per_layer_ms = [statistics.mean(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps))
@@ -310,19 +304,14 @@ def impl_tdc(args):
         for L, (xh, yh) in zip(layers, host):
             L["plan"].forward_host(xh, yh, stream=stream)
         e2e_steps = max(1, min(args.steps, 5))
-        if world > 1:
-            dist.barrier()
+        tdist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             for L, (xh, yh) in zip(layers, host):
                 L["plan"].forward_host(xh, yh, stream=stream)
         torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([el], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        el = tdist.max_over_ranks(time.perf_counter() - t0, "cuda")
         e2e = {"value": step_bytes * e2e_steps * world / el / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": sum(int(h[0].numel()) * 4 for h in host),
                "d2h_bytes_per_step": sum(int(h[1].numel()) * 4 for h in host),
@@ -340,7 +329,11 @@ def impl_tdc(args):
                 "steps": args.steps, "warmup": max(args.warmup, 3),
                 "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None,
-                "dtype": {"fp32": "f32", "tf32": "tf32", "3xtf32": "3xtf32"}[args.math],
+                "dtype": {"fp32": "f32", "tf32": "tf32", "3xtf32": "f32(3xtf32)"}[args.math],
+                "accuracy": {"fp32": "fp32 FFMA; max-normalized err vs fp64 oracle <= 1e-4",
+                             "tf32": "TF32 products; tolerance 1e-2 (north_star TF32 stage)",
+                             "3xtf32": "hi*hi+hi*lo+lo*hi TF32 split, fp32 accumulate; fp32-grade, "
+                                       "tolerance 1e-4 (measured ~5e-7)"}[args.math],
                 "data": "synthetic", "config": config_dict(args, world),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps,
@@ -349,8 +342,7 @@ def impl_tdc(args):
         print(json.dumps(line), flush=True)
     for L in layers:
         L["plan"].close()
-    if world > 1:
-        dist.destroy_process_group()
+    tdist.finalize()
 
 
 def main():
