@@ -111,6 +111,8 @@ struct tdc_conv_plan_s {
     int fgrid = 0, num_sms = 148;
     bool tc_core = false;          // stage 2 uses the band-resident core kernel
     bool split = false;            // 3xTF32
+    float *d_part = nullptr;       // split-K partials (shared by the three stages)
+    tdc::ReduceArgs red[3];        // per-stage reduce (used when that stage's ksplit > 1)
     tdc::TcCoreArgs core_args;
     float *d_tc_w = nullptr;       // Bt1 | Bt2 | Bt3 | bias
     float *d_xg = nullptr;         // X' phase grids (zero borders)
@@ -122,12 +124,6 @@ struct tdc_conv_plan_s {
 
 namespace {
 
-int pick_bn(int nn, long long mtiles) {
-    int bn = 256;
-    while (bn > 32 && bn / 2 >= nn) bn /= 2;          // do not exceed the output width
-    while (bn > 64 && mtiles * ((nn + bn - 1) / bn) < 2 * 148) bn /= 2;  // fill the SMs
-    return bn;
-}
 
 int div_up(int a, int b) { return (a + b - 1) / b; }
 
@@ -156,10 +152,13 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     if (M1 > (1LL << 31) - 256 || M2 * s * s > (1LL << 31) - 256)
         return fail(TDC_ERR_UNSUPPORTED, "batch too large for the tensor-core variant");
     const int sp = split ? 1 : 0;
-    const int BN1 = pick_bn(D1s, div_up((int)M1, 128));
-    const int BN2 = pick_bn(D2s, div_up((int)M2, 128));
-    const int BN3 = pick_bn(N, div_up((int)M3, 128));
-    const int R1 = round_up(D1s, BN1), R2 = round_up(D2s, BN2), R3 = round_up(N, BN3);
+    // Widest N tile: a tcgen05.mma costs ~130-150 cycles whatever N <= 256 is
+    // (DESIGN.md §8), so N = 256 does 8x the work of N = 32 per instruction.
+    // Parallelism lost to wide tiles is restored with split-K below.
+    auto wide_bn = [](int nn) { return std::min(256, round_up(nn, 32)); };
+    int BN1 = wide_bn(D1s);
+    int BN2 = wide_bn(D2s);
+    const int BN3 = wide_bn(N);
     const int KK = K * K;
 
     // Stage-2 kernel choice: band-resident core kernel if its two A slots fit.
@@ -180,10 +179,17 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
             }
     }
     int core_stages = 4;
-    while (core_stages > 2 &&
-           tdc::tc_core_smem_bytes(BN2, nphase, band_rows, core_stages, sp) > p->max_smem)
-        --core_stages;
+    for (;;) {
+        while (core_stages > 2 &&
+               tdc::tc_core_smem_bytes(BN2, nphase, band_rows, core_stages, sp) > p->max_smem)
+            --core_stages;
+        if (BN2 <= 64 || tdc::tc_core_smem_bytes(BN2, nphase, band_rows, core_stages, sp) <= p->max_smem)
+            break;
+        BN2 /= 2;  // narrower tile so the band + weight ring fit
+        core_stages = 4;
+    }
     p->tc_core = tdc::tc_core_smem_bytes(BN2, nphase, band_rows, core_stages, sp) <= p->max_smem;
+    const int R1 = round_up(D1s, BN1), R2 = round_up(D2s, BN2), R3 = round_up(N, BN3);
     const int k2chunks = D1s / 32, nt2 = R2 / BN2;
     const long long rows_total = (long long)s * s * phase_rows + band_rows + 128;
 
@@ -329,6 +335,63 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
             st.mapAlo = st.mapA;
             st.mapBlo = st.mapB;
         }
+    }
+    // ---- split-K: fill the SMs when a stage has few output tiles ----
+    auto choose_ksplit = [&](long long mrows, int ntiles, int iters) {
+        const long long ctas = div_up((int)mrows, 128) * (long long)ntiles;
+        if (ctas >= p->num_sms || iters < 4) return 1;
+        int k = (int)std::min<long long>(div_up(p->num_sms, (int)ctas), std::min(16, iters / 2));
+        if (k < 2) return 1;
+        const int per = div_up(iters, k);
+        return div_up(iters, per);  // no empty splits
+    };
+    size_t part_elems = 0;
+    auto set_reduce = [&](int i, const tdc::TcGemmArgs &a, int part_ld, int ks) {
+        tdc::ReduceArgs &r = p->red[i];
+        std::memset(&r, 0, sizeof r);
+        r.ksplit = ks; r.M = a.M; r.Nn = a.Nn; r.part_ld = part_ld;
+        r.out = a.out; r.out_lo = a.out_lo; r.ldo = a.ldo; r.planar_stride = a.planar_stride;
+        r.bias = a.bias; r.remap = a.remap; r.H = a.H; r.W = a.W; r.s = a.s; r.p = a.p;
+        r.Hq = a.Hq; r.Wq = a.Wq; r.Ho = a.Ho; r.Wo = a.Wo; r.phase_rows = a.phase_rows;
+        r.split = split && a.out_lo ? 1 : 0;
+        part_elems = std::max(part_elems, (size_t)ks * round_up(a.M, 128) * part_ld);
+    };
+    {
+        auto &a = p->tc[0].args;
+        a.ksplit = choose_ksplit(M1, p->tc[0].grid_n, a.taps * a.kchunks);
+        a.part_ld = p->tc[0].grid_n * BN1;
+        if (a.ksplit > 1) set_reduce(0, a, a.part_ld, a.ksplit);
+    }
+    if (p->tc_core) {
+        auto &c = p->core_args;
+        c.ksplit = choose_ksplit(M2, c.ntiles, c.kchunks * c.taps);
+        c.part_ld = c.ntiles * c.BN;
+        if (c.ksplit > 1) {
+            tdc::TcGemmArgs geo;
+            std::memset(&geo, 0, sizeof geo);
+            geo.M = c.M; geo.Nn = c.Nn; geo.out = c.z; geo.out_lo = c.z_lo; geo.ldo = c.ldz;
+            geo.remap = 2; geo.Hq = Hq; geo.Wq = Wq; geo.Ho = Ho; geo.Wo = Wo; geo.H = H; geo.W = W;
+            geo.s = s; geo.p = pad; geo.phase_rows = phase_rows;
+            set_reduce(1, geo, c.part_ld, c.ksplit);
+        }
+    } else {
+        auto &a = p->tc[1].args;
+        a.ksplit = choose_ksplit(M2, p->tc[1].grid_n, a.taps * a.kchunks);
+        a.part_ld = p->tc[1].grid_n * BN2;
+        if (a.ksplit > 1) set_reduce(1, a, a.part_ld, a.ksplit);
+    }
+    {
+        auto &a = p->tc[2].args;
+        a.ksplit = choose_ksplit(M3, p->tc[2].grid_n, a.taps * a.kchunks);
+        a.part_ld = p->tc[2].grid_n * BN3;
+        if (a.ksplit > 1) set_reduce(2, a, a.part_ld, a.ksplit);
+    }
+    if (part_elems) {
+        e = cudaMalloc(&p->d_part, part_elems * sizeof(float));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(split-K partials)");
+        p->tc_ws_bytes += part_elems * sizeof(float);
+        p->tc[0].args.part = p->tc[1].args.part = p->tc[2].args.part = p->d_part;
+        p->core_args.part = p->d_part;
     }
     p->variant = 2;
     p->split = split;
@@ -515,12 +578,21 @@ tdc_status forward_tc(tdc_conv_plan_s *p, const float *x, float *y, int batch, c
     a3.M = batch * d.Ho * d.Wo;
     a3.out = y;
     if (p->split) s1.mapAlo = s1.mapA;  // unused by the converter path; any valid map
+    auto reduce = [&](int i, int M) -> cudaError_t {
+        tdc::ReduceArgs r = p->red[i];
+        if (r.ksplit <= 1) return cudaSuccess;
+        r.M = M;
+        r.part_stride = (long long)div_up(M, 128) * 128 * r.part_ld;
+        return tdc::splitk_reduce_launch(r, st);
+    };
     cudaError_t e = tdc::tc_gemm_launch(s1.mapA, s1.mapAlo, s1.mapB, s1.mapBlo, a1, s1.grid_n, st);
+    if (e == cudaSuccess) e = reduce(0, a1.M);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-1 launch");
     if (p->tc_core) {
         tdc::TcCoreArgs c = p->core_args;
         c.M = a2.M;
         e = tdc::tc_core_launch(c, st);
+        if (e == cudaSuccess) e = reduce(1, c.M);
         if (e != cudaSuccess)
             return fail(TDC_ERR_CUDA, "tcgen05 core launch: %s (M=%d ntiles=%d BN=%d smem=%d nphase=%d band=%d stages=%d)",
                         cudaGetErrorString(e), c.M, c.ntiles, c.BN,
@@ -528,9 +600,11 @@ tdc_status forward_tc(tdc_conv_plan_s *p, const float *x, float *y, int batch, c
                         c.band_rows, c.b_stages);
     } else {
         e = tdc::tc_gemm_launch(s2.mapA, s2.mapAlo, s2.mapB, s2.mapBlo, a2, s2.grid_n, st);
+        if (e == cudaSuccess) e = reduce(1, a2.M);
     }
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-2 launch");
     e = tdc::tc_gemm_launch(s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, a3, s3.grid_n, st);
+    if (e == cudaSuccess) e = reduce(2, a3.M);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-3 launch");
     return TDC_OK;
 }
@@ -693,7 +767,9 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
                      : tc ? (p->split ? (p->tc_core ? "tc3_3xtf32_band" : "tc3_3xtf32")
                                       : (p->tc_core ? "tc3_tf32_band" : "tc3_tf32"))
                           : "fused_simt_fp32");
-    info->launches_per_forward = (tc ? 3 : 1) + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
+    int nred = 0;
+    for (int i = 0; i < 3; ++i) nred += (tc && p->red[i].ksplit > 1) ? 1 : 0;
+    info->launches_per_forward = (tc ? 3 + nred : 1) + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
     info->concurrent_forward = (p->desc.layout == TDC_LAYOUT_NHWC && !tc) ? 1 : 0;
     info->tile_h = p->simt_tile.oth;
     info->tile_w = p->simt_tile.otw;
@@ -803,6 +879,7 @@ tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t p) {
     cudaFree(p->d_stage_y);
     cudaFree(p->d_tc_w);
     cudaFree(p->d_fw);
+    cudaFree(p->d_part);
     cudaFree(p->d_xg);
     cudaFree(p->d_z);
     delete p;

@@ -156,12 +156,19 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const int iters = g.taps * g.kchunks;
+    // split-K: this CTA reduces the flattened (tap, kc) range [it0, it0 + iters)
+    const int iters_all = g.taps * g.kchunks;
+    int it0 = 0, iters = iters_all;
+    if (g.ksplit > 1) {
+        const int per = (iters_all + g.ksplit - 1) / g.ksplit;
+        it0 = blockIdx.z * per;
+        iters = min(iters_all, it0 + per) - it0;
+    }
 
     if (warp == 0) {  // ------------------------------------- TMA producer
         const uint32_t bytes = (SPLIT && !convert ? 2 : 1) * kATileBytes + (SPLIT ? 2 : 1) * b_tile;
         Ring r(S);
-        int tap = 0, kc = 0;
+        int tap = it0 / g.kchunks, kc = it0 % g.kchunks;
         for (int i = 0; i < iters; ++i, r.next()) {
             mbar_wait(&empty[r.slot], r.phase ^ 1);
             if (elect_one()) {
@@ -209,6 +216,23 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         }
         if (elect_one()) mma_commit(tfull);
         __syncwarp();
+    } else if (warp < 6 && g.ksplit > 1) {  // ------------- epilogue: raw partials
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+        const int q = warp & 3;
+        const int m = m0 + q * 32 + lane;
+        float *dst = g.part + ((long long)blockIdx.z * gridDim.x * kBM + m) * g.part_ld;
+        for (int c = 0; c < BN; c += 32) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
+            tmem_ld_wait();
+            if (m >= g.M || n0 + c >= g.part_ld) continue;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4 *>(dst + n0 + c + j) =
+                    make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+        }
     } else if (warp < 6) {  // --------------------------------- epilogue
         mbar_wait(tfull, 0);
         tc_fence_after();
@@ -324,10 +348,18 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t band_bytes = (uint32_t)g.band_rows * 16;
+    // split-K over the flattened (kc, tap) index f = kc * taps + tap
+    int f0 = 0, f1 = g.kchunks * g.taps;
+    if (g.ksplit > 1) {
+        const int per = (f1 + g.ksplit - 1) / g.ksplit;
+        f0 = blockIdx.z * per;
+        f1 = min(f1, f0 + per);
+    }
+    const int kc_lo = f0 / g.taps, kc_hi = (f1 - 1) / g.taps;
 
     if (warp == 0) {  // ---------------------------------- bulk-copy producer
         Ring ra(2), rb(SB);
-        for (int kc = 0; kc < g.kchunks; ++kc, ra.next()) {
+        for (int kc = kc_lo; kc <= kc_hi; ++kc, ra.next()) {
             mbar_wait(&a_empty[ra.slot], ra.phase ^ 1);
             if (elect_one()) {
                 mbar_arrive_expect_tx(&a_full[ra.slot], a_bytes);
@@ -344,7 +376,9 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
                     }
             }
             __syncwarp();
-            for (int tap = 0; tap < g.taps; ++tap, rb.next()) {
+            const int t_lo = kc == kc_lo ? f0 - kc * g.taps : 0;
+            const int t_hi = kc == kc_hi ? f1 - kc * g.taps : g.taps;
+            for (int tap = t_lo; tap < t_hi; ++tap, rb.next()) {
                 mbar_wait(&b_empty[rb.slot], rb.phase ^ 1);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(&b_full[rb.slot], b_bytes);
@@ -362,9 +396,11 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
         const uint64_t db = sdesc_kmajor_none(smem_u32(b_slots), BN * 16, 128);
         Ring ra(2), rb(SB);
         bool first = true;
-        for (int kc = 0; kc < g.kchunks; ++kc, ra.next()) {
+        for (int kc = kc_lo; kc <= kc_hi; ++kc, ra.next()) {
             mbar_wait(&a_full[ra.slot], ra.phase);
-            for (int tap = 0; tap < g.taps; ++tap, rb.next()) {
+            const int t_lo = kc == kc_lo ? f0 - kc * g.taps : 0;
+            const int t_hi = kc == kc_hi ? f1 - kc * g.taps : g.taps;
+            for (int tap = t_lo; tap < t_hi; ++tap, rb.next()) {
                 mbar_wait(&b_full[rb.slot], rb.phase);
                 tc_fence_after();
                 if (elect_one()) {
@@ -391,6 +427,23 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
         }
         if (elect_one()) mma_commit(tfull);
         __syncwarp();
+    } else if (g.ksplit > 1) {  // ------------------ epilogue: raw partials
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+        const int q = warp & 3;
+        const int m = m0 + q * 32 + lane;
+        float *dst = g.part + ((long long)blockIdx.z * gridDim.x * kBM + m) * g.part_ld;
+        for (int c = 0; c < BN; c += 32) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
+            tmem_ld_wait();
+            if (m >= g.M || n0 + c >= g.part_ld) continue;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4 *>(dst + n0 + c + j) =
+                    make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+        }
     } else {  // --------------------------------- epilogue warps 2..5: Z compact
         mbar_wait(tfull, 0);
         tc_fence_after();
@@ -426,7 +479,7 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
 
 cudaError_t tc_core_launch(const TcCoreArgs &g, cudaStream_t st) {
     const int smem = tc_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.b_stages, g.split);
-    dim3 grid((g.M + kBM - 1) / kBM, g.ntiles);
+    dim3 grid((g.M + kBM - 1) / kBM, g.ntiles, g.ksplit > 1 ? g.ksplit : 1);
     cudaError_t e;
     if (g.split) {
         e = cudaFuncSetAttribute(tdc_tc_core_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -437,6 +490,66 @@ cudaError_t tc_core_launch(const TcCoreArgs &g, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         tdc_tc_core_kernel<false><<<grid, kCoreThreads, smem, st>>>(g);
     }
+    return cudaGetLastError();
+}
+
+// ============================================================ split-K reduce
+// Sums the ksplit partials in a fixed order (deterministic), then applies the
+// producing stage's epilogue: bias, row remap, planar/row-major store, hi/lo split.
+__global__ void __launch_bounds__(256) tdc_splitk_reduce_kernel(const ReduceArgs r) {
+    const int n4 = (r.Nn + 3) >> 2;
+    const long long total = (long long)r.M * n4;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int m = (int)(e / n4), n = (int)(e - (long long)m * n4) * 4;
+        long long dst_row;
+        TcGemmArgs geo;  // reuse the row remap of the GEMM epilogue
+        geo.M = r.M; geo.remap = r.remap; geo.H = r.H; geo.W = r.W; geo.s = r.s; geo.p = r.p;
+        geo.Hq = r.Hq; geo.Wq = r.Wq; geo.Ho = r.Ho; geo.Wo = r.Wo; geo.phase_rows = r.phase_rows;
+        if (!remap_row(geo, m, &dst_row)) continue;
+        const float *src = r.part + (long long)m * r.part_ld + n;
+        float4 acc = *reinterpret_cast<const float4 *>(src);
+        for (int z = 1; z < r.ksplit; ++z) {
+            const float4 v = *reinterpret_cast<const float4 *>(src + z * r.part_stride);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        float v[4] = {acc.x, acc.y, acc.z, acc.w};
+        if (r.bias)
+            for (int j = 0; j < 4; ++j)
+                if (n + j < r.Nn) v[j] += r.bias[n + j];
+        if (r.planar_stride) {
+            const long long off = (long long)(n >> 2) * r.planar_stride + dst_row * 4;
+            if (r.split)
+                split4(v, reinterpret_cast<float4 *>(r.out + off), reinterpret_cast<float4 *>(r.out_lo + off));
+            else
+                *reinterpret_cast<float4 *>(r.out + off) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
+            const long long off = dst_row * r.ldo + n;
+            if (n + 4 <= r.Nn && (r.ldo & 3) == 0) {
+                if (r.split)
+                    split4(v, reinterpret_cast<float4 *>(r.out + off), reinterpret_cast<float4 *>(r.out_lo + off));
+                else
+                    *reinterpret_cast<float4 *>(r.out + off) = make_float4(v[0], v[1], v[2], v[3]);
+            } else {
+                for (int j = 0; j < 4 && n + j < r.Nn; ++j) {
+                    if (r.split) {
+                        const float h = rna_tf32(v[j]);
+                        r.out[off + j] = h;
+                        r.out_lo[off + j] = v[j] - h;
+                    } else {
+                        r.out[off + j] = v[j];
+                    }
+                }
+            }
+        }
+    }
+}
+
+cudaError_t splitk_reduce_launch(const ReduceArgs &r, cudaStream_t st) {
+    const long long total = (long long)r.M * ((r.Nn + 3) / 4);
+    long long blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    tdc_splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(r);
     return cudaGetLastError();
 }
 
@@ -488,7 +601,7 @@ cudaError_t tc_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo,
                            const CUtensorMap &mapB, const CUtensorMap &mapBlo, const TcGemmArgs &g,
                            int grid_n, cudaStream_t st) {
     const int smem = tc_smem_bytes(g.BN, g.stages, g.split);
-    dim3 grid((g.M + kBM - 1) / kBM, grid_n);
+    dim3 grid((g.M + kBM - 1) / kBM, grid_n, g.ksplit > 1 ? g.ksplit : 1);
     cudaError_t e;
     if (g.split) {
         e = cudaFuncSetAttribute(tdc_tc_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
