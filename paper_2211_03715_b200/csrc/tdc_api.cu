@@ -392,6 +392,7 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
         p->tc_ws_bytes += part_elems * sizeof(float);
         p->tc[0].args.part = p->tc[1].args.part = p->tc[2].args.part = p->d_part;
         p->core_args.part = p->d_part;
+        for (int i = 0; i < 3; ++i) p->red[i].part = p->d_part;
     }
     p->variant = 2;
     p->split = split;
