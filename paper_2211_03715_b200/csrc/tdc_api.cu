@@ -155,7 +155,11 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     // Widest N tile: a tcgen05.mma costs ~130-150 cycles whatever N <= 256 is
     // (DESIGN.md §8), so N = 256 does 8x the work of N = 32 per instruction.
     // Parallelism lost to wide tiles is restored with split-K below.
-    auto wide_bn = [](int nn) { return std::min(256, round_up(nn, 32)); };
+    auto wide_bn = [](int nn) {  // power of two: it is also the TMEM allocation
+        int b = 32;
+        while (b < nn && b < 256) b *= 2;
+        return b;
+    };
     int BN1 = wide_bn(D1s);
     int BN2 = wide_bn(D2s);
     const int BN3 = wide_bn(N);

@@ -135,7 +135,8 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
-    const uint32_t ncols = BN < 32 ? 32 : BN;
+    uint32_t ncols = 32;  // TMEM allocations are powers of two >= 32
+    while ((int)ncols < BN) ncols *= 2;
     const bool convert = SPLIT && g.a_convert;
 
     if (threadIdx.x == 0) {
@@ -328,7 +329,8 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * kBM, nt = blockIdx.y, n0 = nt * BN;
-    const uint32_t ncols = BN < 32 ? 32 : BN;
+    uint32_t ncols = 32;  // TMEM allocations are powers of two >= 32
+    while ((int)ncols < BN) ncols *= 2;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
