@@ -588,6 +588,7 @@ tdc_status forward_tc(tdc_conv_plan_s *p, const float *x, float *y, int batch, c
         if (r.ksplit <= 1) return cudaSuccess;
         r.M = M;
         r.part_stride = (long long)div_up(M, 128) * 128 * r.part_ld;
+        if (i == 2) r.out = y;  // the layer output is only known per forward
         return tdc::splitk_reduce_launch(r, st);
     };
     cudaError_t e = tdc::tc_gemm_launch(s1.mapA, s1.mapAlo, s1.mapB, s1.mapBlo, a1, s1.grid_n, st);
