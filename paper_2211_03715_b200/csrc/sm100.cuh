@@ -184,6 +184,33 @@ __device__ __forceinline__ void tmem_ld_wait() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// ------------------------------------------------------------ epilogue store
+// Warp-cooperative store of a 32 x 32 fp32 block whose row `lane` is held by
+// lane `lane` (the tcgen05.ld 32x32b layout): transpose through a 4 KB
+// per-warp scratch (16-byte XOR swizzle, conflict-free both ways) so that every
+// global store instruction writes four full 128-byte row segments instead of
+// 32 scattered 16-byte pieces.  row_ptr: this lane's destination row (already
+// offset to the column block), nullptr to skip the row.
+__device__ __forceinline__ void warp_store_block32(float *scratch, const float (&v)[32],
+                                                   float *row_ptr, int lane) {
+    float4 *s4 = reinterpret_cast<float4 *>(scratch);
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4)
+        s4[lane * 8 + (c4 ^ (lane & 7))] =
+            make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+    __syncwarp();
+    const int c4 = lane & 7;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int r = i * 4 + (lane >> 3);
+        float *dst = reinterpret_cast<float *>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(row_ptr), r));
+        const float4 val = s4[r * 8 + (c4 ^ (r & 7))];
+        if (dst) reinterpret_cast<float4 *>(dst)[c4] = val;
+    }
+    __syncwarp();
+}
+
 // ------------------------------------------------------------ descriptors
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"):
 //   [0,14) start>>4, [16,30) LBO>>4, [32,46) SBO>>4, [46,48) version=1,

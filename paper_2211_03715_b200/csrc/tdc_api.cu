@@ -155,14 +155,20 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     // Widest N tile: a tcgen05.mma costs ~130-150 cycles whatever N <= 256 is
     // (DESIGN.md §8), so N = 256 does 8x the work of N = 32 per instruction.
     // Parallelism lost to wide tiles is restored with split-K below.
-    auto wide_bn = [](int nn) {  // power of two: it is also the TMEM allocation
+    // Measured (r01 launch lists): at batch 32 the small-image stages are bound
+    // by per-CTA fixed costs, so narrower tiles that spread work over more SMs
+    // beat wide tiles + split-K (split-K stays available via TDC_SPLITK=1).
+    const bool wide = getenv("TDC_SPLITK") != nullptr;
+    auto pick = [&](int nn, long long mrows) {
         int b = 32;
-        while (b < nn && b < 256) b *= 2;
+        while (b < nn && b < 256) b *= 2;  // power of two: also the TMEM allocation
+        if (!wide)
+            while (b > 64 && div_up((int)mrows, 128) * (long long)div_up(nn, b) < 2 * p->num_sms) b /= 2;
         return b;
     };
-    int BN1 = wide_bn(D1s);
-    int BN2 = wide_bn(D2s);
-    const int BN3 = wide_bn(N);
+    int BN1 = pick(D1s, M1);
+    int BN2 = pick(D2s, M2);
+    const int BN3 = pick(N, M3);
     const int KK = K * K;
 
     // Stage-2 kernel choice: band-resident core kernel if its two A slots fit.
@@ -343,7 +349,7 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     // ---- split-K: fill the SMs when a stage has few output tiles ----
     auto choose_ksplit = [&](long long mrows, int ntiles, int iters) {
         const long long ctas = div_up((int)mrows, 128) * (long long)ntiles;
-        if (ctas >= p->num_sms || iters < 4) return 1;
+        if (!wide || ctas >= p->num_sms || iters < 4) return 1;
         int k = (int)std::min<long long>(div_up(p->num_sms, (int)ctas), std::min(16, iters / 2));
         if (k < 2) return 1;
         const int per = div_up(iters, k);

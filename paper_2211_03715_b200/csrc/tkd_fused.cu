@@ -65,9 +65,11 @@ __host__ __device__ inline int fused_w_slot_bytes(const FusedArgs &g) {
     return r * 128;
 }
 
+constexpr int kEpiScratchF = 4 * 4096;  // epilogue-3 warps' 32x32 transpose blocks
+
 int fused_smem_bytes(const FusedArgs &g) {
     return 1024 + g.XS * g.nblk1 * (int)kXBlockBytes + g.WS * fused_w_slot_bytes(g) +
-           g.TR * g.D1s * 4 + (2 * g.XS + 2 * g.WS + 6) * 8 + 16;
+           g.TR * g.D1s * 4 + kEpiScratchF + (2 * g.XS + 2 * g.WS + 6) * 8 + 16;
 }
 
 __global__ void __launch_bounds__(kFusedThreads, 1)
@@ -80,7 +82,8 @@ tdc_tkd_fused_tc_kernel(const __grid_constant__ CUtensorMap mapX, const FusedArg
     uint8_t *x_ring = smem;
     uint8_t *w_ring = x_ring + (size_t)g.XS * x_slot;
     uint8_t *x1 = w_ring + (size_t)g.WS * w_slot;
-    uint64_t *x_full = reinterpret_cast<uint64_t *>(x1 + (size_t)g.TR * g.D1s * 4);
+    float *epi_scratch = reinterpret_cast<float *>(x1 + (size_t)g.TR * g.D1s * 4);
+    uint64_t *x_full = reinterpret_cast<uint64_t *>(x1 + (size_t)g.TR * g.D1s * 4 + kEpiScratchF);
     uint64_t *x_empty = x_full + g.XS;
     uint64_t *w_full = x_empty + g.XS;
     uint64_t *w_empty = w_full + g.WS;
@@ -322,6 +325,7 @@ tdc_tkd_fused_tc_kernel(const __grid_constant__ CUtensorMap mapX, const FusedArg
                 tc_fence_after();
                 if (warp == 8 && lane == 0 && h == 0) TL(it, 12);  // acc3 full seen
                 const uint32_t acc3 = tmem + lane_base + g.acc3_col + ab * g.P3 * g.Nh;
+                float *scratch = epi_scratch + q * 1024;
                 for (int c = 0; c < g.Nh; c += 32) {
                     uint32_t r[32];
                     tmem_ld_32x32b_x32(acc3 + c, r);
@@ -335,21 +339,15 @@ tdc_tkd_fused_tc_kernel(const __grid_constant__ CUtensorMap mapX, const FusedArg
                             r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
                     }
                     const int n = h * g.Nh + c;
-                    if (!valid || n >= g.N) continue;
-                    if (vec && n + 32 <= g.N) {
+                    if (n >= g.N) continue;  // warp-uniform
+                    float v[32];
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4) {
-                            float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                   __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-                            if (g.bias) {
-                                const float4 bb = __ldg(reinterpret_cast<const float4 *>(g.bias + n + j));
-                                v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
-                            }
-                            *reinterpret_cast<float4 *>(dst + n + j) = v;
-                        }
-                    } else {
-                        for (int j = 0; j < 32 && n + j < g.N; ++j)
-                            dst[n + j] = __uint_as_float(r[j]) + (g.bias ? g.bias[n + j] : 0.f);
+                    for (int j = 0; j < 32; ++j)
+                        v[j] = __uint_as_float(r[j]) + (g.bias && n + j < g.N ? __ldg(g.bias + n + j) : 0.f);
+                    if (vec && n + 32 <= g.N) {  // coalesced through shared memory
+                        warp_store_block32(scratch, v, valid ? dst + n : nullptr, lane);
+                    } else if (valid) {
+                        for (int j = 0; j < 32 && n + j < g.N; ++j) dst[n + j] = v[j];
                     }
                 }
                 tc_fence_before();

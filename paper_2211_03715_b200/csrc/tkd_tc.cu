@@ -41,6 +41,26 @@ using namespace sm100;
 constexpr int kBM = 128;
 constexpr int kBK = 32;                     // fp32 elements per K chunk = one 128 B swizzle row
 constexpr int kATileBytes = kBM * kBK * 4;  // 16 KB
+constexpr int kEpiScratch = 4 * 4096;      // 4 epilogue warps x 32x32 fp32 transpose blocks
+
+#ifdef TDC_TIMELINE
+// Debug build only: per-CTA %globaltimer stamps [cta][8] of the GEMM kernel.
+__device__ unsigned long long g_tdc_gemm_tl[4096 * 8];
+__device__ __forceinline__ void gtl(int ev) {
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (cta < 4096) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_tdc_gemm_tl[cta * 8 + ev] = t;
+    }
+}
+extern "C" int tdc_debug_gemm_timeline(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_tdc_gemm_tl, sizeof(unsigned long long) * n);
+}
+#define GTL(ev) gtl(ev)
+#else
+#define GTL(ev) ((void)0)
+#endif
 
 __device__ __forceinline__ float rna_tf32(float x) {
     uint32_t r;
@@ -127,7 +147,8 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     const uint32_t b_tile = (uint32_t)BN * kBK * 4;
     const uint32_t slot_bytes = (SPLIT ? 2 : 1) * (kATileBytes + b_tile);
     // slot layout: A hi | B hi | [A lo | B lo]
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * slot_bytes);
+    float *epi_scratch = reinterpret_cast<float *>(smem + (size_t)S * slot_bytes);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * slot_bytes + kEpiScratch);
     uint64_t *conv = full + S;
     uint64_t *empty = conv + S;
     uint64_t *tfull = empty + S;
@@ -138,6 +159,7 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     uint32_t ncols = 32;  // TMEM allocations are powers of two >= 32
     while ((int)ncols < BN) ncols *= 2;
     const bool convert = SPLIT && g.a_convert;
+    if (threadIdx.x == 0) GTL(0);  // CTA start
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -156,6 +178,7 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (threadIdx.x == 0) GTL(1);  // setup done (barriers + TMEM)
     const uint32_t tmem = *tmem_slot;
     // split-K: this CTA reduces the flattened (tap, kc) range [it0, it0 + iters)
     const int iters_all = g.taps * g.kchunks;
@@ -200,6 +223,7 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         for (int i = 0; i < iters; ++i, r.next()) {
             mbar_wait(convert ? &conv[r.slot] : &full[r.slot], r.phase);
             tc_fence_after();
+            if (i == 0 && lane == 0) GTL(2);  // first operands ready
             if (elect_one()) {
                 const uint64_t a = da + ((r.slot * slot_bytes) >> 4);
                 const uint64_t b = db + ((r.slot * slot_bytes) >> 4);
@@ -217,6 +241,7 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         }
         if (elect_one()) mma_commit(tfull);
         __syncwarp();
+        if (lane == 0) GTL(3);  // all MMAs issued
     } else if (warp < 6 && g.ksplit > 1) {  // ------------- epilogue: raw partials
         mbar_wait(tfull, 0);
         tc_fence_after();
@@ -237,6 +262,7 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     } else if (warp < 6) {  // --------------------------------- epilogue
         mbar_wait(tfull, 0);
         tc_fence_after();
+        if (warp == 2 && lane == 0) GTL(4);  // accumulator ready
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int row = q * 32 + lane;
         long long dst_row = 0;
@@ -244,12 +270,14 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         const long long off = g.planar_stride ? dst_row * 4 : dst_row * g.ldo;
         float *dst = g.out + off;
         float *dst_lo = (SPLIT && g.out_lo) ? g.out_lo + off : nullptr;
+        float *scratch = epi_scratch + q * 1024;
+        const bool rowmajor_vec = !g.planar_stride && (g.ldo & 3) == 0;
         for (int c = 0; c < BN; c += 32) {
             uint32_t r[32];
             tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
             tmem_ld_wait();
             const int n = n0 + c;
-            if (!valid || n >= g.Nn) continue;
+            if (n >= g.Nn) continue;  // warp-uniform
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
@@ -258,7 +286,22 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                 for (int j = 0; j < 32; ++j)
                     if (n + j < g.Nn) v[j] += __ldg(&g.bias[n + j]);
             }
-            store_row32(dst, dst_lo, g.planar_stride, n, g.Nn, (g.ldo & 3) == 0, v, dst_lo != nullptr);
+            if (rowmajor_vec && n + 32 <= g.Nn) {  // coalesced through shared memory
+                if (dst_lo) {
+                    float h[32], l[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        h[j] = rna_tf32(v[j]);
+                        l[j] = v[j] - h[j];
+                    }
+                    warp_store_block32(scratch, h, valid ? dst + n : nullptr, lane);
+                    warp_store_block32(scratch, l, valid ? dst_lo + n : nullptr, lane);
+                } else {
+                    warp_store_block32(scratch, v, valid ? dst + n : nullptr, lane);
+                }
+            } else if (valid) {
+                store_row32(dst, dst_lo, g.planar_stride, n, g.Nn, (g.ldo & 3) == 0, v, dst_lo != nullptr);
+            }
         }
     } else if (convert) {  // ------------------------ converter (3xTF32 stage 1)
         const int t = threadIdx.x - 192;  // 0..127: each owns 128 contiguous bytes of A
@@ -278,14 +321,16 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             mbar_arrive(&conv[r.slot]);
         }
     }
+    if (warp == 2 && lane == 0) GTL(5);  // epilogue stores issued
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, ncols);
+    if (threadIdx.x == 64) GTL(6);  // CTA end
 }
 
 int tc_smem_bytes(int BN, int stages, int split) {
     return 1024 /*align slack*/ + stages * (split ? 2 : 1) * (kATileBytes + BN * kBK * 4) +
-           (3 * stages + 1) * 8 + 16;
+           kEpiScratch + (3 * stages + 1) * 8 + 16;
 }
 
 int tc_pick_stages(int BN, int iters, int max_smem, int split) {
@@ -305,7 +350,7 @@ __host__ __device__ inline int core_a_slot_bytes(int nphase, int band_rows) {
 int tc_core_smem_bytes(int BN, int nphase, int band_rows, int b_stages, int split) {
     const int f = split ? 2 : 1;
     return 1024 + 2 * f * core_a_slot_bytes(nphase, band_rows) + b_stages * f * BN * 128 +
-           (4 + 2 * b_stages + 1) * 8 + 16;
+           kEpiScratch + (4 + 2 * b_stages + 1) * 8 + 16;
 }
 
 template <bool SPLIT>
@@ -320,7 +365,8 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
     const uint32_t b_bytes = b_half * (SPLIT ? 2 : 1);
     uint8_t *a_slots = smem;
     uint8_t *b_slots = smem + 2 * (size_t)a_bytes;
-    uint64_t *a_full = reinterpret_cast<uint64_t *>(b_slots + (size_t)SB * b_bytes);
+    float *epi_scratch = reinterpret_cast<float *>(b_slots + (size_t)SB * b_bytes);
+    uint64_t *a_full = reinterpret_cast<uint64_t *>(b_slots + (size_t)SB * b_bytes + kEpiScratch);
     uint64_t *a_empty = a_full + 2;
     uint64_t *b_full = a_empty + 2;
     uint64_t *b_empty = b_full + SB;
@@ -463,15 +509,27 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
         }
         float *dst = g.z + dst_row * g.ldz;
         float *dst_lo = SPLIT ? g.z_lo + dst_row * g.ldz : nullptr;
+        float *scratch = epi_scratch + q * 1024;
         for (int c = 0; c < BN; c += 32) {
             uint32_t r[32];
             tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
             tmem_ld_wait();
-            if (!valid || n0 + c >= g.Nn) continue;
+            if (n0 + c >= g.Nn) continue;  // warp-uniform
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-            store_row32(dst, dst_lo, 0, n0 + c, g.Nn, true, v, SPLIT);
+            if (SPLIT) {
+                float h[32], l[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    h[j] = rna_tf32(v[j]);
+                    l[j] = v[j] - h[j];
+                }
+                warp_store_block32(scratch, h, valid ? dst + n0 + c : nullptr, lane);
+                warp_store_block32(scratch, l, valid ? dst_lo + n0 + c : nullptr, lane);
+            } else {
+                warp_store_block32(scratch, v, valid ? dst + n0 + c : nullptr, lane);
+            }
         }
     }
     tc_fence_before();
