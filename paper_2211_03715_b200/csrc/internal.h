@@ -50,9 +50,7 @@ struct TcGemmArgs {
     int split;        // 1: 3xTF32 (hi*hi + hi*lo + lo*hi), fp32-grade accuracy
     int a_convert;    // split only: 1 = A lo computed in-kernel from A (user input); 0 = loaded
     float *out_lo;    // split only: epilogue also writes the lo part of the output (next stage's A lo)
-    int ksplit;       // >1: split-K over blockIdx.z; raw partials go to part[z][row][part_ld]
-    float *part;
-    int part_ld;
+    int ntiles;       // N tiles (persistent kernel walks mtiles x ntiles)
 };
 
 // Stage-2 core convolution with a shared-memory-resident X' band (tkd_tc.cu):
@@ -73,36 +71,20 @@ struct TcCoreArgs {
     const float *xg_lo;        // split: X' lo planes
     const float *w_lo;         // split: blocked core weights, lo parts
     float *z_lo;               // split: Z lo (next stage's A lo)
-    int ksplit;                // >1: split-K over blockIdx.z (flattened (kc, tap) range)
-    float *part;               // raw partials [z][output-grid row][part_ld]
-    int part_ld;
 };
 
-// Deterministic split-K reduction + the producing kernel's epilogue semantics:
-// out(row remap) = sum_{z in order} part[z][m][n] (+bias), optional hi/lo split.
-struct ReduceArgs {
-    const float *part;
-    int ksplit, M, Nn, part_ld;
-    long long part_stride;     // floats between splits
-    float *out, *out_lo;
-    int ldo;
-    long long planar_stride;   // >0: out is planar [n/4][row][4]
-    const float *bias;
-    int remap;                 // 0 identity, 1 pixel -> phase grid, 2 output grid -> compact
-    int H, W, s, p, Hq, Wq, Ho, Wo;
-    long long phase_rows;
-    int split;                 // write hi = rna_tf32(v), lo = v - hi
-};
-cudaError_t splitk_reduce_launch(const ReduceArgs &r, cudaStream_t st);
+
 int tc_core_smem_bytes(int BN, int nphase, int band_rows, int b_stages, int split);
-cudaError_t tc_core_launch(const TcCoreArgs &g, cudaStream_t st);
+cudaError_t tc_core_launch(const TcCoreArgs &g, int grid, cudaStream_t st);
+// CTAs per SM for a persistent kernel given its smem and TMEM (2 x ncols) footprint.
+int persistent_occupancy(int smem_bytes, int bn);
 int tc_smem_bytes(int BN, int stages, int split);
 int tc_pick_stages(int BN, int iters, int max_smem, int split);
 bool make_tma_2d(CUtensorMap *map, const float *base, long long rows, int k_extent, int pitch,
                  int box_rows);
 cudaError_t tc_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo,
                            const CUtensorMap &mapB, const CUtensorMap &mapBlo, const TcGemmArgs &g,
-                           int grid_n, cudaStream_t st);
+                           int grid, cudaStream_t st);
 
 // ---- fused single-kernel TKD layer (tkd_fused.cu) ----
 struct FusedArgs {

@@ -111,8 +111,7 @@ struct tdc_conv_plan_s {
     int fgrid = 0, num_sms = 148;
     bool tc_core = false;          // stage 2 uses the band-resident core kernel
     bool split = false;            // 3xTF32
-    float *d_part = nullptr;       // split-K partials (shared by the three stages)
-    tdc::ReduceArgs red[3];        // per-stage reduce (used when that stage's ksplit > 1)
+
     tdc::TcCoreArgs core_args;
     float *d_tc_w = nullptr;       // Bt1 | Bt2 | Bt3 | bias
     float *d_xg = nullptr;         // X' phase grids (zero borders)
@@ -155,15 +154,12 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     // Widest N tile: a tcgen05.mma costs ~130-150 cycles whatever N <= 256 is
     // (DESIGN.md §8), so N = 256 does 8x the work of N = 32 per instruction.
     // Parallelism lost to wide tiles is restored with split-K below.
-    // Measured (r01 launch lists): at batch 32 the small-image stages are bound
-    // by per-CTA fixed costs, so narrower tiles that spread work over more SMs
-    // beat wide tiles + split-K (split-K stays available via TDC_SPLITK=1).
-    const bool wide = getenv("TDC_SPLITK") != nullptr;
+    // N tile: a power of two (it is also the TMEM allocation), narrowed while the
+    // stage has fewer than 2 tiles per SM so small-image stages spread over the GPU.
     auto pick = [&](int nn, long long mrows) {
         int b = 32;
-        while (b < nn && b < 256) b *= 2;  // power of two: also the TMEM allocation
-        if (!wide)
-            while (b > 64 && div_up((int)mrows, 128) * (long long)div_up(nn, b) < 2 * p->num_sms) b /= 2;
+        while (b < nn && b < 256) b *= 2;
+        while (b > 64 && div_up((int)mrows, 128) * (long long)div_up(nn, b) < 2 * p->num_sms) b /= 2;
         return b;
     };
     int BN1 = pick(D1s, M1);
@@ -278,6 +274,7 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
         st.args.out_lo = xg_lo;
         st.args.stages = tdc::tc_pick_stages(BN1, Cs / 32, p->max_smem, sp);
         st.grid_n = R1 / BN1;
+        st.args.ntiles = st.grid_n;
         if (!tdc::make_tma_2d(&st.mapB, dB1, R1, Cs, Cs, BN1) ||
             (split && !tdc::make_tma_2d(&st.mapBlo, dB1lo, R1, Cs, Cs, BN1)))
             return fail(TDC_ERR_CUDA, "%s (stage-1 weights)", enc_err);
@@ -314,6 +311,7 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
             }
         st.args.stages = tdc::tc_pick_stages(BN2, KK * D1s / 32, p->max_smem, sp);
         st.grid_n = R2 / BN2;
+        st.args.ntiles = st.grid_n;
         if (!tdc::make_tma_2d(&st.mapA, p->d_xg, (long long)s * s * phase_rows, D1s, D1s, 128) ||
             !tdc::make_tma_2d(&st.mapB, dB2, (long long)KK * R2, D1s, D1s, BN2))
             return fail(TDC_ERR_CUDA, "%s (stage 2)", enc_err);
@@ -334,6 +332,7 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
         st.args.BN = BN3; st.args.ldo = N; st.args.remap = 0; st.args.bias = bias ? dbias : nullptr;
         st.args.stages = tdc::tc_pick_stages(BN3, D2s / 32, p->max_smem, sp);
         st.grid_n = R3 / BN3;
+        st.args.ntiles = st.grid_n;
         if (!tdc::make_tma_2d(&st.mapA, p->d_z, M3, D2s, D2s, 128) ||
             !tdc::make_tma_2d(&st.mapB, dB3, R3, D2s, D2s, BN3))
             return fail(TDC_ERR_CUDA, "%s (stage 3)", enc_err);
@@ -345,64 +344,6 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
             st.mapAlo = st.mapA;
             st.mapBlo = st.mapB;
         }
-    }
-    // ---- split-K: fill the SMs when a stage has few output tiles ----
-    auto choose_ksplit = [&](long long mrows, int ntiles, int iters) {
-        const long long ctas = div_up((int)mrows, 128) * (long long)ntiles;
-        if (!wide || ctas >= p->num_sms || iters < 4) return 1;
-        int k = (int)std::min<long long>(div_up(p->num_sms, (int)ctas), std::min(16, iters / 2));
-        if (k < 2) return 1;
-        const int per = div_up(iters, k);
-        return div_up(iters, per);  // no empty splits
-    };
-    size_t part_elems = 0;
-    auto set_reduce = [&](int i, const tdc::TcGemmArgs &a, int part_ld, int ks) {
-        tdc::ReduceArgs &r = p->red[i];
-        std::memset(&r, 0, sizeof r);
-        r.ksplit = ks; r.M = a.M; r.Nn = a.Nn; r.part_ld = part_ld;
-        r.out = a.out; r.out_lo = a.out_lo; r.ldo = a.ldo; r.planar_stride = a.planar_stride;
-        r.bias = a.bias; r.remap = a.remap; r.H = a.H; r.W = a.W; r.s = a.s; r.p = a.p;
-        r.Hq = a.Hq; r.Wq = a.Wq; r.Ho = a.Ho; r.Wo = a.Wo; r.phase_rows = a.phase_rows;
-        r.split = split && a.out_lo ? 1 : 0;
-        part_elems = std::max(part_elems, (size_t)ks * round_up(a.M, 128) * part_ld);
-    };
-    {
-        auto &a = p->tc[0].args;
-        a.ksplit = choose_ksplit(M1, p->tc[0].grid_n, a.taps * a.kchunks);
-        a.part_ld = p->tc[0].grid_n * BN1;
-        if (a.ksplit > 1) set_reduce(0, a, a.part_ld, a.ksplit);
-    }
-    if (p->tc_core) {
-        auto &c = p->core_args;
-        c.ksplit = choose_ksplit(M2, c.ntiles, c.kchunks * c.taps);
-        c.part_ld = c.ntiles * c.BN;
-        if (c.ksplit > 1) {
-            tdc::TcGemmArgs geo;
-            std::memset(&geo, 0, sizeof geo);
-            geo.M = c.M; geo.Nn = c.Nn; geo.out = c.z; geo.out_lo = c.z_lo; geo.ldo = c.ldz;
-            geo.remap = 2; geo.Hq = Hq; geo.Wq = Wq; geo.Ho = Ho; geo.Wo = Wo; geo.H = H; geo.W = W;
-            geo.s = s; geo.p = pad; geo.phase_rows = phase_rows;
-            set_reduce(1, geo, c.part_ld, c.ksplit);
-        }
-    } else {
-        auto &a = p->tc[1].args;
-        a.ksplit = choose_ksplit(M2, p->tc[1].grid_n, a.taps * a.kchunks);
-        a.part_ld = p->tc[1].grid_n * BN2;
-        if (a.ksplit > 1) set_reduce(1, a, a.part_ld, a.ksplit);
-    }
-    {
-        auto &a = p->tc[2].args;
-        a.ksplit = choose_ksplit(M3, p->tc[2].grid_n, a.taps * a.kchunks);
-        a.part_ld = p->tc[2].grid_n * BN3;
-        if (a.ksplit > 1) set_reduce(2, a, a.part_ld, a.ksplit);
-    }
-    if (part_elems) {
-        e = cudaMalloc(&p->d_part, part_elems * sizeof(float));
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(split-K partials)");
-        p->tc_ws_bytes += part_elems * sizeof(float);
-        p->tc[0].args.part = p->tc[1].args.part = p->tc[2].args.part = p->d_part;
-        p->core_args.part = p->d_part;
-        for (int i = 0; i < 3; ++i) p->red[i].part = p->d_part;
     }
     p->variant = 2;
     p->split = split;
@@ -589,34 +530,32 @@ tdc_status forward_tc(tdc_conv_plan_s *p, const float *x, float *y, int batch, c
     a3.M = batch * d.Ho * d.Wo;
     a3.out = y;
     if (p->split) s1.mapAlo = s1.mapA;  // unused by the converter path; any valid map
-    auto reduce = [&](int i, int M) -> cudaError_t {
-        tdc::ReduceArgs r = p->red[i];
-        if (r.ksplit <= 1) return cudaSuccess;
-        r.M = M;
-        r.part_stride = (long long)div_up(M, 128) * 128 * r.part_ld;
-        if (i == 2) r.out = y;  // the layer output is only known per forward
-        return tdc::splitk_reduce_launch(r, st);
+    auto grid_of = [&](const tdc::TcGemmArgs &a) {
+        const long long tiles = (long long)div_up(a.M, 128) * a.ntiles;
+        const long long cap = (long long)p->num_sms *
+                              tdc::persistent_occupancy(tdc::tc_smem_bytes(a.BN, a.stages, a.split), a.BN);
+        return (int)std::max<long long>(1, std::min(tiles, cap));
     };
-    cudaError_t e = tdc::tc_gemm_launch(s1.mapA, s1.mapAlo, s1.mapB, s1.mapBlo, a1, s1.grid_n, st);
-    if (e == cudaSuccess) e = reduce(0, a1.M);
+    cudaError_t e = tdc::tc_gemm_launch(s1.mapA, s1.mapAlo, s1.mapB, s1.mapBlo, a1, grid_of(a1), st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-1 launch");
     if (p->tc_core) {
         tdc::TcCoreArgs c = p->core_args;
         c.M = a2.M;
-        e = tdc::tc_core_launch(c, st);
-        if (e == cudaSuccess) e = reduce(1, c.M);
+        const long long tiles = (long long)div_up(c.M, 128) * c.ntiles;
+        const long long cap = (long long)p->num_sms *
+                              tdc::persistent_occupancy(tdc::tc_core_smem_bytes(c.BN, c.nphase, c.band_rows,
+                                                                                c.b_stages, c.split), c.BN);
+        e = tdc::tc_core_launch(c, (int)std::max<long long>(1, std::min(tiles, cap)), st);
         if (e != cudaSuccess)
             return fail(TDC_ERR_CUDA, "tcgen05 core launch: %s (M=%d ntiles=%d BN=%d smem=%d nphase=%d band=%d stages=%d)",
                         cudaGetErrorString(e), c.M, c.ntiles, c.BN,
                         tdc::tc_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.b_stages, c.split), c.nphase,
                         c.band_rows, c.b_stages);
     } else {
-        e = tdc::tc_gemm_launch(s2.mapA, s2.mapAlo, s2.mapB, s2.mapBlo, a2, s2.grid_n, st);
-        if (e == cudaSuccess) e = reduce(1, a2.M);
+        e = tdc::tc_gemm_launch(s2.mapA, s2.mapAlo, s2.mapB, s2.mapBlo, a2, grid_of(a2), st);
     }
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-2 launch");
-    e = tdc::tc_gemm_launch(s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, a3, s3.grid_n, st);
-    if (e == cudaSuccess) e = reduce(2, a3.M);
+    e = tdc::tc_gemm_launch(s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, a3, grid_of(a3), st);
     if (e != cudaSuccess) return cuda_fail(e, "tcgen05 stage-3 launch");
     return TDC_OK;
 }
@@ -779,9 +718,7 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
                      : tc ? (p->split ? (p->tc_core ? "tc3_3xtf32_band" : "tc3_3xtf32")
                                       : (p->tc_core ? "tc3_tf32_band" : "tc3_tf32"))
                           : "fused_simt_fp32");
-    int nred = 0;
-    for (int i = 0; i < 3; ++i) nred += (tc && p->red[i].ksplit > 1) ? 1 : 0;
-    info->launches_per_forward = (tc ? 3 + nred : 1) + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
+    info->launches_per_forward = (tc ? 3 : 1) + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
     info->concurrent_forward = (p->desc.layout == TDC_LAYOUT_NHWC && !tc) ? 1 : 0;
     info->tile_h = p->simt_tile.oth;
     info->tile_w = p->simt_tile.otw;
@@ -891,7 +828,6 @@ tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t p) {
     cudaFree(p->d_stage_y);
     cudaFree(p->d_tc_w);
     cudaFree(p->d_fw);
-    cudaFree(p->d_part);
     cudaFree(p->d_xg);
     cudaFree(p->d_z);
     delete p;

@@ -41,7 +41,6 @@ using namespace sm100;
 constexpr int kBM = 128;
 constexpr int kBK = 32;                     // fp32 elements per K chunk = one 128 B swizzle row
 constexpr int kATileBytes = kBM * kBK * 4;  // 16 KB
-constexpr int kEpiScratch = 4 * 4096;      // 4 epilogue warps x 32x32 fp32 transpose blocks
 
 #ifdef TDC_TIMELINE
 // Debug build only: per-CTA %globaltimer stamps [cta][8] of the GEMM kernel.
@@ -135,6 +134,13 @@ __device__ __forceinline__ void store_row32(float *dst, float *dst_lo, long long
 }
 
 // ============================================================ GEMM with taps
+// Persistent: each CTA walks tiles t = blockIdx.x, += gridDim.x (M-tile fastest,
+// so concurrently running CTAs share a weight tile in L2).  The TMEM accumulator
+// is double-buffered, so the epilogue of tile i (TMEM -> global) overlaps the
+// loads and MMAs of tile i+1 and HBM sees reads and writes interleaved instead
+// of the lock-step load/compute/store waves of a one-tile-per-CTA launch.
+constexpr int kEpiScratch = 4 * 4096;  // 4 epilogue warps x 32x32 fp32 transpose blocks
+
 template <bool SPLIT>
 __global__ void __launch_bounds__(SPLIT ? 320 : 192, 1)
 tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
@@ -151,14 +157,17 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * slot_bytes + kEpiScratch);
     uint64_t *conv = full + S;
     uint64_t *empty = conv + S;
-    uint64_t *tfull = empty + S;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfull + 1);
+    uint64_t *tfull = empty + S;    // [2]
+    uint64_t *tempty = tfull + 2;   // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
     uint32_t ncols = 32;  // TMEM allocations are powers of two >= 32
     while ((int)ncols < BN) ncols *= 2;
     const bool convert = SPLIT && g.a_convert;
+    const int mtiles = (g.M + kBM - 1) / kBM;
+    const int num_tiles = mtiles * g.ntiles;
+    const int iters = g.taps * g.kchunks;
     if (threadIdx.x == 0) GTL(0);  // CTA start
 
     if (threadIdx.x == 0) {
@@ -167,51 +176,49 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             mbar_init(&conv[i], 128);
             mbar_init(&empty[i], 1);
         }
-        mbar_init(tfull, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 128);
+        }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch(&mapA);
         tma_prefetch(&mapB);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, ncols);
+    if (warp == 1) tmem_alloc(tmem_slot, 2 * ncols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (threadIdx.x == 0) GTL(1);  // setup done (barriers + TMEM)
     const uint32_t tmem = *tmem_slot;
-    // split-K: this CTA reduces the flattened (tap, kc) range [it0, it0 + iters)
-    const int iters_all = g.taps * g.kchunks;
-    int it0 = 0, iters = iters_all;
-    if (g.ksplit > 1) {
-        const int per = (iters_all + g.ksplit - 1) / g.ksplit;
-        it0 = blockIdx.z * per;
-        iters = min(iters_all, it0 + per) - it0;
-    }
 
     if (warp == 0) {  // ------------------------------------- TMA producer
         const uint32_t bytes = (SPLIT && !convert ? 2 : 1) * kATileBytes + (SPLIT ? 2 : 1) * b_tile;
         Ring r(S);
-        int tap = it0 / g.kchunks, kc = it0 % g.kchunks;
-        for (int i = 0; i < iters; ++i, r.next()) {
-            mbar_wait(&empty[r.slot], r.phase ^ 1);
-            if (elect_one()) {
-                uint8_t *base = smem + (size_t)r.slot * slot_bytes;
-                mbar_arrive_expect_tx(&full[r.slot], bytes);
-                tma_load_2d(base, &mapA, &full[r.slot], kc * kBK, m0 + g.a_off[tap]);
-                tma_load_2d(base + kATileBytes, &mapB, &full[r.slot], kc * kBK, g.b_off[tap] + n0);
-                if (SPLIT) {
-                    if (!convert)
-                        tma_load_2d(base + kATileBytes + b_tile, &mapAlo, &full[r.slot], kc * kBK,
-                                    m0 + g.a_off[tap]);
-                    tma_load_2d(base + 2 * kATileBytes + b_tile, &mapBlo, &full[r.slot], kc * kBK,
-                                g.b_off[tap] + n0);
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            const int m0 = (t % mtiles) * kBM, n0 = (t / mtiles) * BN;
+            int tap = 0, kc = 0;
+            for (int i = 0; i < iters; ++i, r.next()) {
+                mbar_wait(&empty[r.slot], r.phase ^ 1);
+                if (elect_one()) {
+                    uint8_t *base = smem + (size_t)r.slot * slot_bytes;
+                    mbar_arrive_expect_tx(&full[r.slot], bytes);
+                    tma_load_2d(base, &mapA, &full[r.slot], kc * kBK, m0 + g.a_off[tap]);
+                    tma_load_2d(base + kATileBytes, &mapB, &full[r.slot], kc * kBK, g.b_off[tap] + n0);
+                    if (SPLIT) {
+                        if (!convert)
+                            tma_load_2d(base + kATileBytes + b_tile, &mapAlo, &full[r.slot], kc * kBK,
+                                        m0 + g.a_off[tap]);
+                        tma_load_2d(base + 2 * kATileBytes + b_tile, &mapBlo, &full[r.slot], kc * kBK,
+                                    g.b_off[tap] + n0);
+                    }
                 }
-            }
-            __syncwarp();
-            if (++kc == g.kchunks) {
-                kc = 0;
-                ++tap;
+                __syncwarp();
+                if (++kc == g.kchunks) {
+                    kc = 0;
+                    ++tap;
+                }
             }
         }
     } else if (warp == 1) {  // ------------------------------ MMA issuer
@@ -219,124 +226,130 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         const uint64_t da = sdesc_kmajor_sw128(smem_u32(smem));
         const uint64_t db = sdesc_kmajor_sw128(smem_u32(smem + kATileBytes));
         const uint32_t lo_off = (kATileBytes + b_tile) >> 4;  // hi -> lo, 16-byte units
-        Ring r(S);
-        for (int i = 0; i < iters; ++i, r.next()) {
-            mbar_wait(convert ? &conv[r.slot] : &full[r.slot], r.phase);
+        Ring r(S), acc(2);
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next()) {
+            mbar_wait(&tempty[acc.slot], acc.phase ^ 1);  // epilogue drained this buffer
             tc_fence_after();
-            if (i == 0 && lane == 0) GTL(2);  // first operands ready
-            if (elect_one()) {
-                const uint64_t a = da + ((r.slot * slot_bytes) >> 4);
-                const uint64_t b = db + ((r.slot * slot_bytes) >> 4);
+            const uint32_t d = tmem + acc.slot * ncols;
+            for (int i = 0; i < iters; ++i, r.next()) {
+                mbar_wait(convert ? &conv[r.slot] : &full[r.slot], r.phase);
+                tc_fence_after();
+                if (i == 0 && lane == 0) GTL(2);  // first operands ready
+                if (elect_one()) {
+                    const uint64_t a = da + ((r.slot * slot_bytes) >> 4);
+                    const uint64_t b = db + ((r.slot * slot_bytes) >> 4);
 #pragma unroll
-                for (int j = 0; j < kBK / 8; ++j) {  // K = 8 tf32 = 32 B per MMA
-                    mma_tf32(tmem, a + j * 2, b + j * 2, idesc, (i | j) != 0);
-                    if (SPLIT) {
-                        mma_tf32(tmem, a + j * 2, b + lo_off + j * 2, idesc, 1);  // hi * lo
-                        mma_tf32(tmem, a + lo_off + j * 2, b + j * 2, idesc, 1);  // lo * hi
+                    for (int j = 0; j < kBK / 8; ++j) {  // K = 8 tf32 = 32 B per MMA
+                        mma_tf32(d, a + j * 2, b + j * 2, idesc, (i | j) != 0);
+                        if (SPLIT) {
+                            mma_tf32(d, a + j * 2, b + lo_off + j * 2, idesc, 1);  // hi * lo
+                            mma_tf32(d, a + lo_off + j * 2, b + j * 2, idesc, 1);  // lo * hi
+                        }
                     }
+                    mma_commit(&empty[r.slot]);
                 }
-                mma_commit(&empty[r.slot]);
+                __syncwarp();
             }
+            if (elect_one()) mma_commit(&tfull[acc.slot]);
             __syncwarp();
-        }
-        if (elect_one()) mma_commit(tfull);
-        __syncwarp();
-        if (lane == 0) GTL(3);  // all MMAs issued
-    } else if (warp < 6 && g.ksplit > 1) {  // ------------- epilogue: raw partials
-        mbar_wait(tfull, 0);
-        tc_fence_after();
-        const int q = warp & 3;
-        const int m = m0 + q * 32 + lane;
-        float *dst = g.part + ((long long)blockIdx.z * gridDim.x * kBM + m) * g.part_ld;
-        for (int c = 0; c < BN; c += 32) {
-            uint32_t r[32];
-            tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
-            tmem_ld_wait();
-            if (m >= g.M || n0 + c >= g.part_ld) continue;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4 *>(dst + n0 + c + j) =
-                    make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+            if (lane == 0) GTL(3);  // all MMAs of the tile issued
         }
     } else if (warp < 6) {  // --------------------------------- epilogue
-        mbar_wait(tfull, 0);
-        tc_fence_after();
-        if (warp == 2 && lane == 0) GTL(4);  // accumulator ready
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const int row = q * 32 + lane;
-        long long dst_row = 0;
-        const bool valid = remap_row(g, m0 + row, &dst_row);
-        const long long off = g.planar_stride ? dst_row * 4 : dst_row * g.ldo;
-        float *dst = g.out + off;
-        float *dst_lo = (SPLIT && g.out_lo) ? g.out_lo + off : nullptr;
         float *scratch = epi_scratch + q * 1024;
         const bool rowmajor_vec = !g.planar_stride && (g.ldo & 3) == 0;
-        for (int c = 0; c < BN; c += 32) {
-            uint32_t r[32];
-            tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
-            tmem_ld_wait();
-            const int n = n0 + c;
-            if (n >= g.Nn) continue;  // warp-uniform
-            float v[32];
+        Ring acc(2);
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next()) {
+            const int m0 = (t % mtiles) * kBM, n0 = (t / mtiles) * BN;
+            mbar_wait(&tfull[acc.slot], acc.phase);
+            tc_fence_after();
+            if (warp == 2 && lane == 0) GTL(4);  // accumulator ready
+            long long dst_row = 0;
+            const bool valid = remap_row(g, m0 + q * 32 + lane, &dst_row);
+            const long long off = g.planar_stride ? dst_row * 4 : dst_row * g.ldo;
+            float *dst = g.out + off;
+            float *dst_lo = (SPLIT && g.out_lo) ? g.out_lo + off : nullptr;
+            const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(src + c, r);
+                tmem_ld_wait();
+                const int n = n0 + c;
+                if (n >= g.Nn) continue;  // warp-uniform
+                float v[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-            if (g.bias) {
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                if (g.bias) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (n + j < g.Nn) v[j] += __ldg(&g.bias[n + j]);
-            }
-            if (rowmajor_vec && n + 32 <= g.Nn) {  // coalesced through shared memory
-                if (dst_lo) {
-                    float h[32], l[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        h[j] = rna_tf32(v[j]);
-                        l[j] = v[j] - h[j];
-                    }
-                    warp_store_block32(scratch, h, valid ? dst + n : nullptr, lane);
-                    warp_store_block32(scratch, l, valid ? dst_lo + n : nullptr, lane);
-                } else {
-                    warp_store_block32(scratch, v, valid ? dst + n : nullptr, lane);
+                    for (int j = 0; j < 32; ++j)
+                        if (n + j < g.Nn) v[j] += __ldg(&g.bias[n + j]);
                 }
-            } else if (valid) {
-                store_row32(dst, dst_lo, g.planar_stride, n, g.Nn, (g.ldo & 3) == 0, v, dst_lo != nullptr);
+                if (rowmajor_vec && n + 32 <= g.Nn) {  // coalesced through shared memory
+                    if (dst_lo) {
+                        float h[32], l[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            h[j] = rna_tf32(v[j]);
+                            l[j] = v[j] - h[j];
+                        }
+                        warp_store_block32(scratch, h, valid ? dst + n : nullptr, lane);
+                        warp_store_block32(scratch, l, valid ? dst_lo + n : nullptr, lane);
+                    } else {
+                        warp_store_block32(scratch, v, valid ? dst + n : nullptr, lane);
+                    }
+                } else if (valid) {
+                    store_row32(dst, dst_lo, g.planar_stride, n, g.Nn, (g.ldo & 3) == 0, v,
+                                dst_lo != nullptr);
+                }
             }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc.slot]);
+            if (warp == 2 && lane == 0) GTL(5);  // epilogue stores issued
         }
     } else if (convert) {  // ------------------------ converter (3xTF32 stage 1)
-        const int t = threadIdx.x - 192;  // 0..127: each owns 128 contiguous bytes of A
+        const int tid = threadIdx.x - 192;  // 0..127: each owns 128 contiguous bytes of A
         Ring r(S);
-        for (int i = 0; i < iters; ++i, r.next()) {
-            mbar_wait(&full[r.slot], r.phase);
-            float4 *a = reinterpret_cast<float4 *>(smem + (size_t)r.slot * slot_bytes) + t * 8;
-            float4 *lo = reinterpret_cast<float4 *>(smem + (size_t)r.slot * slot_bytes +
-                                                    kATileBytes + b_tile) + t * 8;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            for (int i = 0; i < iters; ++i, r.next()) {
+                mbar_wait(&full[r.slot], r.phase);
+                float4 *a = reinterpret_cast<float4 *>(smem + (size_t)r.slot * slot_bytes) + tid * 8;
+                float4 *lo = reinterpret_cast<float4 *>(smem + (size_t)r.slot * slot_bytes +
+                                                        kATileBytes + b_tile) + tid * 8;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {  // elementwise: the 128B swizzle is irrelevant
-                const float4 v = a[j];
-                const float vv[4] = {v.x, v.y, v.z, v.w};
-                split4(vv, &a[j], &lo[j]);
+                for (int j = 0; j < 8; ++j) {  // elementwise: the 128B swizzle is irrelevant
+                    const float4 v = a[j];
+                    const float vv[4] = {v.x, v.y, v.z, v.w};
+                    split4(vv, &a[j], &lo[j]);
+                }
+                fence_proxy_async_smem();
+                mbar_arrive(&conv[r.slot]);
             }
-            fence_proxy_async_smem();
-            mbar_arrive(&conv[r.slot]);
         }
     }
-    if (warp == 2 && lane == 0) GTL(5);  // epilogue stores issued
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, ncols);
+    if (warp == 1) tmem_dealloc(tmem, 2 * ncols);
     if (threadIdx.x == 64) GTL(6);  // CTA end
 }
 
 int tc_smem_bytes(int BN, int stages, int split) {
     return 1024 /*align slack*/ + stages * (split ? 2 : 1) * (kATileBytes + BN * kBK * 4) +
-           kEpiScratch + (3 * stages + 1) * 8 + 16;
+           kEpiScratch + (3 * stages + 4) * 8 + 16;
+}
+
+int persistent_occupancy(int smem_bytes, int bn) {
+    int ncols = 32;
+    while (ncols < bn) ncols *= 2;
+    const int by_tmem = 512 / (2 * ncols);
+    const int by_smem = (228 * 1024) / (smem_bytes + 1024);
+    int occ = by_tmem < by_smem ? by_tmem : by_smem;
+    return occ < 1 ? 1 : occ;
 }
 
 int tc_pick_stages(int BN, int iters, int max_smem, int split) {
     int s = 8;
     while (s > 2 && tc_smem_bytes(BN, s, split) > max_smem) --s;
-    if (s > iters) s = iters < 2 ? 2 : iters;
+    (void)iters;  // persistent: the ring also prefetches the next tile
     return s;
 }
 
@@ -350,7 +363,7 @@ __host__ __device__ inline int core_a_slot_bytes(int nphase, int band_rows) {
 int tc_core_smem_bytes(int BN, int nphase, int band_rows, int b_stages, int split) {
     const int f = split ? 2 : 1;
     return 1024 + 2 * f * core_a_slot_bytes(nphase, band_rows) + b_stages * f * BN * 128 +
-           kEpiScratch + (4 + 2 * b_stages + 1) * 8 + 16;
+           kEpiScratch + (4 + 2 * b_stages + 4) * 8 + 16;
 }
 
 template <bool SPLIT>
@@ -370,176 +383,166 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
     uint64_t *a_empty = a_full + 2;
     uint64_t *b_full = a_empty + 2;
     uint64_t *b_empty = b_full + SB;
-    uint64_t *tfull = b_empty + SB;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfull + 1);
+    uint64_t *tfull = b_empty + SB;  // [2]
+    uint64_t *tempty = tfull + 2;    // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * kBM, nt = blockIdx.y, n0 = nt * BN;
     uint32_t ncols = 32;  // TMEM allocations are powers of two >= 32
     while ((int)ncols < BN) ncols *= 2;
+    const int mtiles = (g.M + kBM - 1) / kBM;
+    const int num_tiles = mtiles * g.ntiles;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&a_full[i], 1);
             mbar_init(&a_empty[i], 1);
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 128);
         }
         for (int i = 0; i < SB; ++i) {
             mbar_init(&b_full[i], 1);
             mbar_init(&b_empty[i], 1);
         }
-        mbar_init(tfull, 1);
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, ncols);
+    if (warp == 1) tmem_alloc(tmem_slot, 2 * ncols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t band_bytes = (uint32_t)g.band_rows * 16;
-    // split-K over the flattened (kc, tap) index f = kc * taps + tap
-    int f0 = 0, f1 = g.kchunks * g.taps;
-    if (g.ksplit > 1) {
-        const int per = (f1 + g.ksplit - 1) / g.ksplit;
-        f0 = blockIdx.z * per;
-        f1 = min(f1, f0 + per);
-    }
-    const int kc_lo = f0 / g.taps, kc_hi = (f1 - 1) / g.taps;
 
     if (warp == 0) {  // ---------------------------------- bulk-copy producer
         Ring ra(2), rb(SB);
-        for (int kc = kc_lo; kc <= kc_hi; ++kc, ra.next()) {
-            mbar_wait(&a_empty[ra.slot], ra.phase ^ 1);
-            if (elect_one()) {
-                mbar_arrive_expect_tx(&a_full[ra.slot], a_bytes);
-                uint8_t *dst = a_slots + (size_t)ra.slot * a_bytes;
-                for (int ph = 0; ph < g.nphase; ++ph)
-                    for (int kg = 0; kg < 8; ++kg) {
-                        const long long off = (long long)(kc * 8 + kg) * g.plane_stride +
-                                              ((long long)g.phase_src[ph] * g.phase_rows + m0) * 4;
-                        bulk_load(dst + (size_t)(ph * 8 + kg) * band_bytes, g.xg + off, band_bytes,
-                                  &a_full[ra.slot]);
-                        if (SPLIT)
-                            bulk_load(dst + a_half + (size_t)(ph * 8 + kg) * band_bytes, g.xg_lo + off,
-                                      band_bytes, &a_full[ra.slot]);
-                    }
-            }
-            __syncwarp();
-            const int t_lo = kc == kc_lo ? f0 - kc * g.taps : 0;
-            const int t_hi = kc == kc_hi ? f1 - kc * g.taps : g.taps;
-            for (int tap = t_lo; tap < t_hi; ++tap, rb.next()) {
-                mbar_wait(&b_empty[rb.slot], rb.phase ^ 1);
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            const int m0 = (t % mtiles) * kBM, nt = t / mtiles;
+            for (int kc = 0; kc < g.kchunks; ++kc, ra.next()) {
+                mbar_wait(&a_empty[ra.slot], ra.phase ^ 1);
                 if (elect_one()) {
-                    mbar_arrive_expect_tx(&b_full[rb.slot], b_bytes);
-                    const long long woff = ((long long)(tap * g.kchunks + kc) * g.ntiles + nt) * BN * 32;
-                    uint8_t *dst = b_slots + (size_t)rb.slot * b_bytes;
-                    bulk_load(dst, g.w + woff, b_half, &b_full[rb.slot]);
-                    if (SPLIT) bulk_load(dst + b_half, g.w_lo + woff, b_half, &b_full[rb.slot]);
+                    mbar_arrive_expect_tx(&a_full[ra.slot], a_bytes);
+                    uint8_t *dst = a_slots + (size_t)ra.slot * a_bytes;
+                    for (int ph = 0; ph < g.nphase; ++ph)
+                        for (int kg = 0; kg < 8; ++kg) {
+                            const long long off = (long long)(kc * 8 + kg) * g.plane_stride +
+                                                  ((long long)g.phase_src[ph] * g.phase_rows + m0) * 4;
+                            bulk_load(dst + (size_t)(ph * 8 + kg) * band_bytes, g.xg + off, band_bytes,
+                                      &a_full[ra.slot]);
+                            if (SPLIT)
+                                bulk_load(dst + a_half + (size_t)(ph * 8 + kg) * band_bytes,
+                                          g.xg_lo + off, band_bytes, &a_full[ra.slot]);
+                        }
                 }
                 __syncwarp();
+                for (int tap = 0; tap < g.taps; ++tap, rb.next()) {
+                    mbar_wait(&b_empty[rb.slot], rb.phase ^ 1);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&b_full[rb.slot], b_bytes);
+                        const long long woff =
+                            ((long long)(tap * g.kchunks + kc) * g.ntiles + nt) * BN * 32;
+                        uint8_t *dst = b_slots + (size_t)rb.slot * b_bytes;
+                        bulk_load(dst, g.w + woff, b_half, &b_full[rb.slot]);
+                        if (SPLIT) bulk_load(dst + b_half, g.w_lo + woff, b_half, &b_full[rb.slot]);
+                    }
+                    __syncwarp();
+                }
             }
         }
     } else if (warp == 1) {  // ------------------------------ MMA issuer
         const uint32_t idesc = idesc_tf32(kBM, BN);
         const uint64_t da = sdesc_kmajor_none(smem_u32(a_slots), band_bytes, 128);
         const uint64_t db = sdesc_kmajor_none(smem_u32(b_slots), BN * 16, 128);
-        Ring ra(2), rb(SB);
-        bool first = true;
-        for (int kc = kc_lo; kc <= kc_hi; ++kc, ra.next()) {
-            mbar_wait(&a_full[ra.slot], ra.phase);
-            const int t_lo = kc == kc_lo ? f0 - kc * g.taps : 0;
-            const int t_hi = kc == kc_hi ? f1 - kc * g.taps : g.taps;
-            for (int tap = t_lo; tap < t_hi; ++tap, rb.next()) {
-                mbar_wait(&b_full[rb.slot], rb.phase);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint64_t a = da + ((ra.slot * a_bytes + (uint32_t)g.tap_phase[tap] * 8 * band_bytes +
-                                              (uint32_t)g.tap_off[tap] * 16) >> 4);
-                    const uint64_t b = db + ((rb.slot * b_bytes) >> 4);
+        Ring ra(2), rb(SB), acc(2);
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next()) {
+            mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem + acc.slot * ncols;
+            bool first = true;
+            for (int kc = 0; kc < g.kchunks; ++kc, ra.next()) {
+                mbar_wait(&a_full[ra.slot], ra.phase);
+                for (int tap = 0; tap < g.taps; ++tap, rb.next()) {
+                    mbar_wait(&b_full[rb.slot], rb.phase);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint64_t a =
+                            da + ((ra.slot * a_bytes + (uint32_t)g.tap_phase[tap] * 8 * band_bytes +
+                                   (uint32_t)g.tap_off[tap] * 16) >> 4);
+                        const uint64_t b = db + ((rb.slot * b_bytes) >> 4);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {  // K = 8 = two 4-channel planes
-                        const uint64_t aj = a + ((j * 2 * band_bytes) >> 4);
-                        const uint64_t bj = b + ((j * 2 * BN * 16) >> 4);
-                        mma_tf32(tmem, aj, bj, idesc, !(first && j == 0));
-                        if (SPLIT) {
-                            mma_tf32(tmem, aj, bj + (b_half >> 4), idesc, 1);
-                            mma_tf32(tmem, aj + (a_half >> 4), bj, idesc, 1);
+                        for (int j = 0; j < 4; ++j) {  // K = 8 = two 4-channel planes
+                            const uint64_t aj = a + ((j * 2 * band_bytes) >> 4);
+                            const uint64_t bj = b + ((j * 2 * BN * 16) >> 4);
+                            mma_tf32(d, aj, bj, idesc, !(first && j == 0));
+                            if (SPLIT) {
+                                mma_tf32(d, aj, bj + (b_half >> 4), idesc, 1);
+                                mma_tf32(d, aj + (a_half >> 4), bj, idesc, 1);
+                            }
                         }
+                        mma_commit(&b_empty[rb.slot]);
                     }
-                    mma_commit(&b_empty[rb.slot]);
+                    __syncwarp();
+                    first = false;
                 }
+                if (elect_one()) mma_commit(&a_empty[ra.slot]);
                 __syncwarp();
-                first = false;
             }
-            if (elect_one()) mma_commit(&a_empty[ra.slot]);
+            if (elect_one()) mma_commit(&tfull[acc.slot]);
             __syncwarp();
         }
-        if (elect_one()) mma_commit(tfull);
-        __syncwarp();
-    } else if (g.ksplit > 1) {  // ------------------ epilogue: raw partials
-        mbar_wait(tfull, 0);
-        tc_fence_after();
-        const int q = warp & 3;
-        const int m = m0 + q * 32 + lane;
-        float *dst = g.part + ((long long)blockIdx.z * gridDim.x * kBM + m) * g.part_ld;
-        for (int c = 0; c < BN; c += 32) {
-            uint32_t r[32];
-            tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
-            tmem_ld_wait();
-            if (m >= g.M || n0 + c >= g.part_ld) continue;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4 *>(dst + n0 + c + j) =
-                    make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-        }
     } else {  // --------------------------------- epilogue warps 2..5: Z compact
-        mbar_wait(tfull, 0);
-        tc_fence_after();
         const int q = warp & 3;
-        const int m = m0 + q * 32 + lane;
-        bool valid = m < g.M;
-        long long dst_row = 0;
-        if (valid) {
-            const int ox = m % g.Wq;
-            const int t = m / g.Wq;
-            const int oy = t % g.Hq;
-            const int b = t / g.Hq;
-            valid = oy < g.Ho && ox < g.Wo;
-            dst_row = ((long long)b * g.Ho + oy) * g.Wo + ox;
-        }
-        float *dst = g.z + dst_row * g.ldz;
-        float *dst_lo = SPLIT ? g.z_lo + dst_row * g.ldz : nullptr;
         float *scratch = epi_scratch + q * 1024;
-        for (int c = 0; c < BN; c += 32) {
-            uint32_t r[32];
-            tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
-            tmem_ld_wait();
-            if (n0 + c >= g.Nn) continue;  // warp-uniform
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-            if (SPLIT) {
-                float h[32], l[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    h[j] = rna_tf32(v[j]);
-                    l[j] = v[j] - h[j];
-                }
-                warp_store_block32(scratch, h, valid ? dst + n0 + c : nullptr, lane);
-                warp_store_block32(scratch, l, valid ? dst_lo + n0 + c : nullptr, lane);
-            } else {
-                warp_store_block32(scratch, v, valid ? dst + n0 + c : nullptr, lane);
+        Ring acc(2);
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next()) {
+            const int m0 = (t % mtiles) * kBM, n0 = (t / mtiles) * BN;
+            mbar_wait(&tfull[acc.slot], acc.phase);
+            tc_fence_after();
+            const int m = m0 + q * 32 + lane;
+            bool valid = m < g.M;
+            long long dst_row = 0;
+            if (valid) {
+                const int ox = m % g.Wq;
+                const int tt = m / g.Wq;
+                const int oy = tt % g.Hq;
+                const int b = tt / g.Hq;
+                valid = oy < g.Ho && ox < g.Wo;
+                dst_row = ((long long)b * g.Ho + oy) * g.Wo + ox;
             }
+            float *dst = g.z + dst_row * g.ldz;
+            float *dst_lo = SPLIT ? g.z_lo + dst_row * g.ldz : nullptr;
+            const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(src + c, r);
+                tmem_ld_wait();
+                if (n0 + c >= g.Nn) continue;  // warp-uniform
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                if (SPLIT) {
+                    float h[32], l[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        h[j] = rna_tf32(v[j]);
+                        l[j] = v[j] - h[j];
+                    }
+                    warp_store_block32(scratch, h, valid ? dst + n0 + c : nullptr, lane);
+                    warp_store_block32(scratch, l, valid ? dst_lo + n0 + c : nullptr, lane);
+                } else {
+                    warp_store_block32(scratch, v, valid ? dst + n0 + c : nullptr, lane);
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc.slot]);
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, ncols);
+    if (warp == 1) tmem_dealloc(tmem, 2 * ncols);
 }
 
-cudaError_t tc_core_launch(const TcCoreArgs &g, cudaStream_t st) {
+cudaError_t tc_core_launch(const TcCoreArgs &g, int grid, cudaStream_t st) {
     const int smem = tc_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.b_stages, g.split);
-    dim3 grid((g.M + kBM - 1) / kBM, g.ntiles, g.ksplit > 1 ? g.ksplit : 1);
     cudaError_t e;
     if (g.split) {
         e = cudaFuncSetAttribute(tdc_tc_core_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -550,66 +553,6 @@ cudaError_t tc_core_launch(const TcCoreArgs &g, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         tdc_tc_core_kernel<false><<<grid, kCoreThreads, smem, st>>>(g);
     }
-    return cudaGetLastError();
-}
-
-// ============================================================ split-K reduce
-// Sums the ksplit partials in a fixed order (deterministic), then applies the
-// producing stage's epilogue: bias, row remap, planar/row-major store, hi/lo split.
-__global__ void __launch_bounds__(256) tdc_splitk_reduce_kernel(const ReduceArgs r) {
-    const int n4 = (r.Nn + 3) >> 2;
-    const long long total = (long long)r.M * n4;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int m = (int)(e / n4), n = (int)(e - (long long)m * n4) * 4;
-        long long dst_row;
-        TcGemmArgs geo;  // reuse the row remap of the GEMM epilogue
-        geo.M = r.M; geo.remap = r.remap; geo.H = r.H; geo.W = r.W; geo.s = r.s; geo.p = r.p;
-        geo.Hq = r.Hq; geo.Wq = r.Wq; geo.Ho = r.Ho; geo.Wo = r.Wo; geo.phase_rows = r.phase_rows;
-        if (!remap_row(geo, m, &dst_row)) continue;
-        const float *src = r.part + (long long)m * r.part_ld + n;
-        float4 acc = *reinterpret_cast<const float4 *>(src);
-        for (int z = 1; z < r.ksplit; ++z) {
-            const float4 v = *reinterpret_cast<const float4 *>(src + z * r.part_stride);
-            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
-        float v[4] = {acc.x, acc.y, acc.z, acc.w};
-        if (r.bias)
-            for (int j = 0; j < 4; ++j)
-                if (n + j < r.Nn) v[j] += r.bias[n + j];
-        if (r.planar_stride) {
-            const long long off = (long long)(n >> 2) * r.planar_stride + dst_row * 4;
-            if (r.split)
-                split4(v, reinterpret_cast<float4 *>(r.out + off), reinterpret_cast<float4 *>(r.out_lo + off));
-            else
-                *reinterpret_cast<float4 *>(r.out + off) = make_float4(v[0], v[1], v[2], v[3]);
-        } else {
-            const long long off = dst_row * r.ldo + n;
-            if (n + 4 <= r.Nn && (r.ldo & 3) == 0) {
-                if (r.split)
-                    split4(v, reinterpret_cast<float4 *>(r.out + off), reinterpret_cast<float4 *>(r.out_lo + off));
-                else
-                    *reinterpret_cast<float4 *>(r.out + off) = make_float4(v[0], v[1], v[2], v[3]);
-            } else {
-                for (int j = 0; j < 4 && n + j < r.Nn; ++j) {
-                    if (r.split) {
-                        const float h = rna_tf32(v[j]);
-                        r.out[off + j] = h;
-                        r.out_lo[off + j] = v[j] - h;
-                    } else {
-                        r.out[off + j] = v[j];
-                    }
-                }
-            }
-        }
-    }
-}
-
-cudaError_t splitk_reduce_launch(const ReduceArgs &r, cudaStream_t st) {
-    const long long total = (long long)r.M * ((r.Nn + 3) / 4);
-    long long blocks = (total + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    tdc_splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, st>>>(r);
     return cudaGetLastError();
 }
 
@@ -659,9 +602,8 @@ bool make_tma_4d_nhwc(CUtensorMap *map, const float *x, int C, int W, int H, int
 
 cudaError_t tc_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo,
                            const CUtensorMap &mapB, const CUtensorMap &mapBlo, const TcGemmArgs &g,
-                           int grid_n, cudaStream_t st) {
+                           int grid, cudaStream_t st) {
     const int smem = tc_smem_bytes(g.BN, g.stages, g.split);
-    dim3 grid((g.M + kBM - 1) / kBM, grid_n, g.ksplit > 1 ? g.ksplit : 1);
     cudaError_t e;
     if (g.split) {
         e = cudaFuncSetAttribute(tdc_tc_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
