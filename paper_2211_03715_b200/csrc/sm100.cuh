@@ -50,6 +50,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Relaxed arrive: signals progress without ordering this thread's prior memory
+// operations (used when the barrier only guards TMEM, which tcgen05.wait::ld +
+// tcgen05.fence already order) -- a release arrive would wait for the warp's
+// outstanding global stores to complete.
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -191,23 +198,40 @@ __device__ __forceinline__ void tmem_ld_wait() {
 // global store instruction writes four full 128-byte row segments instead of
 // 32 scattered 16-byte pieces.  row_ptr: this lane's destination row (already
 // offset to the column block), nullptr to skip the row.
+__device__ __forceinline__ float4 ld_shared_v4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void st_global_v4(void *ptr, float4 v) {
+    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
 __device__ __forceinline__ void warp_store_block32(float *scratch, const float (&v)[32],
                                                    float *row_ptr, int lane) {
-    float4 *s4 = reinterpret_cast<float4 *>(scratch);
+    // Explicit state spaces: with generic pointers (lost through __shfl_sync) the
+    // scratch loads were ordered behind the previous global store.
+    const uint32_t base = smem_u32(scratch);
 #pragma unroll
     for (int c4 = 0; c4 < 8; ++c4)
-        s4[lane * 8 + (c4 ^ (lane & 7))] =
-            make_float4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+        st_shared_v4(base + (uint32_t)(lane * 8 + (c4 ^ (lane & 7))) * 16, v[4 * c4], v[4 * c4 + 1],
+                     v[4 * c4 + 2], v[4 * c4 + 3]);
     __syncwarp();
     const int c4 = lane & 7;
+    float4 val[8];
+    unsigned long long dst[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int r = i * 4 + (lane >> 3);
-        float *dst = reinterpret_cast<float *>(
-            __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(row_ptr), r));
-        const float4 val = s4[r * 8 + (c4 ^ (r & 7))];
-        if (dst) reinterpret_cast<float4 *>(dst)[c4] = val;
+        val[i] = ld_shared_v4(base + (uint32_t)(r * 8 + (c4 ^ (r & 7))) * 16);
+        dst[i] = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(row_ptr), r);
     }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (dst[i]) st_global_v4(reinterpret_cast<float4 *>(dst[i]) + c4, val[i]);
     __syncwarp();
 }
 

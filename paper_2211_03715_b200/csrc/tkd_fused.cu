@@ -351,7 +351,7 @@ tdc_tkd_fused_tc_kernel(const __grid_constant__ CUtensorMap mapX, const FusedArg
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(&acc3_empty[ab]);
+                mbar_arrive_relaxed(&acc3_empty[ab]);
             }
             if (warp == 8 && lane == 0) TL(it, 13);  // Y stored
         }

@@ -57,8 +57,23 @@ extern "C" int tdc_debug_gemm_timeline(unsigned long long *host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_tdc_gemm_tl, sizeof(unsigned long long) * n);
 }
 #define GTL(ev) gtl(ev)
+// per-tile events of CTA 0: [launch seq % 4][tile iter][8]
+__device__ unsigned long long g_tdc_tile_tl[4 * 64 * 8];
+__device__ unsigned int g_tdc_launch_seq;
+__device__ __forceinline__ void ttl(int seq, int it, int ev) {
+    if (blockIdx.x == 0 && it < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_tdc_tile_tl[((seq & 3) * 64 + it) * 8 + ev] = t;
+    }
+}
+extern "C" int tdc_debug_tile_timeline(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_tdc_tile_tl, sizeof(unsigned long long) * n);
+}
+#define TTL(seq, it, ev) ttl((seq), (it), (ev))
 #else
 #define GTL(ev) ((void)0)
+#define TTL(seq, it, ev) ((void)0)
 #endif
 
 __device__ __forceinline__ float rna_tf32(float x) {
@@ -169,6 +184,9 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     const int num_tiles = mtiles * g.ntiles;
     const int iters = g.taps * g.kchunks;
     if (threadIdx.x == 0) GTL(0);  // CTA start
+#ifdef TDC_TIMELINE
+    const int seq = (int)*(volatile unsigned int *)&g_tdc_launch_seq;
+#endif
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -196,9 +214,11 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     if (warp == 0) {  // ------------------------------------- TMA producer
         const uint32_t bytes = (SPLIT && !convert ? 2 : 1) * kATileBytes + (SPLIT ? 2 : 1) * b_tile;
         Ring r(S);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int tit = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tit) {
             const int m0 = (t % mtiles) * kBM, n0 = (t / mtiles) * BN;
             int tap = 0, kc = 0;
+            if (lane == 0) TTL(seq, tit, 0);  // producer starts tile
             for (int i = 0; i < iters; ++i, r.next()) {
                 mbar_wait(&empty[r.slot], r.phase ^ 1);
                 if (elect_one()) {
@@ -227,9 +247,11 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         const uint64_t db = sdesc_kmajor_sw128(smem_u32(smem + kATileBytes));
         const uint32_t lo_off = (kATileBytes + b_tile) >> 4;  // hi -> lo, 16-byte units
         Ring r(S), acc(2);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next()) {
+        int tit = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next(), ++tit) {
             mbar_wait(&tempty[acc.slot], acc.phase ^ 1);  // epilogue drained this buffer
             tc_fence_after();
+            if (lane == 0) TTL(seq, tit, 1);  // MMA: accumulator free
             const uint32_t d = tmem + acc.slot * ncols;
             for (int i = 0; i < iters; ++i, r.next()) {
                 mbar_wait(convert ? &conv[r.slot] : &full[r.slot], r.phase);
@@ -253,17 +275,20 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             if (elect_one()) mma_commit(&tfull[acc.slot]);
             __syncwarp();
             if (lane == 0) GTL(3);  // all MMAs of the tile issued
+            if (lane == 0) TTL(seq, tit, 2);  // MMA: all issued
         }
     } else if (warp < 6) {  // --------------------------------- epilogue
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         float *scratch = epi_scratch + q * 1024;
         const bool rowmajor_vec = !g.planar_stride && (g.ldo & 3) == 0;
         Ring acc(2);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next()) {
+        int tit = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next(), ++tit) {
             const int m0 = (t % mtiles) * kBM, n0 = (t / mtiles) * BN;
             mbar_wait(&tfull[acc.slot], acc.phase);
             tc_fence_after();
             if (warp == 2 && lane == 0) GTL(4);  // accumulator ready
+            if (warp == 2 && lane == 0) TTL(seq, tit, 3);  // epilogue: accumulator ready
             long long dst_row = 0;
             const bool valid = remap_row(g, m0 + q * 32 + lane, &dst_row);
             const long long off = g.planar_stride ? dst_row * 4 : dst_row * g.ldo;
@@ -274,6 +299,7 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(src + c, r);
                 tmem_ld_wait();
+                if (c == 0 && warp == 2 && lane == 0) TTL(seq, tit, 6);  // first TMEM block loaded
                 const int n = n0 + c;
                 if (n >= g.Nn) continue;  // warp-uniform
                 float v[32];
@@ -301,25 +327,30 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                     store_row32(dst, dst_lo, g.planar_stride, n, g.Nn, (g.ldo & 3) == 0, v,
                                 dst_lo != nullptr);
                 }
+                if (c == 0 && warp == 2 && lane == 0) TTL(seq, tit, 7);  // first block stored
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc.slot]);
+            mbar_arrive_relaxed(&tempty[acc.slot]);
             if (warp == 2 && lane == 0) GTL(5);  // epilogue stores issued
+            if (warp == 2 && lane == 0) TTL(seq, tit, 4);  // epilogue done
         }
     } else if (convert) {  // ------------------------ converter (3xTF32 stage 1)
         const int tid = threadIdx.x - 192;  // 0..127: each owns 128 contiguous bytes of A
         Ring r(S);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int tit = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tit) {
             for (int i = 0; i < iters; ++i, r.next()) {
                 mbar_wait(&full[r.slot], r.phase);
-                float4 *a = reinterpret_cast<float4 *>(smem + (size_t)r.slot * slot_bytes) + tid * 8;
+                if (tid == 0 && i == 0) TTL(seq, tit, 5);  // converter: first chunk landed
+                float4 *a = reinterpret_cast<float4 *>(smem + (size_t)r.slot * slot_bytes);
                 float4 *lo = reinterpret_cast<float4 *>(smem + (size_t)r.slot * slot_bytes +
-                                                        kATileBytes + b_tile) + tid * 8;
+                                                        kATileBytes + b_tile);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {  // elementwise: the 128B swizzle is irrelevant
-                    const float4 v = a[j];
+                for (int j = 0; j < 8; ++j) {  // elementwise (the 128B swizzle is irrelevant);
+                    const int k = j * 128 + tid;  // consecutive lanes -> consecutive 16 B
+                    const float4 v = a[k];
                     const float vv[4] = {v.x, v.y, v.z, v.w};
-                    split4(vv, &a[j], &lo[j]);
+                    split4(vv, &a[k], &lo[k]);
                 }
                 fence_proxy_async_smem();
                 mbar_arrive(&conv[r.slot]);
@@ -330,6 +361,9 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 2 * ncols);
     if (threadIdx.x == 64) GTL(6);  // CTA end
+#ifdef TDC_TIMELINE
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_tdc_launch_seq, 1u);
+#endif
 }
 
 int tc_smem_bytes(int BN, int stages, int split) {
@@ -533,7 +567,7 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc.slot]);
+            mbar_arrive_relaxed(&tempty[acc.slot]);
         }
     }
     tc_fence_before();
