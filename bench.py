@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["tdc", "reference"], default="tdc")
-    ap.add_argument("--math", choices=["fp32", "tf32", "3xtf32"], default="3xtf32",
+    ap.add_argument("--math", choices=["fp32", "tf32", "3xtf32", "3xbf16"], default="3xtf32",
                     help="3xtf32: fp32-accurate tensor-core split (default); tf32: 1e-2 mode; "
                          "fp32: CUDA-core FFMA")
     ap.add_argument("--batch", type=int, default=32)
@@ -329,11 +329,14 @@ def impl_tdc(args):
                 "steps": args.steps, "warmup": max(args.warmup, 3),
                 "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None,
-                "dtype": {"fp32": "f32", "tf32": "tf32", "3xtf32": "f32(3xtf32)"}[args.math],
+                "dtype": {"fp32": "f32", "tf32": "tf32", "3xtf32": "f32(3xtf32)",
+                          "3xbf16": "f32(3xbf16)"}[args.math],
                 "accuracy": {"fp32": "fp32 FFMA; max-normalized err vs fp64 oracle <= 1e-4",
                              "tf32": "TF32 products; tolerance 1e-2 (north_star TF32 stage)",
                              "3xtf32": "hi*hi+hi*lo+lo*hi TF32 split, fp32 accumulate; fp32-grade, "
-                                       "tolerance 1e-4 (measured ~5e-7)"}[args.math],
+                                       "tolerance 1e-4 (measured ~5e-7)",
+                             "3xbf16": "hi*hi+hi*lo+lo*hi bf16 split, fp32 accumulate; fp32-grade, "
+                                       "tolerance 1e-4"}[args.math],
                 "data": "synthetic", "config": config_dict(args, world),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps,

@@ -54,7 +54,8 @@ typedef enum {
 typedef enum {
     TDC_MATH_FP32 = 0,   /* fp32 FFMA on CUDA cores (the paper's precision); tol 1e-4 */
     TDC_MATH_3XTF32 = 1, /* tcgen05 TF32 with hi/lo split (3 products); tol 1e-4            */
-    TDC_MATH_TF32 = 2    /* tcgen05 TF32, one product; tol 1e-2 (north_star)                */
+    TDC_MATH_TF32 = 2,   /* tcgen05 TF32, one product; tol 1e-2 (north_star)                */
+    TDC_MATH_3XBF16 = 3  /* tcgen05 bf16 with hi/lo split (3 products); tol 1e-4            */
 } tdc_math;
 
 /* Layer descriptor.  All sizes > 0; 1 <= rank_in <= c_in and

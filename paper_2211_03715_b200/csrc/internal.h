@@ -51,6 +51,7 @@ struct TcGemmArgs {
     int a_convert;    // split only: 1 = A lo computed in-kernel from A (user input); 0 = loaded
     float *out_lo;    // split only: epilogue also writes the lo part of the output (next stage's A lo)
     int ntiles;       // N tiles (persistent kernel walks mtiles x ntiles)
+    int out_bf16;     // 3xBF16 stage 1: out/out_lo are bf16 planar [c/8][row][8], planar_stride in rows
 };
 
 // Stage-2 core convolution with a shared-memory-resident X' band (tkd_tc.cu):
@@ -108,6 +109,16 @@ bool make_tma_4d_nhwc(CUtensorMap *map, const float *x, int C, int W, int H, int
                       int box_h);
 bool fused_make_x_map(CUtensorMap *map, const float *x, const FusedArgs &g);
 cudaError_t fused_launch(const CUtensorMap &mapX, const FusedArgs &g, int grid, cudaStream_t st);
+
+// ---- 3xBF16 variant of the 3-launch path (tkd_bf16.cu) ----
+int bf_smem_bytes(int BN, int stages, int convert);
+int bf_pick_stages(int BN, int max_smem, int convert);
+cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, const CUtensorMap &mapB,
+                           const CUtensorMap &mapBlo, const TcGemmArgs &g, int grid, cudaStream_t st);
+int bf_core_smem_bytes(int BN, int nphase, int band_rows, int b_stages);
+cudaError_t bf_core_launch(const TcCoreArgs &g, int grid, cudaStream_t st);
+bool make_tma_2d_bf16(CUtensorMap *map, const void *base, long long rows, int k_extent, int pitch,
+                      int box_rows);
 
 // NCHW <-> NHWC for the NCHW API layout.
 cudaError_t nchw_to_nhwc(const float *src, float *dst, int B, int C, int H, int W,

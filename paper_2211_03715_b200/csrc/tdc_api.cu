@@ -70,7 +70,7 @@ tdc_status validate_desc(const tdc_conv_desc *d, int *ho, int *wo) {
                     d->height + 2 * d->pad, d->width + 2 * d->pad);
     if (d->layout != TDC_LAYOUT_NCHW && d->layout != TDC_LAYOUT_NHWC)
         return fail(TDC_ERR_INVALID_ARGUMENT, "unknown layout %d", d->layout);
-    if (d->math < TDC_MATH_FP32 || d->math > TDC_MATH_TF32)
+    if (d->math < TDC_MATH_FP32 || d->math > TDC_MATH_3XBF16)
         return fail(TDC_ERR_INVALID_ARGUMENT, "unknown math mode %d", d->math);
     const long long elems_in = (long long)d->batch * d->c_in * d->height * d->width;
     if (elems_in > (1LL << 40))
@@ -111,6 +111,7 @@ struct tdc_conv_plan_s {
     int fgrid = 0, num_sms = 148;
     bool tc_core = false;          // stage 2 uses the band-resident core kernel
     bool split = false;            // 3xTF32
+    bool bf16x3 = false;           // 3xBF16 (variant 4 uses tc[] maps + core_args, bf16 formats)
 
     tdc::TcCoreArgs core_args;
     float *d_tc_w = nullptr;       // Bt1 | Bt2 | Bt3 | bias
@@ -127,6 +128,21 @@ namespace {
 int div_up(int a, int b) { return (a + b - 1) / b; }
 
 // Round-to-nearest (ties away) to tf32: clear the low 13 mantissa bits.
+// fp32 -> bf16 round-to-nearest-even, returned as the bf16 bit pattern.
+uint16_t bf16_bits_host(float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u) return (uint16_t)(u >> 16);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+float bf16_to_float_host(uint16_t b) {
+    const uint32_t u = (uint32_t)b << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
 float tf32_round_host(float x) {
     uint32_t u;
     std::memcpy(&u, &x, 4);
@@ -347,6 +363,212 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     }
     p->variant = 2;
     p->split = split;
+    return TDC_OK;
+}
+
+// Plan the 3xBF16 3-launch variant (fp32-grade accuracy, bf16 tensor cores).
+// Returns TDC_OK with *used = false when the band-resident core kernel does not
+// fit (the caller then plans 3xTF32 instead).
+tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, const float *u_out,
+                     const float *bias, bool *used) {
+    *used = false;
+    const tdc_conv_desc &d = p->desc;
+    const int C = d.c_in, N = d.c_out, D1 = d.rank_in, D2 = d.rank_out, K = d.kernel;
+    const int s = d.stride, pad = d.pad, H = d.height, W = d.width;
+    const int Ho = p->dims.Ho, Wo = p->dims.Wo, Bm = d.batch;
+    if (C % 4 || K * K > tdc::kMaxTaps) return TDC_OK;
+    const int C64 = round_up(C, 64), D1s = round_up(D1, 32), D2s = round_up(D2, 32),
+              D2p = round_up(D2, 64);
+    const int Hq = div_up(H + 2 * pad, s), Wq = div_up(W + 2 * pad, s);
+    const long long phase_rows = (long long)Bm * Hq * Wq;
+    const long long M1 = (long long)Bm * H * W, M2 = phase_rows, M3 = (long long)Bm * Ho * Wo;
+    if (M1 > (1LL << 31) - 256 || M2 * s * s > (1LL << 31) - 256) return TDC_OK;
+    auto pick = [&](int nn, long long mrows) {
+        int b = 32;
+        while (b < nn && b < 256) b *= 2;
+        while (b > 64 && div_up((int)mrows, 128) * (long long)div_up(nn, b) < 2 * p->num_sms) b /= 2;
+        return b;
+    };
+    const int BN1 = pick(D1s, M1), BN3 = pick(N, M3);
+    int BN2 = pick(D2s, M2);
+    const int KK = K * K;
+    const int maxoff = ((K - 1) / s) * Wq + (K - 1) / s;
+    const int band_rows = round_up(128 + maxoff, 8);
+    int phase_of[tdc::kMaxTaps], nphase = 0, phase_src[tdc::kMaxTaps];
+    {
+        int idx_of[tdc::kMaxTaps];
+        for (int i = 0; i < tdc::kMaxTaps; ++i) idx_of[i] = -1;
+        for (int r = 0; r < K; ++r)
+            for (int t = 0; t < K; ++t) {
+                const int ph = (r % s) * s + (t % s);
+                if (idx_of[ph] < 0) {
+                    idx_of[ph] = nphase;
+                    phase_src[nphase++] = ph;
+                }
+                phase_of[r * K + t] = idx_of[ph];
+            }
+    }
+    int core_stages = 4;
+    for (;;) {
+        while (core_stages > 2 && tdc::bf_core_smem_bytes(BN2, nphase, band_rows, core_stages) > p->max_smem)
+            --core_stages;
+        if (BN2 <= 64 || tdc::bf_core_smem_bytes(BN2, nphase, band_rows, core_stages) <= p->max_smem) break;
+        BN2 /= 2;
+        core_stages = 4;
+    }
+    if (tdc::bf_core_smem_bytes(BN2, nphase, band_rows, core_stages) > p->max_smem) return TDC_OK;
+    const int R1 = round_up(D1s, BN1), R2 = round_up(D2s, BN2), R3 = round_up(N, BN3);
+    const int k2chunks = D1s / 32, nt2 = R2 / BN2;
+    const long long rows_total = (long long)s * s * phase_rows + band_rows + 128;
+
+    // ---- a0: bf16 hi/lo weight panels (CRSN idea) ----
+    const size_t n1 = (size_t)R1 * C64, n2 = (size_t)KK * R2 * D1s, n3 = (size_t)R3 * D2p;
+    const size_t nw = n1 + n2 + n3;
+    std::vector<float> wf(nw, 0.f);  // fp32 staging in the final element order
+    float *w1 = wf.data(), *w2 = w1 + n1, *w3 = w2 + n2;
+    for (int a = 0; a < D1; ++a)
+        for (int c = 0; c < C; ++c) w1[(size_t)a * C64 + c] = u_in[(size_t)c * D1 + a];
+    for (int r = 0; r < K; ++r)
+        for (int t = 0; t < K; ++t)
+            for (int q = 0; q < D2; ++q)
+                for (int a = 0; a < D1; ++a) {
+                    // blocked [tap][kc(32)][ntile][plane(4)][BN2][8] no-swizzle K-major chunks
+                    const int kc = a / 32, pl = (a % 32) / 8, e = a % 8, tap = r * K + t;
+                    const int ntl = q / BN2, n = q % BN2;
+                    w2[((((size_t)(tap * k2chunks + kc) * nt2 + ntl) * 4 + pl) * BN2 + n) * 8 + e] =
+                        core[(((size_t)q * D1 + a) * K + r) * K + t];
+                }
+    for (int n = 0; n < N; ++n)
+        for (int q = 0; q < D2; ++q) w3[(size_t)n * D2p + q] = u_out[(size_t)n * D2 + q];
+    std::vector<uint16_t> hb(2 * nw);
+    for (size_t i = 0; i < nw; ++i) {
+        const uint16_t hi = bf16_bits_host(wf[i]);
+        hb[i] = hi;
+        hb[nw + i] = bf16_bits_host(wf[i] - bf16_to_float_host(hi));
+    }
+    const size_t wbytes = 2 * nw * sizeof(uint16_t), nbias = round_up(N, 4);
+    cudaError_t e = cudaMalloc(&p->d_tc_w, wbytes + nbias * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(bf16 weights)");
+    e = cudaMemcpy(p->d_tc_w, hb.data(), wbytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && bias) {
+        std::vector<float> bb(nbias, 0.f);
+        for (int n = 0; n < N; ++n) bb[n] = bias[n];
+        e = cudaMemcpy(reinterpret_cast<uint8_t *>(p->d_tc_w) + wbytes, bb.data(), nbias * sizeof(float),
+                       cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(bf16 weights)");
+    p->weight_bytes += wbytes + nbias * sizeof(float);
+    const uint16_t *wb = reinterpret_cast<const uint16_t *>(p->d_tc_w);
+    const uint16_t *dB1 = wb, *dB2 = wb + n1, *dB3 = wb + n1 + n2;
+    const uint16_t *dB1lo = dB1 + nw, *dB2lo = dB2 + nw, *dB3lo = dB3 + nw;
+    const float *dbias =
+        bias ? reinterpret_cast<const float *>(reinterpret_cast<uint8_t *>(p->d_tc_w) + wbytes) : nullptr;
+
+    // ---- workspaces: X' hi/lo planar bf16 (zero borders), Z hi/lo bf16 [M3][D2p] ----
+    const size_t xg_elems = (size_t)rows_total * D1s, z_elems = (size_t)M3 * D2p;
+    e = cudaMalloc(&p->d_xg, 2 * xg_elems * sizeof(uint16_t));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_z, 2 * z_elems * sizeof(uint16_t));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(bf16 workspace)");
+    e = cudaMemset(p->d_xg, 0, 2 * xg_elems * sizeof(uint16_t));
+    if (e == cudaSuccess) e = cudaMemset(p->d_z, 0, 2 * z_elems * sizeof(uint16_t));  // pad columns stay 0
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(bf16 workspace)");
+    p->tc_ws_bytes = 2 * (xg_elems + z_elems) * sizeof(uint16_t);
+    uint16_t *xg = reinterpret_cast<uint16_t *>(p->d_xg), *xg_lo = xg + xg_elems;
+    uint16_t *z = reinterpret_cast<uint16_t *>(p->d_z), *z_lo = z + z_elems;
+
+    auto base_args = [&](tdc::TcGemmArgs &g) {
+        std::memset(&g, 0, sizeof g);
+        g.H = H; g.W = W; g.s = s; g.p = pad; g.Hq = Hq; g.Wq = Wq; g.Ho = Ho; g.Wo = Wo;
+        g.phase_rows = phase_rows;
+    };
+    const char *enc_err = "cuTensorMapEncodeTiled failed (3xBF16)";
+    {   // stage 1: A = X fp32 (map per forward, 32-channel boxes), B = U_in^T bf16
+        auto &st = p->tc[0];
+        base_args(st.args);
+        st.args.M = (int)M1; st.args.Nn = D1s; st.args.kchunks = C64 / 64; st.args.taps = 1;
+        st.args.BN = BN1; st.args.remap = 1; st.args.a_convert = 1; st.args.out_bf16 = 1;
+        st.args.out = reinterpret_cast<float *>(xg); st.args.out_lo = reinterpret_cast<float *>(xg_lo);
+        st.args.planar_stride = rows_total;  // rows
+        st.args.stages = tdc::bf_pick_stages(BN1, p->max_smem, 1);
+        st.grid_n = R1 / BN1;
+        st.args.ntiles = st.grid_n;
+        if (!tdc::make_tma_2d_bf16(&st.mapB, dB1, R1, C64, C64, BN1) ||
+            !tdc::make_tma_2d_bf16(&st.mapBlo, dB1lo, R1, C64, C64, BN1))
+            return fail(TDC_ERR_CUDA, "%s (stage 1)", enc_err);
+    }
+    {   // stage 2: band-resident core kernel on bf16 planes
+        tdc::TcCoreArgs &g = p->core_args;
+        std::memset(&g, 0, sizeof g);
+        g.xg = reinterpret_cast<const float *>(xg);
+        g.xg_lo = reinterpret_cast<const float *>(xg_lo);
+        g.plane_stride = rows_total;  // rows
+        g.w = reinterpret_cast<const float *>(dB2);
+        g.w_lo = reinterpret_cast<const float *>(dB2lo);
+        g.z = reinterpret_cast<float *>(z);
+        g.z_lo = reinterpret_cast<float *>(z_lo);
+        g.ldz = D2p; g.Nn = D2s; g.M = (int)M2; g.kchunks = k2chunks; g.taps = KK;
+        g.ntiles = nt2; g.BN = BN2; g.nphase = nphase; g.band_rows = band_rows;
+        g.b_stages = core_stages; g.phase_rows = phase_rows;
+        for (int r = 0; r < K; ++r)
+            for (int t = 0; t < K; ++t) {
+                g.tap_phase[r * K + t] = phase_of[r * K + t];
+                g.tap_off[r * K + t] = (r / s) * Wq + (t / s);
+            }
+        for (int i = 0; i < nphase; ++i) g.phase_src[i] = phase_src[i];
+        g.Hq = Hq; g.Wq = Wq; g.Ho = Ho; g.Wo = Wo;
+        g.split = 1;
+    }
+    {   // stage 3: A = Z hi/lo bf16, B = U_out bf16; out = Y fp32 (+bias)
+        auto &st = p->tc[2];
+        base_args(st.args);
+        st.args.M = (int)M3; st.args.Nn = N; st.args.kchunks = D2p / 64; st.args.taps = 1;
+        st.args.BN = BN3; st.args.ldo = N; st.args.remap = 0; st.args.bias = dbias;
+        st.args.stages = tdc::bf_pick_stages(BN3, p->max_smem, 0);
+        st.grid_n = R3 / BN3;
+        st.args.ntiles = st.grid_n;
+        if (!tdc::make_tma_2d_bf16(&st.mapA, z, M3, D2p, D2p, 128) ||
+            !tdc::make_tma_2d_bf16(&st.mapAlo, z_lo, M3, D2p, D2p, 128) ||
+            !tdc::make_tma_2d_bf16(&st.mapB, dB3, R3, D2p, D2p, BN3) ||
+            !tdc::make_tma_2d_bf16(&st.mapBlo, dB3lo, R3, D2p, D2p, BN3))
+            return fail(TDC_ERR_CUDA, "%s (stage 3)", enc_err);
+    }
+    p->tc_core = true;
+    p->bf16x3 = true;
+    p->variant = 4;
+    *used = true;
+    return TDC_OK;
+}
+
+tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch, cudaStream_t st) {
+    const tdc::LayerDims &d = p->dims;
+    auto &s1 = p->tc[0], &s3 = p->tc[2];
+    if (x != p->tc_last_x) {
+        if (!tdc::make_tma_2d(&s1.mapA, x, (long long)p->desc.batch * d.H * d.W, d.C, d.C, 128))
+            return fail(TDC_ERR_INVALID_ARGUMENT,
+                        "cuTensorMapEncodeTiled rejected x (needs 16-byte aligned pointer)");
+        p->tc_last_x = x;
+    }
+    tdc::TcGemmArgs a1 = s1.args, a3 = s3.args;
+    a1.M = batch * d.H * d.W;
+    a3.M = batch * d.Ho * d.Wo;
+    a3.out = y;
+    tdc::TcCoreArgs c = p->core_args;
+    c.M = batch * a1.Hq * a1.Wq;
+    auto grid = [&](long long M, int ntiles, int smem, int bn) {
+        const long long tiles = (long long)div_up((int)M, 128) * ntiles;
+        const long long cap = (long long)p->num_sms * tdc::persistent_occupancy(smem, bn);
+        return (int)std::max<long long>(1, std::min(tiles, cap));
+    };
+    cudaError_t e = tdc::bf_gemm_launch(
+        s1.mapA, s1.mapA, s1.mapB, s1.mapBlo, a1,
+        grid(a1.M, a1.ntiles, tdc::bf_smem_bytes(a1.BN, a1.stages, 1), a1.BN), st);
+    if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-1 launch");
+    e = tdc::bf_core_launch(
+        c, grid(c.M, c.ntiles, tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.b_stages), c.BN), st);
+    if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-2 launch");
+    e = tdc::bf_gemm_launch(s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, a3,
+                            grid(a3.M, a3.ntiles, tdc::bf_smem_bytes(a3.BN, a3.stages, 0), a3.BN), st);
+    if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-3 launch");
     return TDC_OK;
 }
 
@@ -683,8 +905,16 @@ tdc_status tdc_conv_plan(const tdc_conv_desc *desc, const float *core, const flo
             return s;
         }
     }
-    if (!fused && d.math != TDC_MATH_FP32 && C % 4 == 0 && K * K <= tdc::kMaxTaps) {
-        s = plan_tc(p, core, u_in, u_out, bias, d.math == TDC_MATH_3XTF32);
+    bool bf = false;
+    if (d.math == TDC_MATH_3XBF16) {
+        s = plan_bf16(p, core, u_in, u_out, bias, &bf);
+        if (s != TDC_OK) {
+            tdc_conv_plan_destroy(p);
+            return s;
+        }
+    }
+    if (!fused && !bf && d.math != TDC_MATH_FP32 && C % 4 == 0 && K * K <= tdc::kMaxTaps) {
+        s = plan_tc(p, core, u_in, u_out, bias, d.math != TDC_MATH_TF32);
         if (s != TDC_OK) {
             tdc_conv_plan_destroy(p);
             return s;
@@ -712,9 +942,9 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
     info->h_out = p->dims.Ho;
     info->w_out = p->dims.Wo;
     info->variant = p->variant;
-    const bool tc = p->variant == 2, fz = p->variant == 3;
+    const bool tc = p->variant == 2 || p->variant == 4, fz = p->variant == 3;
     std::snprintf(info->variant_name, sizeof info->variant_name, "%s",
-                  fz ? "fused_tc_tf32"
+                  p->variant == 4 ? "tc3_3xbf16_band" : fz ? "fused_tc_tf32"
                      : tc ? (p->split ? (p->tc_core ? "tc3_3xtf32_band" : "tc3_3xtf32")
                                       : (p->tc_core ? "tc3_tf32_band" : "tc3_tf32"))
                           : "fused_simt_fp32");
@@ -763,6 +993,7 @@ tdc_status tdc_conv_forward(tdc_conv_plan_t p, const float *x, float *y, int32_t
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
     if (p->desc.layout == TDC_LAYOUT_NHWC) {
+        if (p->variant == 4) return forward_bf16(p, x, y, batch, st);
         if (p->variant == 3) return forward_fused(p, x, y, batch, st);
         if (p->variant == 2) return forward_tc(p, x, y, batch, st);
         e = tdc::simt_fused_launch(d, p->simt, p->simt_tile, x, y, batch, st);
@@ -771,7 +1002,10 @@ tdc_status tdc_conv_forward(tdc_conv_plan_t p, const float *x, float *y, int32_t
     }
     e = tdc::nchw_to_nhwc(x, p->d_ws_in, batch, d.C, d.H, d.W, st);
     if (e != cudaSuccess) return cuda_fail(e, "NCHW->NHWC launch");
-    if (p->variant == 3) {
+    if (p->variant == 4) {
+        tdc_status s = forward_bf16(p, p->d_ws_in, p->d_ws_out, batch, st);
+        if (s != TDC_OK) return s;
+    } else if (p->variant == 3) {
         tdc_status s = forward_fused(p, p->d_ws_in, p->d_ws_out, batch, st);
         if (s != TDC_OK) return s;
     } else if (p->variant == 2) {

@@ -1,0 +1,60 @@
+// tkd_common.cuh -- device helpers shared by the tcgen05 kernels of the
+// 3-launch path (tkd_tc.cu: TF32 / 3xTF32; tkd_bf16.cu: 3xBF16).
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace tdc {
+
+__device__ __forceinline__ float rna_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ bool remap_row(const TcGemmArgs &g, int m, long long *dst) {
+    if (m >= g.M) return false;
+    if (g.remap == 0) {
+        *dst = m;
+        return true;
+    }
+    if (g.remap == 1) {  // compact input pixel -> phase grid row
+        const int x = m % g.W;
+        const int t = m / g.W;
+        const int y = t % g.H;
+        const int b = t / g.H;
+        const int uy = y + g.p, ux = x + g.p;
+        const int ph = (uy % g.s) * g.s + (ux % g.s);
+        *dst = (long long)ph * g.phase_rows + ((long long)b * g.Hq + uy / g.s) * g.Wq + ux / g.s;
+        return true;
+    }
+    // remap == 2: output grid row -> compact output pixel (skip junk rows)
+    const int ox = m % g.Wq;
+    const int t = m / g.Wq;
+    const int oy = t % g.Hq;
+    const int b = t / g.Hq;
+    if (oy >= g.Ho || ox >= g.Wo) return false;
+    *dst = ((long long)b * g.Ho + oy) * g.Wo + ox;
+    return true;
+}
+
+
+// bf16 split of 8 values: x = hi + lo with hi = RN_bf16(x), lo = RN_bf16(x - hi)
+// (|x - hi - lo| <= 2^-17 |x|); packed two per 32-bit word, element 2i low.
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    const __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t *>(&t);
+}
+__device__ __forceinline__ void split_bf16x8(const float *v, uint4 &hi, uint4 &lo) {
+    float h[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
+    hi = make_uint4(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]), pack_bf16x2(h[4], h[5]),
+                    pack_bf16x2(h[6], h[7]));
+    lo = make_uint4(pack_bf16x2(v[0] - h[0], v[1] - h[1]), pack_bf16x2(v[2] - h[2], v[3] - h[3]),
+                    pack_bf16x2(v[4] - h[4], v[5] - h[5]), pack_bf16x2(v[6] - h[6], v[7] - h[7]));
+}
+
+}  // namespace tdc

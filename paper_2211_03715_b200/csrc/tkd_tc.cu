@@ -33,6 +33,7 @@
 
 #include "internal.h"
 #include "sm100.cuh"
+#include "tkd_common.cuh"
 
 namespace tdc {
 
@@ -75,38 +76,6 @@ extern "C" int tdc_debug_tile_timeline(unsigned long long *host, int n) {
 #define GTL(ev) ((void)0)
 #define TTL(seq, it, ev) ((void)0)
 #endif
-
-__device__ __forceinline__ float rna_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
-
-__device__ __forceinline__ bool remap_row(const TcGemmArgs &g, int m, long long *dst) {
-    if (m >= g.M) return false;
-    if (g.remap == 0) {
-        *dst = m;
-        return true;
-    }
-    if (g.remap == 1) {  // compact input pixel -> phase grid row
-        const int x = m % g.W;
-        const int t = m / g.W;
-        const int y = t % g.H;
-        const int b = t / g.H;
-        const int uy = y + g.p, ux = x + g.p;
-        const int ph = (uy % g.s) * g.s + (ux % g.s);
-        *dst = (long long)ph * g.phase_rows + ((long long)b * g.Hq + uy / g.s) * g.Wq + ux / g.s;
-        return true;
-    }
-    // remap == 2: output grid row -> compact output pixel (skip junk rows)
-    const int ox = m % g.Wq;
-    const int t = m / g.Wq;
-    const int oy = t % g.Hq;
-    const int b = t / g.Hq;
-    if (oy >= g.Ho || ox >= g.Wo) return false;
-    *dst = ((long long)b * g.Ho + oy) * g.Wo + ox;
-    return true;
-}
 
 __device__ __forceinline__ void split4(const float *v, float4 *hi, float4 *lo) {
     const float4 h = make_float4(rna_tf32(v[0]), rna_tf32(v[1]), rna_tf32(v[2]), rna_tf32(v[3]));
@@ -617,6 +586,20 @@ bool make_tma_2d(CUtensorMap *map, const float *base, long long rows, int k_exte
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool make_tma_2d_bf16(CUtensorMap *map, const void *base, long long rows, int k_extent, int pitch,
+                      int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)k_extent, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)pitch * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 

@@ -94,5 +94,7 @@ def engine_peak_tflops(math: str, peaks: dict | None = None) -> float:
     peaks = peaks or measured_peaks()
     if math == "fp32":
         return fp32_alu_tflops(peaks["sm_max_mhz"])
+    if math == "3xbf16":  # three bf16 products per fp32-grade product
+        return peaks["bf16_tflops"] / 3.0
     tf32 = peaks["bf16_tflops"] * TF32_OVER_BF16
     return tf32 if math == "tf32" else tf32 / 3.0

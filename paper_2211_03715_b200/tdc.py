@@ -17,8 +17,9 @@ LIB_PATH = os.environ.get("TDC_LIB") or os.path.join(HERE, "libtdc.so")
 TDC_OK, TDC_ERR_INVALID_ARGUMENT, TDC_ERR_UNSUPPORTED, TDC_ERR_CUDA, \
     TDC_ERR_OUT_OF_MEMORY, TDC_ERR_INTERNAL = range(6)
 TDC_LAYOUT_NCHW, TDC_LAYOUT_NHWC = 0, 1
-TDC_MATH_FP32, TDC_MATH_3XTF32, TDC_MATH_TF32 = 0, 1, 2
-MATH_NAMES = {"fp32": TDC_MATH_FP32, "3xtf32": TDC_MATH_3XTF32, "tf32": TDC_MATH_TF32}
+TDC_MATH_FP32, TDC_MATH_3XTF32, TDC_MATH_TF32, TDC_MATH_3XBF16 = 0, 1, 2, 3
+MATH_NAMES = {"fp32": TDC_MATH_FP32, "3xtf32": TDC_MATH_3XTF32, "tf32": TDC_MATH_TF32,
+              "3xbf16": TDC_MATH_3XBF16}
 
 # Every symbol include/tdc.h declares (checked by tests/test_abi.py).
 EXPORTED = [

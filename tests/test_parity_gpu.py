@@ -14,7 +14,7 @@ from synth import LayerShape
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"fp32": 1e-4, "3xtf32": 1e-4, "tf32": 1e-2}
+TOL = {"fp32": 1e-4, "3xtf32": 1e-4, "3xbf16": 1e-4, "tf32": 1e-2}
 
 
 @pytest.fixture(scope="module")
@@ -57,7 +57,7 @@ def ref_of(shape, d, b=None):
     return oracle.tkd_stages(x, d["core"], d["u_in"], d["u_out"], d["bias"], shape.stride, shape.pad)
 
 
-MATHS = ["fp32", "tf32", "3xtf32"]
+MATHS = ["fp32", "tf32", "3xtf32", "3xbf16"]
 
 
 @pytest.mark.parametrize("math", MATHS)
@@ -70,11 +70,11 @@ def test_config1(env, layout, math):
     assert err(got, ref_of(s, d)) <= TOL[math]
 
 
-@pytest.mark.parametrize("math", ["fp32", "3xtf32"])
+@pytest.mark.parametrize("math", ["fp32", "3xtf32", "3xbf16"])
 @pytest.mark.parametrize("layout", ["nhwc", "nchw"])
 def test_integer_layer_is_bit_exact(env, layout, math):
-    """Every partial sum is an integer < 2^22: fp32 FFMA and the exact 3xTF32 split
-    (hi = value, lo = 0) must reproduce the oracle bit for bit."""
+    """Every partial sum is an integer < 2^16: fp32 FFMA and the exact hi/lo splits
+    (3xTF32, 3xBF16: hi + lo == value) must reproduce the oracle bit for bit."""
     s = LayerShape(2, 16, 16, 8, 8, 4, 4, 3, 1, 1)
     d = synth.make_layer(s, integer=True, bias=True)
     got, _ = run_layer(env, s, d, layout, math)
