@@ -50,9 +50,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["tdc", "reference"], default="tdc")
-    ap.add_argument("--math", choices=["fp32", "tf32", "3xtf32", "3xbf16"], default="3xtf32",
-                    help="3xtf32: fp32-accurate tensor-core split (default); tf32: 1e-2 mode; "
-                         "fp32: CUDA-core FFMA")
+    ap.add_argument("--math", choices=["fp32", "tf32", "3xtf32", "3xbf16"], default="3xbf16",
+                    help="3xbf16 (default) / 3xtf32: fp32-accurate tensor-core splits; "
+                         "tf32: 1e-2 mode; fp32: CUDA-core FFMA")
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
