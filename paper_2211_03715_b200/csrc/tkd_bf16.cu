@@ -30,6 +30,24 @@ namespace tdc {
 
 using namespace sm100;
 
+#ifdef TDC_TIMELINE
+__device__ unsigned long long g_tdc_bf_tl[4 * 64 * 8];
+__device__ unsigned int g_tdc_bf_seq;
+__device__ __forceinline__ void bftl(int seq, int it, int ev) {
+    if (blockIdx.x == 0 && it < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_tdc_bf_tl[((seq & 3) * 64 + it) * 8 + ev] = t;
+    }
+}
+extern "C" int tdc_debug_bf_timeline(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_tdc_bf_tl, sizeof(unsigned long long) * n);
+}
+#define BFTL(seq, it, ev) bftl((seq), (it), (ev))
+#else
+#define BFTL(seq, it, ev) ((void)0)
+#endif
+
 constexpr int kBM16 = 128;
 constexpr int kBK16 = 64;                       // bf16 elements per K chunk = one 128 B row
 constexpr int kATile16 = kBM16 * kBK16 * 2;     // 16 KB per hi or lo tile
@@ -71,8 +89,10 @@ __device__ __forceinline__ void warp_store_block32_b16(float *scratch, const uin
 }
 
 // ============================================================ GEMM (stages 1, 3)
+constexpr int kConvThreads16 = 256;  // 8 converter warps (stage 1 is converter-paced otherwise)
+
 template <bool CONVERT>
-__global__ void __launch_bounds__(CONVERT ? 320 : 192, 1)
+__global__ void __launch_bounds__(CONVERT ? 192 + kConvThreads16 : 192, 1)
 tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo,
                    const TcGemmArgs g) {
@@ -98,11 +118,14 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     const int mtiles = (g.M + kBM16 - 1) / kBM16;
     const int num_tiles = mtiles * g.ntiles;
     const int iters = g.taps * g.kchunks;
+#ifdef TDC_TIMELINE
+    const int seq = (int)*(volatile unsigned int *)&g_tdc_bf_seq;
+#endif
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&conv[i], 128);
+            mbar_init(&conv[i], kConvThreads16);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -124,11 +147,13 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     if (warp == 0) {  // ------------------------------------- TMA producer
         const uint32_t bytes = 2 * kATile16 + 2 * b_tile;  // staging fp32 == A hi + A lo bytes
         Ring r(S);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int tit = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tit) {
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
             int tap = 0, kc = 0;
             for (int i = 0; i < iters; ++i, r.next()) {
                 mbar_wait(&empty[r.slot], r.phase ^ 1);
+                if (i == 0 && lane == 0) BFTL(seq, tit, 0);  // producer issues tile
                 if (elect_one()) {
                     uint8_t *base = smem + (size_t)r.slot * slot_bytes;
                     mbar_arrive_expect_tx(&full[r.slot], bytes);
@@ -157,13 +182,16 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         const uint64_t db = sdesc_kmajor_sw128(smem_u32(smem + kATile16));
         const uint32_t lo = half >> 4;
         Ring r(S), acc(2);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next()) {
+        int tit = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next(), ++tit) {
             mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
             tc_fence_after();
+            if (lane == 0) BFTL(seq, tit, 1);  // MMA: accumulator free
             const uint32_t d = tmem + acc.slot * ncols;
             for (int i = 0; i < iters; ++i, r.next()) {
                 mbar_wait(CONVERT ? &conv[r.slot] : &full[r.slot], r.phase);
                 tc_fence_after();
+                if (i == 0 && lane == 0) BFTL(seq, tit, 2);  // MMA: operands ready
                 if (elect_one()) {
                     const uint64_t a = da + ((r.slot * slot_bytes) >> 4);
                     const uint64_t b = db + ((r.slot * slot_bytes) >> 4);
@@ -179,15 +207,18 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             }
             if (elect_one()) mma_commit(&tfull[acc.slot]);
             __syncwarp();
+            if (lane == 0) BFTL(seq, tit, 3);  // MMA: issued
         }
     } else if (warp < 6) {  // --------------------------------- epilogue
         const int q = warp & 3;
         float *scratch = epi_scratch + q * 1024;
         Ring acc(2);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next()) {
+        int tit = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next(), ++tit) {
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
             mbar_wait(&tfull[acc.slot], acc.phase);
             tc_fence_after();
+            if (warp == 2 && lane == 0) BFTL(seq, tit, 4);  // epilogue: accumulator ready
             long long dst_row = 0;
             const bool valid = remap_row(g, m0 + q * 32 + lane, &dst_row);
             const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
@@ -229,18 +260,21 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             }
             tc_fence_before();
             mbar_arrive_relaxed(&tempty[acc.slot]);
+            if (warp == 2 && lane == 0) BFTL(seq, tit, 5);  // epilogue: done
         }
     } else if (CONVERT) {  // --------------- converter: fp32 staging -> bf16 hi/lo tiles
         const int tid = threadIdx.x - 192;
         Ring r(S);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int tit = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tit) {
             for (int i = 0; i < iters; ++i, r.next()) {
                 mbar_wait(&full[r.slot], r.phase);
+                if (i == 0 && tid == 0) BFTL(seq, tit, 6);  // converter: X landed
                 const uint32_t base = smem_u32(smem + (size_t)r.slot * slot_bytes);
                 const uint32_t stage = base + 2 * half;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int item = k * 128 + tid;        // row r, 8-channel chunk c8
+                for (int k = 0; k < 1024 / kConvThreads16; ++k) {
+                    const int item = k * kConvThreads16 + tid;  // row r, 8-channel chunk c8
                     const int row = item >> 3, c8 = item & 7;
                     const uint32_t box = stage + (uint32_t)(c8 >> 2) * (kStage32 / 2) + row * 128;
                     const int j0 = (c8 & 3) * 2;              // fp32 16-byte chunk index in the box
@@ -259,12 +293,16 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                 }
                 fence_proxy_async_smem();
                 mbar_arrive(&conv[r.slot]);
+                if (i == iters - 1 && tid == 0) BFTL(seq, tit, 7);  // converter: done
             }
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 2 * ncols);
+#ifdef TDC_TIMELINE
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_tdc_bf_seq, 1u);
+#endif
 }
 
 int bf_smem_bytes(int BN, int stages, int convert) {
@@ -286,7 +324,7 @@ cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, c
     if (g.a_convert) {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        tdc_bf_gemm_kernel<true><<<grid, 320, smem, st>>>(mapA, mapAlo, mapB, mapBlo, g);
+        tdc_bf_gemm_kernel<true><<<grid, 192 + kConvThreads16, smem, st>>>(mapA, mapAlo, mapB, mapBlo, g);
     } else {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
