@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace tdc {
 
 // Packed weights produced at plan time (§8(a) row a0; CRSN idea).
@@ -125,5 +127,26 @@ cudaError_t nchw_to_nhwc(const float *src, float *dst, int B, int C, int H, int 
                          cudaStream_t st);
 cudaError_t nhwc_to_nchw(const float *src, float *dst, int B, int C, int H, int W,
                          cudaStream_t st);
+
+// Launch a tcgen05 kernel with programmatic dependent launch (PDL) when enabled
+// (default; TDC_NO_PDL=1 disables): the kernel's prologue (barrier init, TMEM
+// alloc, descriptor prefetch) overlaps the tail of the previous kernel in the
+// stream; the kernel calls griddepcontrol.wait before touching global memory.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, int smem, cudaStream_t st,
+                       Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace tdc

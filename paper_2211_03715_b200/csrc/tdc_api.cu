@@ -14,6 +14,16 @@
 #include <string>
 #include <vector>
 
+namespace tdc {
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *v = std::getenv("TDC_NO_PDL");
+        return !(v && v[0] && v[0] != '0');
+    }();
+    return on;
+}
+}  // namespace tdc
+
 namespace {
 
 thread_local std::string g_last_error;

@@ -142,6 +142,8 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();
+    pdl_launch_dependents();
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {  // ------------------------------------- TMA producer
@@ -324,11 +326,11 @@ cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, c
     if (g.a_convert) {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        tdc_bf_gemm_kernel<true><<<grid, 192 + kConvThreads16, smem, st>>>(mapA, mapAlo, mapB, mapBlo, g);
+        return launch_pdl(tdc_bf_gemm_kernel<true>, grid, 192 + kConvThreads16, smem, st, mapA, mapAlo, mapB, mapBlo, g);
     } else {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        tdc_bf_gemm_kernel<false><<<grid, 192, smem, st>>>(mapA, mapAlo, mapB, mapBlo, g);
+        return launch_pdl(tdc_bf_gemm_kernel<false>, grid, 192, smem, st, mapA, mapAlo, mapB, mapBlo, g);
     }
     return cudaGetLastError();
 }
@@ -390,6 +392,8 @@ __global__ void __launch_bounds__(192, 1) tdc_bf_core_kernel(const TcCoreArgs g)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();
+    pdl_launch_dependents();
     const uint32_t tmem = *tmem_slot;
     const uint32_t band_bytes = (uint32_t)g.band_rows * 16;
 
@@ -521,8 +525,7 @@ cudaError_t bf_core_launch(const TcCoreArgs &g, int grid, cudaStream_t st) {
     const int smem = bf_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.b_stages);
     cudaError_t e = cudaFuncSetAttribute(tdc_bf_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    tdc_bf_core_kernel<<<grid, 192, smem, st>>>(g);
-    return cudaGetLastError();
+    return launch_pdl(tdc_bf_core_kernel, grid, 192, smem, st, g);
 }
 
 }  // namespace tdc

@@ -116,6 +116,8 @@ tdc_tkd_fused_tc_kernel(const __grid_constant__ CUtensorMap mapX, const FusedArg
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();
+    pdl_launch_dependents();
     const uint32_t tmem = *tmem_slot;
 
     const int kc1 = g.c_chunks, kc2 = g.D1s / 32, kc3 = g.D2s / 32;
@@ -378,8 +380,7 @@ cudaError_t fused_launch(const CUtensorMap &mapX, const FusedArgs &g, int grid,
     cudaError_t e = cudaFuncSetAttribute(tdc_tkd_fused_tc_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    tdc_tkd_fused_tc_kernel<<<grid, kFusedThreads, smem, st>>>(mapX, g);
-    return cudaGetLastError();
+    return launch_pdl(tdc_tkd_fused_tc_kernel, grid, kFusedThreads, smem, st, mapX, g);
 }
 
 }  // namespace tdc

@@ -177,6 +177,8 @@ tdc_tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();
+    pdl_launch_dependents();
     if (threadIdx.x == 0) GTL(1);  // setup done (barriers + TMEM)
     const uint32_t tmem = *tmem_slot;
 
@@ -413,6 +415,8 @@ __global__ void __launch_bounds__(kCoreThreads, 1) tdc_tc_core_kernel(const TcCo
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();
+    pdl_launch_dependents();
     const uint32_t tmem = *tmem_slot;
     const uint32_t band_bytes = (uint32_t)g.band_rows * 16;
 
@@ -550,11 +554,11 @@ cudaError_t tc_core_launch(const TcCoreArgs &g, int grid, cudaStream_t st) {
     if (g.split) {
         e = cudaFuncSetAttribute(tdc_tc_core_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        tdc_tc_core_kernel<true><<<grid, kCoreThreads, smem, st>>>(g);
+        return launch_pdl(tdc_tc_core_kernel<true>, grid, kCoreThreads, smem, st, g);
     } else {
         e = cudaFuncSetAttribute(tdc_tc_core_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        tdc_tc_core_kernel<false><<<grid, kCoreThreads, smem, st>>>(g);
+        return launch_pdl(tdc_tc_core_kernel<false>, grid, kCoreThreads, smem, st, g);
     }
     return cudaGetLastError();
 }
@@ -625,11 +629,11 @@ cudaError_t tc_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo,
     if (g.split) {
         e = cudaFuncSetAttribute(tdc_tc_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        tdc_tc_gemm_kernel<true><<<grid, 320, smem, st>>>(mapA, mapAlo, mapB, mapBlo, g);
+        return launch_pdl(tdc_tc_gemm_kernel<true>, grid, 320, smem, st, mapA, mapAlo, mapB, mapBlo, g);
     } else {
         e = cudaFuncSetAttribute(tdc_tc_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        tdc_tc_gemm_kernel<false><<<grid, 192, smem, st>>>(mapA, mapAlo, mapB, mapBlo, g);
+        return launch_pdl(tdc_tc_gemm_kernel<false>, grid, 192, smem, st, mapA, mapAlo, mapB, mapBlo, g);
     }
     return cudaGetLastError();
 }

@@ -1,0 +1,118 @@
+// Microbenchmark v2: issue throughput of back-to-back tcgen05.mma (cta_group::1)
+// with everything compile-time (no runtime branches around the MMA, descriptors
+// precomputed in uniform registers), to separate the tensor-pipe floor from
+// issue-loop overheads.  Debug tool, not product.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2211_03715_b200/csrc
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "sm100.cuh"
+
+using namespace tdc::sm100;
+
+// TS: A from TMEM (cols 256..), SS: A from smem (sw128 K-major).
+template <int BF, int M, int N, int TS, int ELECT, int COLS>
+__global__ void bench(int iters, long long *out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t slot;
+    for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x)
+        reinterpret_cast<float *>(smem)[i] = 0.001f * (i % 7);
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    fence_proxy_async_smem();
+    if (warp == 0) tmem_alloc(&slot, COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    if (warp == 0) {
+        const uint64_t ad = sdesc_kmajor_sw128(smem_u32(smem));
+        const uint64_t bd = sdesc_kmajor_sw128(smem_u32(smem + 32768));
+        const uint32_t id = BF ? idesc_bf16(M, N) : idesc_tf32(M, N);
+        __syncwarp();
+        long long t0 = clock64();
+        if (ELECT) {
+            for (int i = 0; i < iters; i += 4) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (elect_one()) {
+                        if (TS) {
+                            if (BF) mma_bf16_ts(tmem, tmem + 256 + k * 8, bd + k * 2, id, 1);
+                            else mma_tf32_ts(tmem, tmem + 256 + k * 8, bd + k * 2, id, 1);
+                        } else {
+                            if (BF) mma_bf16(tmem, ad + k * 2, bd + k * 2, id, 1);
+                            else mma_tf32(tmem, ad + k * 2, bd + k * 2, id, 1);
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            if (elect_one()) mma_commit(&bar);
+        } else if (threadIdx.x == 0) {
+            for (int i = 0; i < iters; i += 4) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (TS) {
+                        if (BF) mma_bf16_ts(tmem, tmem + 256 + k * 8, bd + k * 2, id, 1);
+                        else mma_tf32_ts(tmem, tmem + 256 + k * 8, bd + k * 2, id, 1);
+                    } else {
+                        if (BF) mma_bf16(tmem, ad + k * 2, bd + k * 2, id, 1);
+                        else mma_tf32(tmem, ad + k * 2, bd + k * 2, id, 1);
+                    }
+                }
+            }
+            mma_commit(&bar);
+        }
+        __syncwarp();
+        mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, COLS);
+}
+
+template <int BF, int M, int N, int TS, int ELECT>
+void run(long long *d, int ctas_per_sm) {
+    auto k = ctas_per_sm == 1 ? bench<BF, M, N, TS, ELECT, 512> : bench<BF, M, N, TS, ELECT, 256>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+    const int iters = 4096, grid = 148 * ctas_per_sm;
+    k<<<grid, 128, 66 * 1024>>>(iters, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h[512];
+    cudaMemcpy(h, d, 8 * grid, cudaMemcpyDeviceToHost);
+    double mx = 0, sum = 0;
+    for (int i = 0; i < grid; ++i) {
+        mx = h[i] > mx ? h[i] : mx;
+        sum += h[i];
+    }
+    const double kk = BF ? 16 : 8;
+    printf("[%d CTA/SM] %s M=%3d N=%3d %s %s  %7.1f cyc/mma (max)  %7.1f (mean)  %6.0f MAC/cyc/SM  floor %5.1f %s\n",
+           ctas_per_sm, BF ? "bf16" : "tf32", M, N, TS ? "TS" : "SS", ELECT ? "elect-warp" : "thread0   ",
+           mx / iters, sum / grid / iters, M * N * kk * iters / mx * ctas_per_sm, (M < 128 ? 128 : M) * N / 256.0,
+           e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
+int main() {
+    long long *d;
+    cudaMalloc(&d, 8 * 512);
+#define ALLN(BF, M, TS, E) run<BF, M, 32, TS, E>(d, 1); run<BF, M, 64, TS, E>(d, 1); \
+    run<BF, M, 128, TS, E>(d, 1); run<BF, M, 256, TS, E>(d, 1);
+    ALLN(1, 128, 0, 0)
+    ALLN(1, 128, 0, 1)
+    ALLN(1, 128, 1, 0)
+    ALLN(1, 64, 0, 0)
+    ALLN(0, 128, 0, 0)
+    ALLN(0, 128, 1, 0)
+    run<1, 128, 32, 0, 0>(d, 2);
+    run<1, 128, 64, 0, 0>(d, 2);
+    run<1, 128, 128, 0, 0>(d, 2);
+    return 0;
+}
