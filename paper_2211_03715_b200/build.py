@@ -31,19 +31,24 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, timeline: bool = False) -> str:
+    """timeline=True builds the debug variant libtdc_tl.so (-DTDC_TIMELINE: per-tile
+    %globaltimer events of CTA 0, read by scripts/*timeline.py via TDC_LIB)."""
+    lib = LIB.replace("libtdc.so", "libtdc_tl.so") if timeline else LIB
+    if not force and not timeline and up_to_date():
         return LIB
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = lib + f".{os.getpid()}.tmp"
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
            "-shared", "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources()]
+    if timeline:
+        cmd.insert(1, "-DTDC_TIMELINE")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, timeline="--timeline" in sys.argv))

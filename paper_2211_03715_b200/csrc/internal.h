@@ -54,6 +54,7 @@ struct TcGemmArgs {
     float *out_lo;    // split only: epilogue also writes the lo part of the output (next stage's A lo)
     int ntiles;       // N tiles (persistent kernel walks mtiles x ntiles)
     int out_bf16;     // 3xBF16 stage 1: out/out_lo are bf16 planar [c/8][row][8], planar_stride in rows
+    int xstages;      // 3xBF16 stage 1: depth of the fp32 staging ring (separate from `stages`)
 };
 
 // Stage-2 core convolution with a shared-memory-resident X' band (tkd_tc.cu):
@@ -113,12 +114,36 @@ bool fused_make_x_map(CUtensorMap *map, const float *x, const FusedArgs &g);
 cudaError_t fused_launch(const CUtensorMap &mapX, const FusedArgs &g, int grid, cudaStream_t st);
 
 // ---- 3xBF16 variant of the 3-launch path (tkd_bf16.cu) ----
-int bf_smem_bytes(int BN, int stages, int convert);
-int bf_pick_stages(int BN, int max_smem, int convert);
+int bf_smem_bytes(int BN, int stages, int xstages);
+int bf_pick_stages(int BN, int max_smem, int convert, int *xstages);
 cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, const CUtensorMap &mapB,
                            const CUtensorMap &mapBlo, const TcGemmArgs &g, int grid, cudaStream_t st);
-int bf_core_smem_bytes(int BN, int nphase, int band_rows, int b_stages);
-cudaError_t bf_core_launch(const TcCoreArgs &g, int grid, cudaStream_t st);
+// 3xBF16 stage-2 core convolution (tkd_bf16.cu).  X' hi/lo planar bf16
+// [D1s/8][rows_total][8]; weights blocked [kc][ntile][group][tg taps][plane 4][2BN][8]
+// with rows 0..BN-1 = hi and BN..2BN-1 = lo, so one bulk copy moves a whole
+// (kc, tap-group) slice and, when 2BN <= 128, one N = 2BN MMA covers hi and lo.
+struct BfCoreArgs {
+    const uint16_t *xg, *xg_lo;
+    long long plane_rows;     // rows_total: rows between 8-channel planes
+    const uint16_t *w;
+    uint16_t *z, *z_lo;       // Z hi/lo [B*Ho*Wo][ldz]
+    int ldz, Nn, M;
+    int kchunks, taps, ntiles, BN, nphase, band_rows;
+    int tg, ngroups, w_slots, w_resident, ncat;
+    long long phase_rows;
+    int tap_phase[kMaxTaps], tap_off[kMaxTaps], phase_src[kMaxTaps];
+    int Hq, Wq, Ho, Wo;
+    // fused stage 3 (tdc_bf_core3_kernel): Z stays on chip, Y = Z . U_out^T (+bias)
+    const uint16_t *w3;       // U_out blocked [D2s/8 planes][2*N3p rows: hi | lo][8], resident
+    const float *bias;
+    float *y;                 // Y [B*Ho*Wo][N3]
+    int N3, N3p, ncat3;       // output channels, padded (mult. of 16), hi|lo concat in one MMA
+};
+int bf_core_smem_bytes(int BN, int nphase, int band_rows, int tg, int w_slots);
+int bf_core3_smem_bytes(const BfCoreArgs &g);
+int bf_core3_tmem_cols(const BfCoreArgs &g);
+cudaError_t bf_core3_launch(const BfCoreArgs &g, int grid, cudaStream_t st);
+cudaError_t bf_core_launch(const BfCoreArgs &g, int grid, cudaStream_t st);
 bool make_tma_2d_bf16(CUtensorMap *map, const void *base, long long rows, int k_extent, int pitch,
                       int box_rows);
 

@@ -124,6 +124,8 @@ struct tdc_conv_plan_s {
     bool bf16x3 = false;           // 3xBF16 (variant 4 uses tc[] maps + core_args, bf16 formats)
 
     tdc::TcCoreArgs core_args;
+    tdc::BfCoreArgs bf_core;
+    bool fuse3 = false;            // 3xBF16: core + stage 3 in one kernel (Z on chip)
     float *d_tc_w = nullptr;       // Bt1 | Bt2 | Bt3 | bias
     float *d_xg = nullptr;         // X' phase grids (zero borders)
     float *d_z = nullptr;          // Z compact
@@ -418,45 +420,118 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
                 phase_of[r * K + t] = idx_of[ph];
             }
     }
-    int core_stages = 4;
-    for (;;) {
-        while (core_stages > 2 && tdc::bf_core_smem_bytes(BN2, nphase, band_rows, core_stages) > p->max_smem)
-            --core_stages;
-        if (BN2 <= 64 || tdc::bf_core_smem_bytes(BN2, nphase, band_rows, core_stages) <= p->max_smem) break;
-        BN2 /= 2;
-        core_stages = 4;
+    // Stage-2 weight staging: one bulk copy per (kc, tap group) slice
+    // of tg taps x [4 planes][2*BN2 rows (hi | lo)][8]; resident for the CTA's
+    // lifetime when the whole N tile fits, otherwise a ring of w_slots slices.
+    const int k2chunks = D1s / 32;
+    int tg = 0, w_slots = 0, resident = 0, nt2 = 0;
+    // Fused core + stage 3 (Z stays on chip) when the whole D2 fits one N tile, the
+    // U_out panel is resident and both double-buffered accumulators fit in TMEM.
+    const int N3p = round_up(N, 32), ncat3 = 2 * N3p <= 128;
+    int fuse3 = 0;
+    {
+        const char *ev = std::getenv("TDC_NO_FUSE3");
+        const bool off = ev && ev[0] && ev[0] != '0';
+        int bn = 32;
+        while (bn < D2s) bn *= 2;
+        if (!off && bn <= 128 && (ncat3 ? 2 * N3p : N3p) <= 256) {
+            tdc::BfCoreArgs t;
+            std::memset(&t, 0, sizeof t);
+            t.BN = bn; t.nphase = nphase; t.band_rows = band_rows; t.N3p = N3p;
+            t.ncat = 2 * bn <= 128; t.ncat3 = ncat3;
+            if (tdc::bf_core3_tmem_cols(t) <= 512) {
+                t.tg = KK; t.w_slots = k2chunks;
+                if (tdc::bf_core3_smem_bytes(t) <= p->max_smem) {
+                    tg = KK; w_slots = k2chunks; resident = 1;
+                } else {
+                    for (int g = KK; g >= 1 && !tg; --g) {
+                        if (KK % g) continue;
+                        for (int ws = 4; ws >= 2; --ws) {
+                            t.tg = g; t.w_slots = ws;
+                            if (tdc::bf_core3_smem_bytes(t) <= p->max_smem) {
+                                tg = g; w_slots = ws;
+                                break;
+                            }
+                        }
+                    }
+                }
+                if (tg) {
+                    fuse3 = 1;
+                    BN2 = bn;
+                    nt2 = 1;
+                }
+            }
+        }
     }
-    if (tdc::bf_core_smem_bytes(BN2, nphase, band_rows, core_stages) > p->max_smem) return TDC_OK;
-    const int R1 = round_up(D1s, BN1), R2 = round_up(D2s, BN2), R3 = round_up(N, BN3);
-    const int k2chunks = D1s / 32, nt2 = R2 / BN2;
+    for (; !fuse3 && BN2 >= 32; BN2 /= 2) {
+        nt2 = div_up(D2s, BN2);
+        if (nt2 == 1 && tdc::bf_core_smem_bytes(BN2, nphase, band_rows, KK, k2chunks) <= p->max_smem) {
+            tg = KK;
+            w_slots = k2chunks;
+            resident = 1;
+            break;
+        }
+        for (int g = KK; g >= 1 && !tg; --g) {
+            if (KK % g) continue;
+            for (int ws = 4; ws >= 2; --ws)
+                if (tdc::bf_core_smem_bytes(BN2, nphase, band_rows, g, ws) <= p->max_smem) {
+                    tg = g;
+                    w_slots = ws;
+                    break;
+                }
+        }
+        if (tg) break;
+    }
+    if (!tg) return TDC_OK;
+    const int ngroups = KK / tg;
+    const int ncat = 2 * BN2 <= 128;  // one N = 2*BN2 MMA covers the hi and lo weights
+    const int R1 = round_up(D1s, BN1), R2 = nt2 * BN2, R3 = round_up(N, BN3);
     const long long rows_total = (long long)s * s * phase_rows + band_rows + 128;
 
     // ---- a0: bf16 hi/lo weight panels (CRSN idea) ----
-    const size_t n1 = (size_t)R1 * C64, n2 = (size_t)KK * R2 * D1s, n3 = (size_t)R3 * D2p;
-    const size_t nw = n1 + n2 + n3;
+    // stages 1/3: [all hi][all lo] K-major panels; stage 2: hi/lo interleaved slices.
+    const size_t n1 = (size_t)R1 * C64, n3 = (size_t)R3 * D2p, nw = n1 + n3;
+    const size_t n2 = (size_t)KK * R2 * D1s;  // per hi or lo
+    const size_t n3f = fuse3 ? (size_t)BN2 * 2 * N3p : 0;  // fused stage-3 panel (hi|lo rows)
     std::vector<float> wf(nw, 0.f);  // fp32 staging in the final element order
-    float *w1 = wf.data(), *w2 = w1 + n1, *w3 = w2 + n2;
+    float *w1 = wf.data(), *w3 = w1 + n1;
     for (int a = 0; a < D1; ++a)
         for (int c = 0; c < C; ++c) w1[(size_t)a * C64 + c] = u_in[(size_t)c * D1 + a];
-    for (int r = 0; r < K; ++r)
-        for (int t = 0; t < K; ++t)
-            for (int q = 0; q < D2; ++q)
-                for (int a = 0; a < D1; ++a) {
-                    // blocked [tap][kc(32)][ntile][plane(4)][BN2][8] no-swizzle K-major chunks
-                    const int kc = a / 32, pl = (a % 32) / 8, e = a % 8, tap = r * K + t;
-                    const int ntl = q / BN2, n = q % BN2;
-                    w2[((((size_t)(tap * k2chunks + kc) * nt2 + ntl) * 4 + pl) * BN2 + n) * 8 + e] =
-                        core[(((size_t)q * D1 + a) * K + r) * K + t];
-                }
     for (int n = 0; n < N; ++n)
         for (int q = 0; q < D2; ++q) w3[(size_t)n * D2p + q] = u_out[(size_t)n * D2 + q];
-    std::vector<uint16_t> hb(2 * nw);
+    std::vector<uint16_t> hb(2 * nw + 2 * n2 + n3f, 0);
     for (size_t i = 0; i < nw; ++i) {
         const uint16_t hi = bf16_bits_host(wf[i]);
         hb[i] = hi;
         hb[nw + i] = bf16_bits_host(wf[i] - bf16_to_float_host(hi));
     }
-    const size_t wbytes = 2 * nw * sizeof(uint16_t), nbias = round_up(N, 4);
+    uint16_t *w2 = hb.data() + 2 * nw;
+    for (int r = 0; r < K; ++r)
+        for (int t = 0; t < K; ++t)
+            for (int q = 0; q < D2; ++q)
+                for (int a = 0; a < D1; ++a) {
+                    // [kc][ntile][group][tt][plane(4)][2*BN2][8]: row n = hi, BN2 + n = lo
+                    const int kc = a / 32, pl = (a % 32) / 8, e = a % 8, tap = r * K + t;
+                    const int ntl = q / BN2, n = q % BN2, grp = tap / tg, tt = tap % tg;
+                    const size_t base =
+                        (((((size_t)kc * nt2 + ntl) * ngroups + grp) * tg + tt) * 4 + pl) * 2 * BN2;
+                    const float v = core[(((size_t)q * D1 + a) * K + r) * K + t];
+                    const uint16_t hi = bf16_bits_host(v);
+                    w2[(base + n) * 8 + e] = hi;
+                    w2[(base + BN2 + n) * 8 + e] = bf16_bits_host(v - bf16_to_float_host(hi));
+                }
+    if (fuse3) {  // [D2/8 planes][2*N3p rows: hi n | lo N3p + n][8]
+        uint16_t *w3f = w2 + 2 * n2;
+        for (int n = 0; n < N; ++n)
+            for (int q = 0; q < D2; ++q) {
+                const float v = u_out[(size_t)n * D2 + q];
+                const uint16_t hi = bf16_bits_host(v);
+                const size_t row = (size_t)(q / 8) * 2 * N3p;
+                w3f[(row + n) * 8 + q % 8] = hi;
+                w3f[(row + N3p + n) * 8 + q % 8] = bf16_bits_host(v - bf16_to_float_host(hi));
+            }
+    }
+    const size_t wbytes = hb.size() * sizeof(uint16_t), nbias = round_up(N, 4);
     cudaError_t e = cudaMalloc(&p->d_tc_w, wbytes + nbias * sizeof(float));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(bf16 weights)");
     e = cudaMemcpy(p->d_tc_w, hb.data(), wbytes, cudaMemcpyHostToDevice);
@@ -469,18 +544,19 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(bf16 weights)");
     p->weight_bytes += wbytes + nbias * sizeof(float);
     const uint16_t *wb = reinterpret_cast<const uint16_t *>(p->d_tc_w);
-    const uint16_t *dB1 = wb, *dB2 = wb + n1, *dB3 = wb + n1 + n2;
-    const uint16_t *dB1lo = dB1 + nw, *dB2lo = dB2 + nw, *dB3lo = dB3 + nw;
+    const uint16_t *dB1 = wb, *dB3 = wb + n1, *dB2 = wb + 2 * nw;
+    const uint16_t *dB1lo = dB1 + nw, *dB3lo = dB3 + nw;
     const float *dbias =
         bias ? reinterpret_cast<const float *>(reinterpret_cast<uint8_t *>(p->d_tc_w) + wbytes) : nullptr;
 
     // ---- workspaces: X' hi/lo planar bf16 (zero borders), Z hi/lo bf16 [M3][D2p] ----
-    const size_t xg_elems = (size_t)rows_total * D1s, z_elems = (size_t)M3 * D2p;
+    const size_t xg_elems = (size_t)rows_total * D1s, z_elems = fuse3 ? 0 : (size_t)M3 * D2p;
     e = cudaMalloc(&p->d_xg, 2 * xg_elems * sizeof(uint16_t));
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_z, 2 * z_elems * sizeof(uint16_t));
+    if (e == cudaSuccess && z_elems) e = cudaMalloc(&p->d_z, 2 * z_elems * sizeof(uint16_t));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(bf16 workspace)");
     e = cudaMemset(p->d_xg, 0, 2 * xg_elems * sizeof(uint16_t));
-    if (e == cudaSuccess) e = cudaMemset(p->d_z, 0, 2 * z_elems * sizeof(uint16_t));  // pad columns stay 0
+    if (e == cudaSuccess && z_elems)
+        e = cudaMemset(p->d_z, 0, 2 * z_elems * sizeof(uint16_t));  // pad columns stay 0
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(bf16 workspace)");
     p->tc_ws_bytes = 2 * (xg_elems + z_elems) * sizeof(uint16_t);
     uint16_t *xg = reinterpret_cast<uint16_t *>(p->d_xg), *xg_lo = xg + xg_elems;
@@ -499,7 +575,7 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         st.args.BN = BN1; st.args.remap = 1; st.args.a_convert = 1; st.args.out_bf16 = 1;
         st.args.out = reinterpret_cast<float *>(xg); st.args.out_lo = reinterpret_cast<float *>(xg_lo);
         st.args.planar_stride = rows_total;  // rows
-        st.args.stages = tdc::bf_pick_stages(BN1, p->max_smem, 1);
+        st.args.stages = tdc::bf_pick_stages(BN1, p->max_smem, 1, &st.args.xstages);
         st.grid_n = R1 / BN1;
         st.args.ntiles = st.grid_n;
         if (!tdc::make_tma_2d_bf16(&st.mapB, dB1, R1, C64, C64, BN1) ||
@@ -507,18 +583,18 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
             return fail(TDC_ERR_CUDA, "%s (stage 1)", enc_err);
     }
     {   // stage 2: band-resident core kernel on bf16 planes
-        tdc::TcCoreArgs &g = p->core_args;
+        tdc::BfCoreArgs &g = p->bf_core;
         std::memset(&g, 0, sizeof g);
-        g.xg = reinterpret_cast<const float *>(xg);
-        g.xg_lo = reinterpret_cast<const float *>(xg_lo);
-        g.plane_stride = rows_total;  // rows
-        g.w = reinterpret_cast<const float *>(dB2);
-        g.w_lo = reinterpret_cast<const float *>(dB2lo);
-        g.z = reinterpret_cast<float *>(z);
-        g.z_lo = reinterpret_cast<float *>(z_lo);
+        g.xg = xg;
+        g.xg_lo = xg_lo;
+        g.plane_rows = rows_total;
+        g.w = dB2;
+        g.z = z;
+        g.z_lo = z_lo;
         g.ldz = D2p; g.Nn = D2s; g.M = (int)M2; g.kchunks = k2chunks; g.taps = KK;
         g.ntiles = nt2; g.BN = BN2; g.nphase = nphase; g.band_rows = band_rows;
-        g.b_stages = core_stages; g.phase_rows = phase_rows;
+        g.tg = tg; g.ngroups = ngroups; g.w_slots = w_slots; g.w_resident = resident; g.ncat = ncat;
+        g.phase_rows = phase_rows;
         for (int r = 0; r < K; ++r)
             for (int t = 0; t < K; ++t) {
                 g.tap_phase[r * K + t] = phase_of[r * K + t];
@@ -526,14 +602,19 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
             }
         for (int i = 0; i < nphase; ++i) g.phase_src[i] = phase_src[i];
         g.Hq = Hq; g.Wq = Wq; g.Ho = Ho; g.Wo = Wo;
-        g.split = 1;
+        if (fuse3) {
+            g.w3 = dB2 + 2 * n2;
+            g.bias = dbias;
+            g.N3 = N; g.N3p = N3p; g.ncat3 = ncat3;
+        }
     }
-    {   // stage 3: A = Z hi/lo bf16, B = U_out bf16; out = Y fp32 (+bias)
+    p->fuse3 = fuse3 != 0;
+    if (!fuse3) {   // stage 3: A = Z hi/lo bf16, B = U_out bf16; out = Y fp32 (+bias)
         auto &st = p->tc[2];
         base_args(st.args);
         st.args.M = (int)M3; st.args.Nn = N; st.args.kchunks = D2p / 64; st.args.taps = 1;
         st.args.BN = BN3; st.args.ldo = N; st.args.remap = 0; st.args.bias = dbias;
-        st.args.stages = tdc::bf_pick_stages(BN3, p->max_smem, 0);
+        st.args.stages = tdc::bf_pick_stages(BN3, p->max_smem, 0, nullptr);
         st.grid_n = R3 / BN3;
         st.args.ntiles = st.grid_n;
         if (!tdc::make_tma_2d_bf16(&st.mapA, z, M3, D2p, D2p, 128) ||
@@ -562,7 +643,7 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
     a1.M = batch * d.H * d.W;
     a3.M = batch * d.Ho * d.Wo;
     a3.out = y;
-    tdc::TcCoreArgs c = p->core_args;
+    tdc::BfCoreArgs c = p->bf_core;
     c.M = batch * a1.Hq * a1.Wq;
     auto grid = [&](long long M, int ntiles, int smem, int bn) {
         const long long tiles = (long long)div_up((int)M, 128) * ntiles;
@@ -571,10 +652,18 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
     };
     cudaError_t e = tdc::bf_gemm_launch(
         s1.mapA, s1.mapA, s1.mapB, s1.mapBlo, a1,
-        grid(a1.M, a1.ntiles, tdc::bf_smem_bytes(a1.BN, a1.stages, 1), a1.BN), st);
+        grid(a1.M, a1.ntiles, tdc::bf_smem_bytes(a1.BN, a1.stages, a1.xstages), a1.BN), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-1 launch");
+    if (p->fuse3) {
+        c.y = y;
+        e = tdc::bf_core3_launch(c, grid(c.M, c.ntiles, tdc::bf_core3_smem_bytes(c), tdc::bf_core3_tmem_cols(c) / 2),
+                                 st);
+        if (e != cudaSuccess) return cuda_fail(e, "3xBF16 fused core+stage-3 launch");
+        return TDC_OK;
+    }
     e = tdc::bf_core_launch(
-        c, grid(c.M, c.ntiles, tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.b_stages), c.BN), st);
+        c, grid(c.M, c.ntiles, tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots),
+                c.ncat ? 2 * c.BN : c.BN), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-2 launch");
     e = tdc::bf_gemm_launch(s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, a3,
                             grid(a3.M, a3.ntiles, tdc::bf_smem_bytes(a3.BN, a3.stages, 0), a3.BN), st);
@@ -954,11 +1043,12 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
     info->variant = p->variant;
     const bool tc = p->variant == 2 || p->variant == 4, fz = p->variant == 3;
     std::snprintf(info->variant_name, sizeof info->variant_name, "%s",
-                  p->variant == 4 ? "tc3_3xbf16_band" : fz ? "fused_tc_tf32"
+                  p->variant == 4 ? (p->fuse3 ? "tc2_3xbf16_core3" : "tc3_3xbf16_band") : fz ? "fused_tc_tf32"
                      : tc ? (p->split ? (p->tc_core ? "tc3_3xtf32_band" : "tc3_3xtf32")
                                       : (p->tc_core ? "tc3_tf32_band" : "tc3_tf32"))
                           : "fused_simt_fp32");
-    info->launches_per_forward = (tc ? 3 : 1) + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
+    info->launches_per_forward =
+        (tc ? (p->variant == 4 && p->fuse3 ? 2 : 3) : 1) + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
     info->concurrent_forward = (p->desc.layout == TDC_LAYOUT_NHWC && !tc) ? 1 : 0;
     info->tile_h = p->simt_tile.oth;
     info->tile_w = p->simt_tile.otw;
@@ -972,6 +1062,13 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
         info->threads_per_cta = 192;
         info->smem_bytes_per_cta = tdc::tc_smem_bytes(p->tc[1].args.BN, p->tc[1].args.stages, p->split);
         info->ctas_per_image = 0;
+    }
+    if (p->variant == 4) {  // stage-2 (core) kernel geometry
+        const tdc::BfCoreArgs &c = p->bf_core;
+        info->tile_w = c.BN;
+        info->threads_per_cta = p->fuse3 ? 320 : 192;
+        info->smem_bytes_per_cta = p->fuse3 ? tdc::bf_core3_smem_bytes(c)
+                                            : tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots);
     }
     if (fz) {
         info->tile_h = p->fargs.R;

@@ -44,8 +44,34 @@ extern "C" int tdc_debug_bf_timeline(unsigned long long *host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_tdc_bf_tl, sizeof(unsigned long long) * n);
 }
 #define BFTL(seq, it, ev) bftl((seq), (it), (ev))
+__device__ unsigned long long g_tdc_bfc_tl[64 * 8];
+__device__ __forceinline__ void bfctl(int it, int ev) {
+    if (blockIdx.x == 0 && it < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_tdc_bfc_tl[it * 8 + ev] = t;
+    }
+}
+extern "C" int tdc_debug_bfc_timeline(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_tdc_bfc_tl, sizeof(unsigned long long) * n);
+}
+#define BFCTL(it, ev) bfctl((it), (ev))
+__device__ unsigned long long g_tdc_bfc_tap[128 * 2];
+__device__ __forceinline__ void bfctap(int i, int ev) {
+    if (blockIdx.x == 0 && i < 128) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_tdc_bfc_tap[i * 2 + ev] = t;
+    }
+}
+extern "C" int tdc_debug_bfc_taps(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_tdc_bfc_tap, sizeof(unsigned long long) * n);
+}
+#define BFCTAP(i, ev) bfctap((i), (ev))
 #else
+#define BFCTAP(i, ev) ((void)0)
 #define BFTL(seq, it, ev) ((void)0)
+#define BFCTL(it, ev) ((void)0)
 #endif
 
 constexpr int kBM16 = 128;
@@ -100,17 +126,22 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = g.stages, BN = g.BN;
+    const int SX = CONVERT ? g.xstages : 0;  // fp32 staging ring depth (stage 1)
     const uint32_t b_tile = (uint32_t)BN * kBK16 * 2;
     const uint32_t half = kATile16 + b_tile;                  // hi -> lo offset
-    const uint32_t slot_bytes = 2 * half + (CONVERT ? kStage32 : 0);
-    // slot: A hi | B hi | A lo | B lo | [fp32 staging of A]
-    float *epi_scratch = reinterpret_cast<float *>(smem + (size_t)S * slot_bytes);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)S * slot_bytes + kEpiScratch16);
-    uint64_t *conv = full + S;
-    uint64_t *empty = conv + S;
+    const uint32_t slot_bytes = 2 * half;                     // A hi | B hi | A lo | B lo
+    // [SX fp32 staging slots][S operand slots][epilogue scratch][barriers]
+    uint8_t *xstage = smem;
+    uint8_t *ops = smem + (size_t)SX * kStage32;
+    float *epi_scratch = reinterpret_cast<float *>(ops + (size_t)S * slot_bytes);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ops + (size_t)S * slot_bytes + kEpiScratch16);
+    uint64_t *conv = full + S;       // CONVERT: A hi/lo written by the converter
+    uint64_t *empty = conv + S;      // operand slot consumed by the MMAs
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *xfull = tempty + 2;    // CONVERT: fp32 X landed in a staging slot
+    uint64_t *xempty = xfull + SX;   // CONVERT: staging slot converted
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xempty + SX);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t ncols = 32;
@@ -132,6 +163,10 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 128);
         }
+        for (int i = 0; i < SX; ++i) {
+            mbar_init(&xfull[i], 1);
+            mbar_init(&xempty[i], kConvThreads16);
+        }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -147,29 +182,33 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {  // ------------------------------------- TMA producer
-        const uint32_t bytes = 2 * kATile16 + 2 * b_tile;  // staging fp32 == A hi + A lo bytes
-        Ring r(S);
+        Ring r(CONVERT ? SX : S);
         int tit = 0;
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tit) {
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
             int tap = 0, kc = 0;
             for (int i = 0; i < iters; ++i, r.next()) {
-                mbar_wait(&empty[r.slot], r.phase ^ 1);
-                if (i == 0 && lane == 0) BFTL(seq, tit, 0);  // producer issues tile
-                if (elect_one()) {
-                    uint8_t *base = smem + (size_t)r.slot * slot_bytes;
-                    mbar_arrive_expect_tx(&full[r.slot], bytes);
-                    if (CONVERT) {  // fp32 X: channels [64kc, 64kc+32) and [64kc+32, 64kc+64)
-                        tma_load_2d(base + 2 * half, &mapA, &full[r.slot], kc * 64, m0 + g.a_off[tap]);
-                        tma_load_2d(base + 2 * half + kStage32 / 2, &mapA, &full[r.slot], kc * 64 + 32,
-                                    m0 + g.a_off[tap]);
-                    } else {
+                if (CONVERT) {  // fp32 X: channels [64kc, 64kc+32) and [64kc+32, 64kc+64)
+                    mbar_wait(&xempty[r.slot], r.phase ^ 1);
+                    if (i == 0 && lane == 0) BFTL(seq, tit, 0);  // producer issues tile
+                    if (elect_one()) {
+                        uint8_t *dst = xstage + (size_t)r.slot * kStage32;
+                        mbar_arrive_expect_tx(&xfull[r.slot], kStage32);
+                        tma_load_2d(dst, &mapA, &xfull[r.slot], kc * 64, m0 + g.a_off[tap]);
+                        tma_load_2d(dst + kStage32 / 2, &mapA, &xfull[r.slot], kc * 64 + 32, m0 + g.a_off[tap]);
+                    }
+                } else {
+                    mbar_wait(&empty[r.slot], r.phase ^ 1);
+                    if (i == 0 && lane == 0) BFTL(seq, tit, 0);
+                    if (elect_one()) {
+                        uint8_t *base = ops + (size_t)r.slot * slot_bytes;
+                        mbar_arrive_expect_tx(&full[r.slot], 2 * kATile16 + 2 * b_tile);
                         tma_load_2d(base, &mapA, &full[r.slot], kc * kBK16, m0 + g.a_off[tap]);
                         tma_load_2d(base + half, &mapAlo, &full[r.slot], kc * kBK16, m0 + g.a_off[tap]);
+                        tma_load_2d(base + kATile16, &mapB, &full[r.slot], kc * kBK16, g.b_off[tap] + n0);
+                        tma_load_2d(base + half + kATile16, &mapBlo, &full[r.slot], kc * kBK16,
+                                    g.b_off[tap] + n0);
                     }
-                    tma_load_2d(base + kATile16, &mapB, &full[r.slot], kc * kBK16, g.b_off[tap] + n0);
-                    tma_load_2d(base + half + kATile16, &mapBlo, &full[r.slot], kc * kBK16,
-                                g.b_off[tap] + n0);
                 }
                 __syncwarp();
                 if (++kc == g.kchunks) {
@@ -180,8 +219,8 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         }
     } else if (warp == 1) {  // ------------------------------ MMA issuer
         const uint32_t idesc = idesc_bf16(kBM16, BN);
-        const uint64_t da = sdesc_kmajor_sw128(smem_u32(smem));
-        const uint64_t db = sdesc_kmajor_sw128(smem_u32(smem + kATile16));
+        const uint64_t da = sdesc_kmajor_sw128(smem_u32(ops));
+        const uint64_t db = sdesc_kmajor_sw128(smem_u32(ops + kATile16));
         const uint32_t lo = half >> 4;
         Ring r(S), acc(2);
         int tit = 0;
@@ -191,7 +230,8 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             if (lane == 0) BFTL(seq, tit, 1);  // MMA: accumulator free
             const uint32_t d = tmem + acc.slot * ncols;
             for (int i = 0; i < iters; ++i, r.next()) {
-                mbar_wait(CONVERT ? &conv[r.slot] : &full[r.slot], r.phase);
+                if (CONVERT) mbar_wait(&conv[r.slot], r.phase);
+                mbar_wait(&full[r.slot], r.phase);
                 tc_fence_after();
                 if (i == 0 && lane == 0) BFTL(seq, tit, 2);  // MMA: operands ready
                 if (elect_one()) {
@@ -264,16 +304,25 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             mbar_arrive_relaxed(&tempty[acc.slot]);
             if (warp == 2 && lane == 0) BFTL(seq, tit, 5);  // epilogue: done
         }
-    } else if (CONVERT) {  // --------------- converter: fp32 staging -> bf16 hi/lo tiles
+    } else if (CONVERT) {  // ------- converter: fp32 staging -> bf16 hi/lo tiles (+ B loads)
         const int tid = threadIdx.x - 192;
-        Ring r(S);
+        Ring r(S), rx(SX);
         int tit = 0;
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tit) {
-            for (int i = 0; i < iters; ++i, r.next()) {
-                mbar_wait(&full[r.slot], r.phase);
+            const int n0 = (t / mtiles) * BN;
+            int tap = 0, kc = 0;
+            for (int i = 0; i < iters; ++i, r.next(), rx.next()) {
+                mbar_wait(&empty[r.slot], r.phase ^ 1);  // operand slot free
+                const uint32_t base = smem_u32(ops + (size_t)r.slot * slot_bytes);
+                if (tid == 0) {  // B = U_in^T hi/lo into the operand slot
+                    uint8_t *bs = ops + (size_t)r.slot * slot_bytes + kATile16;
+                    mbar_arrive_expect_tx(&full[r.slot], 2 * b_tile);
+                    tma_load_2d(bs, &mapB, &full[r.slot], kc * kBK16, g.b_off[tap] + n0);
+                    tma_load_2d(bs + half, &mapBlo, &full[r.slot], kc * kBK16, g.b_off[tap] + n0);
+                }
+                mbar_wait(&xfull[rx.slot], rx.phase);
                 if (i == 0 && tid == 0) BFTL(seq, tit, 6);  // converter: X landed
-                const uint32_t base = smem_u32(smem + (size_t)r.slot * slot_bytes);
-                const uint32_t stage = base + 2 * half;
+                const uint32_t stage = smem_u32(xstage + (size_t)rx.slot * kStage32);
 #pragma unroll
                 for (int k = 0; k < 1024 / kConvThreads16; ++k) {
                     const int item = k * kConvThreads16 + tid;  // row r, 8-channel chunk c8
@@ -293,9 +342,14 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                                  "r"(l.x), "r"(l.y), "r"(l.z), "r"(l.w)
                                  : "memory");
                 }
+                mbar_arrive(&xempty[rx.slot]);  // staging slot may be refilled
                 fence_proxy_async_smem();
                 mbar_arrive(&conv[r.slot]);
                 if (i == iters - 1 && tid == 0) BFTL(seq, tit, 7);  // converter: done
+                if (++kc == g.kchunks) {
+                    kc = 0;
+                    ++tap;
+                }
             }
         }
     }
@@ -307,21 +361,24 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
 #endif
 }
 
-int bf_smem_bytes(int BN, int stages, int convert) {
+int bf_smem_bytes(int BN, int stages, int xstages) {
     const int half = kATile16 + BN * kBK16 * 2;
-    return 1024 + stages * (2 * half + (convert ? kStage32 : 0)) + kEpiScratch16 +
-           (3 * stages + 4) * 8 + 16;
+    return 1024 + xstages * kStage32 + stages * 2 * half + kEpiScratch16 +
+           (3 * stages + 4 + 2 * xstages) * 8 + 16;
 }
 
-int bf_pick_stages(int BN, int max_smem, int convert) {
-    int s = 6;
-    while (s > 2 && bf_smem_bytes(BN, s, convert) > max_smem) --s;
+// Operand-ring depth (and, for the converting stage 1, the fp32 staging depth).
+int bf_pick_stages(int BN, int max_smem, int convert, int *xstages) {
+    int s = convert ? 2 : 6, sx = convert ? 4 : 0;
+    while (sx > 2 && bf_smem_bytes(BN, s, sx) > max_smem) --sx;
+    while (s > 2 && bf_smem_bytes(BN, s, sx) > max_smem) --s;
+    if (xstages) *xstages = sx;
     return s;
 }
 
 cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, const CUtensorMap &mapB,
                            const CUtensorMap &mapBlo, const TcGemmArgs &g, int grid, cudaStream_t st) {
-    const int smem = bf_smem_bytes(g.BN, g.stages, g.a_convert);
+    const int smem = bf_smem_bytes(g.BN, g.stages, g.a_convert ? g.xstages : 0);
     cudaError_t e;
     if (g.a_convert) {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -336,44 +393,84 @@ cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, c
 }
 
 // ============================================================ core conv (stage 2)
-__host__ __device__ inline int bf_core_a_half(int nphase, int band_rows) {
-    return nphase * 4 * band_rows * 16;  // 4 planes of 8 bf16 channels per 32-channel chunk
+// Per tile (128 phase-grid rows x BN output channels) and 32-channel chunk kc: the
+// X' band (hi and lo, every phase the taps use) arrives as 8*nphase plane copies
+// issued from different producer lanes (the TMA engine overlaps copies from
+// different threads; one thread's copies are ~100-200 cycles apart);
+// the weights arrive as one large copy per (kc, tap group) -- or stay resident for
+// the CTA's lifetime when they fit -- and every tap is a row-shifted descriptor.
+__host__ __device__ inline uint32_t bf_core_a_half(int nphase, int band_rows) {
+    return (uint32_t)nphase * 4 * band_rows * 16;  // 4 planes of 8 bf16 channels per chunk
 }
 
-int bf_core_smem_bytes(int BN, int nphase, int band_rows, int b_stages) {
-    return 1024 + 2 * 2 * bf_core_a_half(nphase, band_rows) + b_stages * 2 * BN * 64 + kEpiScratch16 +
-           (4 + 2 * b_stages + 4) * 8 + 16;
+int bf_core_smem_bytes(int BN, int nphase, int band_rows, int tg, int w_slots) {
+    return 1024 + 2 * 2 * (int)bf_core_a_half(nphase, band_rows) + w_slots * tg * BN * 128 + kEpiScratch16 +
+           (8 + 2 * w_slots) * 8 + 16;
 }
 
-__global__ void __launch_bounds__(192, 1) tdc_bf_core_kernel(const TcCoreArgs g) {
+__host__ __device__ inline int bf_pow2_cols(int c) {
+    int n = 32;
+    while (n < c) n *= 2;
+    return n;
+}
+// Fused variant: + two Z hi|lo tile buffers [BN/8 planes][128 rows][16 B] x 2 and the
+// resident U_out hi|lo panel [BN/8 planes][2*N3p rows][16 B], + 9 barriers.
+__host__ __device__ inline int bf_core3_zbuf(const BfCoreArgs &g) { return (g.BN / 8) * 128 * 16 * 2; }
+__host__ __device__ inline int bf_core3_w3(const BfCoreArgs &g) { return (g.BN / 8) * 2 * g.N3p * 16; }
+int bf_core3_smem_bytes(const BfCoreArgs &g) {
+    return bf_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.tg, g.w_slots) + 2 * bf_core3_zbuf(g) +
+           bf_core3_w3(g) + 9 * 8;
+}
+__host__ __device__ inline int bf_core3_tmem(const BfCoreArgs &g) {
+    const int a2 = bf_pow2_cols(g.ncat ? 2 * g.BN : g.BN), a3 = bf_pow2_cols(g.ncat3 ? 2 * g.N3p : g.N3p);
+    return bf_pow2_cols(2 * a2 + 2 * a3);
+}
+int bf_core3_tmem_cols(const BfCoreArgs &g) { return bf_core3_tmem(g); }
+
+// F3 = false: stage 2 alone, Z hi/lo to global (the 3-launch path).
+// F3 = true:  stage 2 + stage 3 in one kernel ("core3"): the Z tile is split into
+// bf16 hi/lo by the epilogue-2 warps straight into shared memory, stage 3 multiplies
+// it with the resident U_out panel, epilogue-3 warps write Y (+bias).  Z never
+// touches HBM.  MMA issue is software-pipelined: S2(tile i) then S3(tile i-1).
+template <bool F3>
+__global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const BfCoreArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int BN = g.BN, SB = g.b_stages;
+    const int BN = g.BN, WS = g.w_slots, TG = g.tg;
+    const uint32_t band_bytes = (uint32_t)g.band_rows * 16;
     const uint32_t a_half = bf_core_a_half(g.nphase, g.band_rows);
     const uint32_t a_bytes = 2 * a_half;
-    const uint32_t b_half = BN * 64;  // [4 planes][BN][8 bf16]
-    const uint32_t b_bytes = 2 * b_half;
+    const uint32_t w_tap = (uint32_t)BN * 128;  // [4 planes][2BN rows][16 B]
+    const uint32_t w_slot = (uint32_t)TG * w_tap;
+    const uint32_t zbuf = F3 ? (uint32_t)bf_core3_zbuf(g) : 0u, zhalf = zbuf / 2;
+    const uint32_t w3_bytes = F3 ? (uint32_t)bf_core3_w3(g) : 0u;
     uint8_t *a_slots = smem;
-    uint8_t *b_slots = smem + 2 * (size_t)a_bytes;
-    float *epi_scratch = reinterpret_cast<float *>(b_slots + (size_t)SB * b_bytes);
-    uint64_t *a_full = reinterpret_cast<uint64_t *>(b_slots + (size_t)SB * b_bytes + kEpiScratch16);
+    uint8_t *w_slots = smem + 2 * (size_t)a_bytes;
+    float *epi_scratch = reinterpret_cast<float *>(w_slots + (size_t)WS * w_slot);
+    uint8_t *zs = reinterpret_cast<uint8_t *>(epi_scratch) + kEpiScratch16;  // F3: 2 Z buffers
+    uint8_t *w3s = zs + 2 * (size_t)zbuf;                                    // F3: U_out panel
+    uint64_t *a_full = reinterpret_cast<uint64_t *>(w3s + w3_bytes);
     uint64_t *a_empty = a_full + 2;
-    uint64_t *b_full = a_empty + 2;
-    uint64_t *b_empty = b_full + SB;
-    uint64_t *tfull = b_empty + SB;
+    uint64_t *tfull = a_empty + 2;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *w_full = tempty + 2;
+    uint64_t *w_empty = w_full + WS;
+    uint64_t *z_full = w_empty + WS;   // F3 only from here on
+    uint64_t *z_empty = z_full + 2;
+    uint64_t *t3full = z_empty + 2;
+    uint64_t *t3empty = t3full + 2;
+    uint64_t *w3_full = t3empty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(F3 ? w3_full + 1 : z_full);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t ncols = 32;
-    while ((int)ncols < BN) ncols *= 2;
+    const int acc_cols = g.ncat ? 2 * BN : BN;
+    const uint32_t ncols = bf_pow2_cols(acc_cols);                      // one acc2 buffer
+    const uint32_t ncols3 = F3 ? bf_pow2_cols(g.ncat3 ? 2 * g.N3p : g.N3p) : 0u;
+    const uint32_t tcols = F3 ? (uint32_t)bf_core3_tmem(g) : 2 * ncols;
     const int mtiles = (g.M + kBM16 - 1) / kBM16;
     const int num_tiles = mtiles * g.ntiles;
-    const __nv_bfloat16 *xg = reinterpret_cast<const __nv_bfloat16 *>(g.xg);
-    const __nv_bfloat16 *xg_lo = reinterpret_cast<const __nv_bfloat16 *>(g.xg_lo);
-    const __nv_bfloat16 *w = reinterpret_cast<const __nv_bfloat16 *>(g.w);
-    const __nv_bfloat16 *w_lo = reinterpret_cast<const __nv_bfloat16 *>(g.w_lo);
+    const bool resident = g.w_resident != 0;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -381,151 +478,315 @@ __global__ void __launch_bounds__(192, 1) tdc_bf_core_kernel(const TcCoreArgs g)
             mbar_init(&a_empty[i], 1);
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 128);
+            if (F3) {
+                mbar_init(&z_full[i], 128);
+                mbar_init(&z_empty[i], 1);
+                mbar_init(&t3full[i], 1);
+                mbar_init(&t3empty[i], 128);
+            }
         }
-        for (int i = 0; i < SB; ++i) {
-            mbar_init(&b_full[i], 1);
-            mbar_init(&b_empty[i], 1);
+        for (int i = 0; i < WS; ++i) {
+            mbar_init(&w_full[i], 1);
+            mbar_init(&w_empty[i], 1);
         }
+        if (F3) mbar_init(w3_full, 1);
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 2 * ncols);
+    if (warp == 1) tmem_alloc(tmem_slot, tcols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     pdl_wait();
     pdl_launch_dependents();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t band_bytes = (uint32_t)g.band_rows * 16;
+
+    // phase-grid row m -> compact output row (b, oy, ox), or invalid
+    auto out_row = [&](int m, long long *dst_row) {
+        if (m >= g.M) return false;
+        const int ox = m % g.Wq;
+        const int tt = m / g.Wq;
+        const int oy = tt % g.Hq;
+        const int b = tt / g.Hq;
+        *dst_row = ((long long)b * g.Ho + oy) * g.Wo + ox;
+        return oy < g.Ho && ox < g.Wo;
+    };
 
     if (warp == 0) {  // ---------------------------------- bulk-copy producer
-        Ring ra(2), rb(SB);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(g.w);
+        // copy `bytes` to smem in <= 16 KB pieces issued from different lanes
+        auto load_split = [&](uint8_t *dst, const uint8_t *src, uint32_t bytes, uint64_t *bar) {
+            if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+            __syncwarp();
+            const uint32_t piece = 16384;
+            for (uint32_t o = (uint32_t)lane * piece; o < bytes; o += 32 * piece)
+                bulk_load(dst + o, src + o, bytes - o < piece ? bytes - o : piece, bar);
+            __syncwarp();
+        };
+        if (F3) load_split(w3s, reinterpret_cast<const uint8_t *>(g.w3), w3_bytes, w3_full);
+        if (resident)  // ntiles == 1: every (kc, group) slice once, for the CTA's lifetime
+            for (int i = 0; i < WS; ++i)
+                load_split(w_slots + (size_t)i * w_slot, wsrc + (size_t)i * w_slot, w_slot, &w_full[i]);
+        Ring ra(2), rw(WS);
+        int tit = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tit) {
             const int m0 = (t % mtiles) * kBM16, nt = t / mtiles;
             for (int kc = 0; kc < g.kchunks; ++kc, ra.next()) {
                 mbar_wait(&a_empty[ra.slot], ra.phase ^ 1);
-                if (elect_one()) {
-                    mbar_arrive_expect_tx(&a_full[ra.slot], a_bytes);
-                    uint8_t *dst = a_slots + (size_t)ra.slot * a_bytes;
-                    for (int ph = 0; ph < g.nphase; ++ph)
-                        for (int kg = 0; kg < 4; ++kg) {
-                            const long long off = ((long long)(kc * 4 + kg) * g.plane_stride +
-                                                   (long long)g.phase_src[ph] * g.phase_rows + m0) * 8;
-                            bulk_load(dst + (size_t)(ph * 4 + kg) * band_bytes, xg + off, band_bytes,
-                                      &a_full[ra.slot]);
-                            bulk_load(dst + a_half + (size_t)(ph * 4 + kg) * band_bytes, xg_lo + off,
-                                      band_bytes, &a_full[ra.slot]);
-                        }
+                if (kc == 0 && lane == 0) BFCTL(tit, 0);  // producer: band issue
+                if (lane == 0) mbar_arrive_expect_tx(&a_full[ra.slot], a_bytes);
+                __syncwarp();
+                uint8_t *dst = a_slots + (size_t)ra.slot * a_bytes;
+                for (int c = lane; c < g.nphase * 8; c += 32) {  // (phase, plane, hi/lo)
+                    const int ph = c >> 3, kg = (c >> 1) & 3, lo = c & 1;
+                    const long long off =
+                        ((long long)(kc * 4 + kg) * g.plane_rows + (long long)g.phase_src[ph] * g.phase_rows + m0) * 8;
+                    bulk_load(dst + lo * a_half + (size_t)(ph * 4 + kg) * band_bytes, (lo ? g.xg_lo : g.xg) + off,
+                              band_bytes, &a_full[ra.slot]);
                 }
                 __syncwarp();
-                for (int tap = 0; tap < g.taps; ++tap, rb.next()) {
-                    mbar_wait(&b_empty[rb.slot], rb.phase ^ 1);
-                    if (elect_one()) {
-                        mbar_arrive_expect_tx(&b_full[rb.slot], b_bytes);
-                        const long long woff =
-                            ((long long)(tap * g.kchunks + kc) * g.ntiles + nt) * BN * 32;
-                        uint8_t *dst = b_slots + (size_t)rb.slot * b_bytes;
-                        bulk_load(dst, w + woff, b_half, &b_full[rb.slot]);
-                        bulk_load(dst + b_half, w_lo + woff, b_half, &b_full[rb.slot]);
+                if (!resident)
+                    for (int grp = 0; grp < g.ngroups; ++grp, rw.next()) {
+                        mbar_wait(&w_empty[rw.slot], rw.phase ^ 1);
+                        if (tit == 0 && lane == 0) BFCTAP(kc * g.ngroups + grp, 0);
+                        const long long slice = ((long long)kc * g.ntiles + nt) * g.ngroups + grp;
+                        load_split(w_slots + (size_t)rw.slot * w_slot, wsrc + slice * w_slot, w_slot,
+                                   &w_full[rw.slot]);
                     }
-                    __syncwarp();
-                }
             }
         }
     } else if (warp == 1) {  // ------------------------------ MMA issuer
-        const uint32_t idesc = idesc_bf16(kBM16, BN);
+        const uint32_t idesc = idesc_bf16(kBM16, acc_cols);
         const uint64_t da = sdesc_kmajor_none(smem_u32(a_slots), band_bytes, 128);
-        const uint64_t db = sdesc_kmajor_none(smem_u32(b_slots), BN * 16, 128);
-        Ring ra(2), rb(SB), acc(2);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next()) {
-            mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
-            tc_fence_after();
-            const uint32_t d = tmem + acc.slot * ncols;
-            bool first = true;
-            for (int kc = 0; kc < g.kchunks; ++kc, ra.next()) {
-                mbar_wait(&a_full[ra.slot], ra.phase);
-                for (int tap = 0; tap < g.taps; ++tap, rb.next()) {
-                    mbar_wait(&b_full[rb.slot], rb.phase);
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint64_t a =
-                            da + ((ra.slot * a_bytes + (uint32_t)g.tap_phase[tap] * 4 * band_bytes +
-                                   (uint32_t)g.tap_off[tap] * 16) >> 4);
-                        const uint64_t b = db + ((rb.slot * b_bytes) >> 4);
-#pragma unroll
-                        for (int j = 0; j < 2; ++j) {  // K = 16 = two 8-channel planes
-                            const uint64_t aj = a + ((j * 2 * band_bytes) >> 4);
-                            const uint64_t bj = b + ((j * 2 * BN * 16) >> 4);
-                            mma_bf16(d, aj, bj, idesc, !(first && j == 0));
-                            mma_bf16(d, aj, bj + (b_half >> 4), idesc, 1);
-                            mma_bf16(d, aj + (a_half >> 4), bj, idesc, 1);
+        const uint64_t db = sdesc_kmajor_none(smem_u32(w_slots), 2 * BN * 16, 128);
+        const uint32_t a_lo = a_half >> 4, b_lo = (BN * 16) >> 4;
+        // stage 3 (F3): A = Z tile planar [plane][128][16 B], B = U_out [plane][2*N3p][16 B]
+        const uint32_t id3 = F3 ? idesc_bf16(kBM16, g.ncat3 ? 2 * g.N3p : g.N3p) : 0u;
+        const uint64_t dz = sdesc_kmajor_none(smem_u32(zs), 128 * 16, 128);
+        const uint64_t dw3 = sdesc_kmajor_none(smem_u32(w3s), 2 * g.N3p * 16, 128);
+        const uint32_t z_lo = zhalf >> 4, b3_lo = (g.N3p * 16) >> 4;
+        const int k3 = BN / 16;
+        Ring ra(2), rw(WS), acc(2), zr(2), a3(2);
+        int tit = 0;
+        bool pending = false;  // F3: S3 of the previous tile still to issue
+        if (F3) mbar_wait(w3_full, 0);
+        for (int t = blockIdx.x;; t += gridDim.x, ++tit) {
+            const bool have = t < num_tiles;
+            if (have) {
+                mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
+                tc_fence_after();
+                if (lane == 0) BFCTL(tit, 1);  // MMA: accumulator free
+                const uint32_t d = tmem + acc.slot * ncols;
+                uint32_t accum = 0;
+                for (int kc = 0; kc < g.kchunks; ++kc, ra.next()) {
+                    mbar_wait(&a_full[ra.slot], ra.phase);
+                    if (kc == 0 && lane == 0) BFCTL(tit, 2);  // MMA: band landed
+                    for (int grp = 0; grp < g.ngroups; ++grp) {
+                        int ws;
+                        if (resident) {
+                            ws = kc * g.ngroups + grp;
+                            mbar_wait(&w_full[ws], 0);
+                        } else {
+                            ws = rw.slot;
+                            mbar_wait(&w_full[ws], rw.phase);
                         }
-                        mma_commit(&b_empty[rb.slot]);
+                        tc_fence_after();
+                        if (tit == 0 && lane == 0) BFCTAP(kc * g.ngroups + grp, 1);
+                        if (elect_one()) {
+                            for (int tt = 0; tt < TG; ++tt) {
+                                const int tap = grp * TG + tt;
+                                const uint64_t a =
+                                    da + ((ra.slot * a_bytes + (uint32_t)g.tap_phase[tap] * 4 * band_bytes +
+                                           (uint32_t)g.tap_off[tap] * 16) >> 4);
+                                const uint64_t b = db + ((ws * w_slot + tt * w_tap) >> 4);
+#pragma unroll
+                                for (int j = 0; j < 2; ++j) {  // K = 16 = two 8-channel planes
+                                    const uint64_t aj = a + ((j * 2 * band_bytes) >> 4);
+                                    const uint64_t bj = b + ((j * 2 * 2 * BN * 16) >> 4);
+                                    if (g.ncat) {  // [hi | lo] along N: hi*hi, hi*lo | lo*hi, lo*lo
+                                        mma_bf16(d, aj, bj, idesc, accum);
+                                        mma_bf16(d, aj + a_lo, bj, idesc, 1);
+                                    } else {
+                                        mma_bf16(d, aj, bj, idesc, accum);
+                                        mma_bf16(d, aj, bj + b_lo, idesc, 1);
+                                        mma_bf16(d, aj + a_lo, bj, idesc, 1);
+                                    }
+                                    accum = 1;
+                                }
+                            }
+                            if (!resident) mma_commit(&w_empty[ws]);
+                        }
+                        __syncwarp();
+                        accum = 1;
+                        if (!resident) rw.next();
                     }
+                    if (elect_one()) mma_commit(&a_empty[ra.slot]);
                     __syncwarp();
-                    first = false;
                 }
-                if (elect_one()) mma_commit(&a_empty[ra.slot]);
+                if (elect_one()) mma_commit(&tfull[acc.slot]);
                 __syncwarp();
+                acc.next();
+                if (lane == 0) BFCTL(tit, 3);  // MMA: all issued
             }
-            if (elect_one()) mma_commit(&tfull[acc.slot]);
-            __syncwarp();
+            if (F3 && pending) {  // ---- stage 3 of the previous tile
+                mbar_wait(&t3empty[a3.slot], a3.phase ^ 1);
+                mbar_wait(&z_full[zr.slot], zr.phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t d3 = tmem + 2 * ncols + a3.slot * ncols3;
+                    const uint64_t az = dz + ((zr.slot * zbuf) >> 4);
+                    for (int j = 0; j < k3; ++j) {
+                        const uint64_t aj = az + ((j * 2 * 128 * 16) >> 4);
+                        const uint64_t bj = dw3 + ((j * 2 * 2 * g.N3p * 16) >> 4);
+                        if (g.ncat3) {
+                            mma_bf16(d3, aj, bj, id3, j > 0);
+                            mma_bf16(d3, aj + z_lo, bj, id3, 1);
+                        } else {
+                            mma_bf16(d3, aj, bj, id3, j > 0);
+                            mma_bf16(d3, aj, bj + b3_lo, id3, 1);
+                            mma_bf16(d3, aj + z_lo, bj, id3, 1);
+                        }
+                    }
+                    mma_commit(&z_empty[zr.slot]);
+                    mma_commit(&t3full[a3.slot]);
+                }
+                __syncwarp();
+                zr.next();
+                a3.next();
+            }
+            if (!have) break;
+            pending = true;
         }
-    } else {  // ------------------------------ epilogue warps 2..5: Z hi/lo bf16
+    } else if (warp < 6) {  // ------------------ epilogue warps 2..5: acc2 -> Z hi/lo bf16
         const int q = warp & 3;
         float *scratch = epi_scratch + q * 1024;
         __nv_bfloat16 *z = reinterpret_cast<__nv_bfloat16 *>(g.z);
         __nv_bfloat16 *z_lo = reinterpret_cast<__nv_bfloat16 *>(g.z_lo);
-        Ring acc(2);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next()) {
+        const int r = q * 32 + lane;  // tile row = TMEM lane
+        Ring acc(2), zr(2);
+        int tit = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next(), zr.next(), ++tit) {
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
             mbar_wait(&tfull[acc.slot], acc.phase);
             tc_fence_after();
-            const int m = m0 + q * 32 + lane;
-            bool valid = m < g.M;
+            if (warp == 2 && lane == 0) BFCTL(tit, 4);  // epilogue: accumulator ready
             long long dst_row = 0;
-            if (valid) {
-                const int ox = m % g.Wq;
-                const int tt = m / g.Wq;
-                const int oy = tt % g.Hq;
-                const int b = tt / g.Hq;
-                valid = oy < g.Ho && ox < g.Wo;
-                dst_row = ((long long)b * g.Ho + oy) * g.Wo + ox;
-            }
+            const bool valid = out_row(m0 + r, &dst_row);
+            if (F3) mbar_wait(&z_empty[zr.slot], zr.phase ^ 1);
             const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
+            const uint32_t zb = smem_u32(zs) + zr.slot * zbuf;
             for (int c = 0; c < BN; c += 32) {
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(src + c, r);
-                tmem_ld_wait();
-                if (n0 + c >= g.Nn) continue;  // warp-uniform
+                uint32_t rr[32];
                 float v[32];
+                tmem_ld_32x32b_x32(src + c, rr);
+                if (g.ncat) {
+                    uint32_t r2[32];
+                    tmem_ld_32x32b_x32(src + BN + c, r2);
+                    tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                uint32_t hw[16], lw[16];
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]) + __uint_as_float(r2[j]);
+                } else {
+                    tmem_ld_wait();
 #pragma unroll
-                for (int pl = 0; pl < 4; ++pl) {
-                    uint4 h, l;
-                    split_bf16x8(v + 8 * pl, h, l);
-                    hw[4 * pl] = h.x; hw[4 * pl + 1] = h.y; hw[4 * pl + 2] = h.z; hw[4 * pl + 3] = h.w;
-                    lw[4 * pl] = l.x; lw[4 * pl + 1] = l.y; lw[4 * pl + 2] = l.z; lw[4 * pl + 3] = l.w;
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
                 }
-                const long long off = dst_row * g.ldz + n0 + c;
-                warp_store_block32_b16(scratch, hw, valid ? (void *)(z + off) : nullptr, lane);
-                warp_store_block32_b16(scratch, lw, valid ? (void *)(z_lo + off) : nullptr, lane);
+                if (F3) {  // Z hi/lo planes [c/8 + pl][row r][16 B] (conflict-free: lanes = rows)
+#pragma unroll
+                    for (int pl = 0; pl < 4; ++pl) {
+                        uint4 h, l;
+                        split_bf16x8(v + 8 * pl, h, l);
+                        const uint32_t o = ((uint32_t)(c / 8 + pl) * 128 + r) * 16;
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(zb + o), "r"(h.x), "r"(h.y),
+                                     "r"(h.z), "r"(h.w)
+                                     : "memory");
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(zb + zhalf + o), "r"(l.x),
+                                     "r"(l.y), "r"(l.z), "r"(l.w)
+                                     : "memory");
+                    }
+                } else {
+                    if (n0 + c >= g.Nn) continue;  // warp-uniform
+                    uint32_t hw[16], lw[16];
+#pragma unroll
+                    for (int pl = 0; pl < 4; ++pl) {
+                        uint4 h, l;
+                        split_bf16x8(v + 8 * pl, h, l);
+                        hw[4 * pl] = h.x; hw[4 * pl + 1] = h.y; hw[4 * pl + 2] = h.z; hw[4 * pl + 3] = h.w;
+                        lw[4 * pl] = l.x; lw[4 * pl + 1] = l.y; lw[4 * pl + 2] = l.z; lw[4 * pl + 3] = l.w;
+                    }
+                    const long long off = dst_row * g.ldz + n0 + c;
+                    warp_store_block32_b16(scratch, hw, valid ? (void *)(z + off) : nullptr, lane);
+                    warp_store_block32_b16(scratch, lw, valid ? (void *)(z_lo + off) : nullptr, lane);
+                }
             }
             tc_fence_before();
             mbar_arrive_relaxed(&tempty[acc.slot]);
+            if (F3) {
+                fence_proxy_async_smem();  // Z (generic writes) -> visible to the MMA (async proxy)
+                mbar_arrive(&z_full[zr.slot]);
+            }
+            if (warp == 2 && lane == 0) BFCTL(tit, 5);  // epilogue: done
+        }
+    } else if (F3) {  // ------------------------- epilogue warps 6..9: acc3 (+bias) -> Y
+        const int q = warp & 3;
+        float *scratch = epi_scratch + q * 1024;
+        Ring a3(2);
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, a3.next()) {
+            const int m0 = (t % mtiles) * kBM16;
+            mbar_wait(&t3full[a3.slot], a3.phase);
+            tc_fence_after();
+            long long dst_row = 0;
+            const bool valid = out_row(m0 + q * 32 + lane, &dst_row);
+            const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + 2 * ncols + a3.slot * ncols3;
+            float *dst = g.y + dst_row * g.N3;
+            for (int c = 0; c < g.N3p; c += 32) {
+                uint32_t rr[32];
+                float v[32];
+                tmem_ld_32x32b_x32(src + c, rr);
+                if (g.ncat3) {
+                    uint32_t r2[32];
+                    tmem_ld_32x32b_x32(src + g.N3p + c, r2);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]) + __uint_as_float(r2[j]);
+                } else {
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
+                }
+                if (c >= g.N3) continue;  // warp-uniform
+                if (g.bias) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (c + j < g.N3) v[j] += __ldg(&g.bias[c + j]);
+                }
+                if (c + 32 <= g.N3 && (g.N3 & 3) == 0) {
+                    warp_store_block32(scratch, v, valid ? dst + c : nullptr, lane);
+                } else if (valid) {
+                    for (int j = 0; j < 32 && c + j < g.N3; ++j) dst[c + j] = v[j];
+                }
+            }
+            tc_fence_before();
+            mbar_arrive_relaxed(&t3empty[a3.slot]);
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, 2 * ncols);
+    if (warp == 1) tmem_dealloc(tmem, tcols);
 }
 
-cudaError_t bf_core_launch(const TcCoreArgs &g, int grid, cudaStream_t st) {
-    const int smem = bf_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.b_stages);
-    cudaError_t e = cudaFuncSetAttribute(tdc_bf_core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+cudaError_t bf_core_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
+    const int smem = bf_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.tg, g.w_slots);
+    cudaError_t e =
+        cudaFuncSetAttribute(tdc_bf_core_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(tdc_bf_core_kernel, grid, 192, smem, st, g);
+    return launch_pdl(tdc_bf_core_kernel<false>, grid, 192, smem, st, g);
+}
+
+cudaError_t bf_core3_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
+    const int smem = bf_core3_smem_bytes(g);
+    cudaError_t e =
+        cudaFuncSetAttribute(tdc_bf_core_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(tdc_bf_core_kernel<true>, grid, 320, smem, st, g);
 }
 
 }  // namespace tdc

@@ -19,9 +19,31 @@ tdc.lib.tdc_debug_bf_timeline(buf, n)
 a = np.array(buf, dtype=np.int64).reshape(4, 64, 8)
 for seq in (2, 3):
     t = a[seq]
+    if not (t[:, 1] > 0).any():
+        continue
     rows = t[t[:, 1] > 0]
     t0 = rows[rows > 0].min()
     print(f"--- launch seq {seq} ({'stage 1' if seq % 2 == 0 else 'stage 3'}): tiles {len(rows)}")
     print("tile prod mma_free mma_opnd mma_iss epi_acc epi_done cv_land cv_done")
     for i, r in enumerate(rows[:8]):
         print(i, " ".join(f"{(v - t0) / 1000:7.2f}" if v else "    -  " for v in r))
+n2 = 64 * 8
+buf2 = (ctypes.c_ulonglong * n2)()
+tdc.lib.tdc_debug_bfc_timeline(buf2, n2)
+c = np.array(buf2, dtype=np.int64).reshape(64, 8)
+rows = c[c[:, 1] > 0]
+if len(rows):
+    t0 = rows[rows > 0].min()
+    print(f"--- core kernel (last launch), CTA 0: tiles {len(rows)}")
+    print("tile band_iss mma_free band_land mma_iss epi_acc epi_done")
+    for i, r in enumerate(rows[:12]):
+        print(i, " ".join(f"{(v - t0) / 1000:7.2f}" if v else "    -  " for v in r[:6]))
+buf3 = (ctypes.c_ulonglong * 256)()
+tdc.lib.tdc_debug_bfc_taps(buf3, 256)
+tp = np.array(buf3, dtype=np.int64).reshape(128, 2)
+tp = tp[tp[:, 0] > 0]
+if len(tp):
+    t0 = tp.min()
+    print("--- core kernel CTA 0 tile 0 per (kc, tap): producer-issue  mma-ready (us)")
+    for i, r in enumerate(tp[:80]):
+        print(i, " ".join(f"{(v - t0) / 1000:7.2f}" for v in r))

@@ -79,6 +79,136 @@ __global__ void bench(int iters, long long *out) {
     if (warp == 0) tmem_dealloc(tmem, COLS);
 }
 
+// Layout / commit study (bf16, M = 128, SS): LAYOUT 0 = 128B swizzle, 1 = no swizzle
+// (core-matrix interleave as the core kernel: A LBO = band plane stride, B LBO = N*16);
+// CE = commit to an mbarrier every CE MMAs (0 = only at the end).
+template <int N, int LAYOUT, int CE>
+__global__ void bench_lc(int iters, long long *out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar, cbar[4];
+    __shared__ uint32_t slot;
+    for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x)
+        reinterpret_cast<float *>(smem)[i] = 0.001f * (i % 7);
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        for (int i = 0; i < 4; ++i) mbar_init(&cbar[i], 1);
+        fence_mbar_init();
+    }
+    fence_proxy_async_smem();
+    if (warp == 0) tmem_alloc(&slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    if (threadIdx.x == 0) {
+        uint64_t ad, bd;
+        if (LAYOUT == 0) {
+            ad = sdesc_kmajor_sw128(smem_u32(smem));
+            bd = sdesc_kmajor_sw128(smem_u32(smem + 32768));
+        } else {
+            ad = sdesc_kmajor_none(smem_u32(smem), 3968, 128);
+            bd = sdesc_kmajor_none(smem_u32(smem + 32768), N * 16, 128);
+        }
+        const uint32_t id = idesc_bf16(128, N);
+        long long t0 = clock64();
+        for (int i = 0; i < iters; i += 6) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) mma_bf16(tmem, ad + (k & 1) * 2, bd + (k % 3) * 2, id, 1);
+            if (CE) mma_commit(&cbar[(i / 6) & 3]);
+        }
+        mma_commit(&bar);
+        mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        out[blockIdx.x] = t1 - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int N, int LAYOUT, int CE>
+void run_lc(long long *d) {
+    auto k = bench_lc<N, LAYOUT, CE>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+    const int iters = 6 * 682, grid = 148;
+    k<<<grid, 128, 66 * 1024>>>(iters, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h[512];
+    cudaMemcpy(h, d, 8 * grid, cudaMemcpyDeviceToHost);
+    double mx = 0;
+    for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
+    printf("bf16 M=128 N=%3d %s commit/%d: %7.1f cyc/mma %s\n", N, LAYOUT ? "no-swizzle" : "sw128     ", CE ? 6 : 0,
+           mx / iters, e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
+// A start-address offset study (bf16, M = 128, SS, no commits): LAYOUT 1 = no swizzle
+// with A start shifted by OFF bytes (row shifts of 16 B as the core kernel's taps);
+// LAYOUT 0 = 128B swizzle with A shifted by OFF bytes (multiples of 128 = whole rows)
+// and the descriptor base-offset field set to (addr >> 7) & 7.
+template <int N, int LAYOUT>
+__global__ void bench_off(int iters, int off, long long *out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t slot;
+    for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x)
+        reinterpret_cast<float *>(smem)[i] = 0.001f * (i % 7);
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    fence_proxy_async_smem();
+    if (warp == 0) tmem_alloc(&slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    if (threadIdx.x == 0) {
+        uint64_t ad, bd;
+        const uint32_t a_addr = smem_u32(smem) + off;
+        if (LAYOUT == 0) {
+            ad = sdesc_kmajor_sw128(a_addr) | ((uint64_t)((a_addr >> 7) & 7) << 49);
+            bd = sdesc_kmajor_sw128(smem_u32(smem + 40960));
+        } else {
+            ad = sdesc_kmajor_none(a_addr, 3968, 128);
+            bd = sdesc_kmajor_none(smem_u32(smem + 40960), N * 16, 128);
+        }
+        const uint32_t id = idesc_bf16(128, N);
+        long long t0 = clock64();
+        for (int i = 0; i < iters; i += 4) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mma_bf16(tmem, ad + (k & 1) * 2, bd + (k & 1) * 2, id, 1);
+        }
+        mma_commit(&bar);
+        mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        out[blockIdx.x] = t1 - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int N, int LAYOUT>
+void run_off(long long *d, int off) {
+    auto k = bench_off<N, LAYOUT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+    const int iters = 4096, grid = 148;
+    k<<<grid, 128, 66 * 1024>>>(iters, off, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h[512];
+    cudaMemcpy(h, d, 8 * grid, cudaMemcpyDeviceToHost);
+    double mx = 0;
+    for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
+    printf("bf16 M=128 N=%3d %s A offset %4d B: %7.1f cyc/mma %s\n", N, LAYOUT ? "no-swizzle" : "sw128+base", off,
+           mx / iters, e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
 template <int BF, int M, int N, int TS, int ELECT>
 void run(long long *d, int ctas_per_sm) {
     auto k = ctas_per_sm == 1 ? bench<BF, M, N, TS, ELECT, 512> : bench<BF, M, N, TS, ELECT, 256>;
@@ -105,6 +235,15 @@ int main() {
     cudaMalloc(&d, 8 * 512);
 #define ALLN(BF, M, TS, E) run<BF, M, 32, TS, E>(d, 1); run<BF, M, 64, TS, E>(d, 1); \
     run<BF, M, 128, TS, E>(d, 1); run<BF, M, 256, TS, E>(d, 1);
+    for (int off : {0, 16, 32, 48, 64, 112}) run_off<32, 1>(d, off);
+    for (int off : {0, 16, 32, 64}) run_off<64, 1>(d, off);
+    for (int off : {0, 16, 64}) run_off<128, 1>(d, off);
+    for (int off : {0, 128, 256, 384, 640}) run_off<32, 0>(d, off);
+    for (int off : {0, 128, 384}) run_off<64, 0>(d, off);
+    for (int off : {0, 128}) run_off<128, 0>(d, off);
+    run_lc<32, 0, 0>(d); run_lc<32, 0, 1>(d); run_lc<32, 1, 0>(d); run_lc<32, 1, 1>(d);
+    run_lc<64, 0, 0>(d); run_lc<64, 0, 1>(d); run_lc<64, 1, 0>(d); run_lc<64, 1, 1>(d);
+    run_lc<128, 0, 0>(d); run_lc<128, 1, 0>(d); run_lc<128, 1, 1>(d);
     ALLN(1, 128, 0, 0)
     ALLN(1, 128, 0, 1)
     ALLN(1, 128, 1, 0)

@@ -189,3 +189,33 @@ def test_forward_rejects_bad_calls(env):
     with pytest.raises(tdc.TdcError):
         tdc.tdc_conv_forward(plan._h, x.data_ptr(), y.data_ptr(), 2)  # batch > plan
     plan.close()
+
+
+@pytest.mark.parametrize("fuse3", [True, False], ids=["core3", "three_launch"])
+@pytest.mark.parametrize("shape", [s for s, _ in synth.R18_SHAPES] + [
+    LayerShape(3, 64, 40, 13, 11, 24, 20, 3, 1, 1),
+    LayerShape(2, 32, 48, 15, 9, 16, 32, 3, 2, 1),
+    LayerShape(2, 40, 72, 12, 10, 40, 48, 5, 1, 2),
+], ids=lambda s: s.name or f"{s.C}_{s.N}_{s.H}x{s.W}_k{s.K}_s{s.stride}")
+def test_3xbf16_core3_and_three_launch(env, shape, fuse3, monkeypatch):
+    """3xBF16 with stage 3 fused into the core kernel (Z on chip) where it fits,
+    and the three-launch path forced with TDC_NO_FUSE3, against the oracle."""
+    if not fuse3:
+        monkeypatch.setenv("TDC_NO_FUSE3", "1")
+    s = shape.with_batch(2)
+    d = synth.make_layer(s, seed=21, bias=True)
+    got, info = run_layer(env, s, d, "nhwc", "3xbf16")
+    if not fuse3:
+        assert info.variant_name == "tc3_3xbf16_band"
+    assert err(got, ref_of(s, d)) <= TOL["3xbf16"]
+
+
+@pytest.mark.parametrize("shape,count", synth.R18_SHAPES, ids=[s.name for s, _ in synth.R18_SHAPES])
+def test_3xbf16_variant_names(env, shape, count):
+    torch, tdc = env
+    d = synth.make_layer(shape)
+    plan = tdc.ConvPlan(shape.with_batch(32), d, math=tdc.TDC_MATH_3XBF16)
+    info = plan.info()
+    assert info.variant_name in ("tc2_3xbf16_core3", "tc3_3xbf16_band")
+    assert info.launches_per_forward == (2 if info.variant_name == "tc2_3xbf16_core3" else 3)
+    plan.close()
