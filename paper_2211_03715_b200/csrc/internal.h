@@ -55,6 +55,8 @@ struct TcGemmArgs {
     int ntiles;       // N tiles (persistent kernel walks mtiles x ntiles)
     int out_bf16;     // 3xBF16 stage 1: out/out_lo are bf16 planar [c/8][row][8], planar_stride in rows
     int xstages;      // 3xBF16 stage 1: depth of the fp32 staging ring (separate from `stages`)
+    int ksplit;       // 3xBF16: >1 = split K over a cluster of ksplit CTAs, DSMEM reduction
+    int bstages;      // 3xBF16 stage 1: depth of the weight (B) ring
 };
 
 // Stage-2 core convolution with a shared-memory-resident X' band (tkd_tc.cu):
@@ -114,8 +116,8 @@ bool fused_make_x_map(CUtensorMap *map, const float *x, const FusedArgs &g);
 cudaError_t fused_launch(const CUtensorMap &mapX, const FusedArgs &g, int grid, cudaStream_t st);
 
 // ---- 3xBF16 variant of the 3-launch path (tkd_bf16.cu) ----
-int bf_smem_bytes(int BN, int stages, int xstages);
-int bf_pick_stages(int BN, int max_smem, int convert, int *xstages);
+int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages);
+int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, int *bstages);
 cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, const CUtensorMap &mapB,
                            const CUtensorMap &mapBlo, const TcGemmArgs &g, int grid, cudaStream_t st);
 // 3xBF16 stage-2 core convolution (tkd_bf16.cu).  X' hi/lo planar bf16
@@ -171,6 +173,33 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, int smem, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+// Same, with a thread-block cluster of `cluster` CTAs along x (grid a multiple of it).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), int grid, int block, int smem, cudaStream_t st,
+                               int cluster, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (cluster > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = (unsigned)cluster;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    if (pdl_enabled()) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -401,8 +401,41 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         while (b > 64 && div_up((int)mrows, 128) * (long long)div_up(nn, b) < 2 * p->num_sms) b /= 2;
         return b;
     };
-    const int BN1 = pick(D1s, M1), BN3 = pick(N, M3);
+    int BN1 = pick(D1s, M1), BN3 = pick(N, M3);
     int BN2 = pick(D2s, M2);
+    // Split K over a thread-block cluster (DSMEM reduction, deterministic order) when the
+    // output tiles alone leave SMs idle: pick (BN, cluster size) maximising busy SMs,
+    // larger BN on ties.  Opt-in (TDC_SPLITK=1): on the R18 shapes the per-tile
+    // cluster handshake costs more than the shorter K loop saves.
+    int ks1 = 1, ks3 = 1;
+    {
+        const char *ev = std::getenv("TDC_SPLITK");
+        const bool off = !(ev && ev[0] && ev[0] != '0');
+        auto split_pick = [&](long long mrows, int nn, int bn_max, int iters, int *bn) {
+            const long long tiles0 = (long long)div_up((int)mrows, 128) * div_up(nn, *bn);
+            if (off || tiles0 >= p->num_sms) return 1;
+            int best_bn = *bn, best_cs = 1;
+            long long best_u = tiles0;
+            int b = 32;
+            while (b < nn && b < bn_max) b *= 2;
+            for (; b >= 32; b /= 2) {
+                const long long tiles = (long long)div_up((int)mrows, 128) * div_up(nn, b);
+                int cs = 1;
+                for (int c = 2; c <= 8 && c <= iters; ++c)
+                    if (tiles * c <= p->num_sms) cs = c;
+                const long long u = std::min<long long>(tiles * cs, p->num_sms);
+                if (u > best_u) {
+                    best_u = u;
+                    best_bn = b;
+                    best_cs = cs;
+                }
+            }
+            *bn = best_bn;
+            return best_cs;
+        };
+        ks1 = split_pick(M1, D1s, 64, C64 / 64, &BN1);
+        ks3 = split_pick(M3, N, 128, D2p / 64, &BN3);
+    }
     const int KK = K * K;
     const int maxoff = ((K - 1) / s) * Wq + (K - 1) / s;
     const int band_rows = round_up(128 + maxoff, 8);
@@ -575,7 +608,8 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         st.args.BN = BN1; st.args.remap = 1; st.args.a_convert = 1; st.args.out_bf16 = 1;
         st.args.out = reinterpret_cast<float *>(xg); st.args.out_lo = reinterpret_cast<float *>(xg_lo);
         st.args.planar_stride = rows_total;  // rows
-        st.args.stages = tdc::bf_pick_stages(BN1, p->max_smem, 1, &st.args.xstages);
+        st.args.ksplit = ks1;
+        st.args.stages = tdc::bf_pick_stages(BN1, p->max_smem, 1, &st.args.xstages, ks1, &st.args.bstages);
         st.grid_n = R1 / BN1;
         st.args.ntiles = st.grid_n;
         if (!tdc::make_tma_2d_bf16(&st.mapB, dB1, R1, C64, C64, BN1) ||
@@ -614,7 +648,8 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         base_args(st.args);
         st.args.M = (int)M3; st.args.Nn = N; st.args.kchunks = D2p / 64; st.args.taps = 1;
         st.args.BN = BN3; st.args.ldo = N; st.args.remap = 0; st.args.bias = dbias;
-        st.args.stages = tdc::bf_pick_stages(BN3, p->max_smem, 0, nullptr);
+        st.args.ksplit = ks3;
+        st.args.stages = tdc::bf_pick_stages(BN3, p->max_smem, 0, nullptr, ks3, nullptr);
         st.grid_n = R3 / BN3;
         st.args.ntiles = st.grid_n;
         if (!tdc::make_tma_2d_bf16(&st.mapA, z, M3, D2p, D2p, 128) ||
@@ -650,9 +685,16 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
         const long long cap = (long long)p->num_sms * tdc::persistent_occupancy(smem, bn);
         return (int)std::max<long long>(1, std::min(tiles, cap));
     };
+    // split-K launches: clusters of ksplit CTAs, one cluster per output tile (persistent)
+    auto grid_ks = [&](long long M, int ntiles, int smem, int bn, int ks) {
+        if (ks <= 1) return grid(M, ntiles, smem, bn);
+        const long long tiles = (long long)div_up((int)M, 128) * ntiles;
+        const long long cap = (long long)p->num_sms * tdc::persistent_occupancy(smem, bn) / ks;
+        return (int)(std::max<long long>(1, std::min(tiles, cap)) * ks);
+    };
     cudaError_t e = tdc::bf_gemm_launch(
         s1.mapA, s1.mapA, s1.mapB, s1.mapBlo, a1,
-        grid(a1.M, a1.ntiles, tdc::bf_smem_bytes(a1.BN, a1.stages, a1.xstages), a1.BN), st);
+        grid_ks(a1.M, a1.ntiles, tdc::bf_smem_bytes(a1.BN, a1.stages, a1.xstages, a1.ksplit, a1.bstages), a1.BN, a1.ksplit), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-1 launch");
     if (p->fuse3) {
         c.y = y;
@@ -665,8 +707,9 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
         c, grid(c.M, c.ntiles, tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots),
                 c.ncat ? 2 * c.BN : c.BN), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-2 launch");
-    e = tdc::bf_gemm_launch(s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, a3,
-                            grid(a3.M, a3.ntiles, tdc::bf_smem_bytes(a3.BN, a3.stages, 0), a3.BN), st);
+    e = tdc::bf_gemm_launch(
+        s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, a3,
+        grid_ks(a3.M, a3.ntiles, tdc::bf_smem_bytes(a3.BN, a3.stages, 0, a3.ksplit, 0), a3.BN, a3.ksplit), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-3 launch");
     return TDC_OK;
 }

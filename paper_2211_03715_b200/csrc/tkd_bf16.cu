@@ -68,7 +68,31 @@ extern "C" int tdc_debug_bfc_taps(unsigned long long *host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_tdc_bfc_tap, sizeof(unsigned long long) * n);
 }
 #define BFCTAP(i, ev) bfctap((i), (ev))
+// per-CTA [start, after-prologue, end] stamps of the last core launch
+__device__ unsigned long long g_tdc_bfc_span[1024 * 4];
+__device__ __forceinline__ void bfcspan(int ev) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_tdc_bfc_span[blockIdx.x * 4 + ev] = t;
+}
+extern "C" int tdc_debug_bfc_span(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_tdc_bfc_span, sizeof(unsigned long long) * n);
+}
+#define BFCSPAN(ev) bfcspan(ev)
+// per-CTA [start, after-prologue, end] of the gemm launches: [launch seq % 4][cta][4]
+__device__ unsigned long long g_tdc_bfg_span[4 * 1024 * 4];
+__device__ __forceinline__ void bfgspan(int seq, int ev) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_tdc_bfg_span[((seq & 3) * 1024 + blockIdx.x) * 4 + ev] = t;
+}
+extern "C" int tdc_debug_bfg_span(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_tdc_bfg_span, sizeof(unsigned long long) * n);
+}
+#define BFGSPAN(seq, ev) bfgspan((seq), (ev))
 #else
+#define BFGSPAN(seq, ev) ((void)0)
+#define BFCSPAN(ev) ((void)0)
 #define BFCTAP(i, ev) ((void)0)
 #define BFTL(seq, it, ev) ((void)0)
 #define BFCTL(it, ev) ((void)0)
@@ -127,21 +151,35 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = g.stages, BN = g.BN;
     const int SX = CONVERT ? g.xstages : 0;  // fp32 staging ring depth (stage 1)
+    const int SB = CONVERT ? g.bstages : 0;  // stage 1: separate weight ring depth
     const uint32_t b_tile = (uint32_t)BN * kBK16 * 2;
-    const uint32_t half = kATile16 + b_tile;                  // hi -> lo offset
-    const uint32_t slot_bytes = 2 * half;                     // A hi | B hi | A lo | B lo
-    // [SX fp32 staging slots][S operand slots][epilogue scratch][barriers]
+    // non-CONVERT slot: A hi | B hi | A lo | B lo (one TMA ring);
+    // CONVERT: A slots (A hi | A lo, written by the converter) + a separate B ring
+    // (B hi | B lo) that the producer fills ahead of the conversion.
+    const uint32_t half = CONVERT ? kATile16 : kATile16 + b_tile;   // A hi -> A lo
+    const uint32_t slot_bytes = CONVERT ? 2 * kATile16 : 2 * half;
+    const uint32_t bslot = 2 * b_tile;
+    // [SX fp32 staging slots][S operand slots][SB B slots][epilogue scratch][red][barriers]
     uint8_t *xstage = smem;
     uint8_t *ops = smem + (size_t)SX * kStage32;
-    float *epi_scratch = reinterpret_cast<float *>(ops + (size_t)S * slot_bytes);
-    uint64_t *full = reinterpret_cast<uint64_t *>(ops + (size_t)S * slot_bytes + kEpiScratch16);
+    uint8_t *bring = ops + (size_t)S * slot_bytes;
+    float *epi_scratch = reinterpret_cast<float *>(bring + (size_t)SB * bslot);
+    // split-K (cluster of CS CTAs over K): fp32 partial tile [128][BN], float4-swizzled
+    const int CS = g.ksplit > 1 ? g.ksplit : 1;
+    float *red = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(epi_scratch) + kEpiScratch16);
+    uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(red) +
+                                                  (CS > 1 ? (size_t)128 * BN * 4 : 0));
     uint64_t *conv = full + S;       // CONVERT: A hi/lo written by the converter
     uint64_t *empty = conv + S;      // operand slot consumed by the MMAs
     uint64_t *tfull = empty + S;
     uint64_t *tempty = tfull + 2;
     uint64_t *xfull = tempty + 2;    // CONVERT: fp32 X landed in a staging slot
     uint64_t *xempty = xfull + SX;   // CONVERT: staging slot converted
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xempty + SX);
+    uint64_t *bfull = xempty + SX;      // CONVERT: B ring
+    uint64_t *bempty = bfull + SB;
+    uint64_t *red_ready = bempty + SB;  // split-K: all CS partials of the tile written
+    uint64_t *red_free = red_ready + 1; // split-K: all CS readers done with this CTA's partial
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(red_free + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t ncols = 32;
@@ -149,6 +187,9 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     const int mtiles = (g.M + kBM16 - 1) / kBM16;
     const int num_tiles = mtiles * g.ntiles;
     const int iters = g.taps * g.kchunks;
+    const int crank = CS > 1 ? (int)cluster_ctarank() : 0;
+    const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;  // cluster id / count
+    const int i0 = crank * iters / CS, i1 = (crank + 1) * iters / CS;  // this CTA's K range
 #ifdef TDC_TIMELINE
     const int seq = (int)*(volatile unsigned int *)&g_tdc_bf_seq;
 #endif
@@ -167,39 +208,57 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             mbar_init(&xfull[i], 1);
             mbar_init(&xempty[i], kConvThreads16);
         }
+        for (int i = 0; i < SB; ++i) {
+            mbar_init(&bfull[i], 1);
+            mbar_init(&bempty[i], 1);
+        }
+        mbar_init(red_ready, CS * 128);
+        mbar_init(red_free, CS * 128);
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch(&mapA);
         tma_prefetch(&mapB);
     }
+    if (threadIdx.x == 0) BFGSPAN(seq, 0);
     if (warp == 1) tmem_alloc(tmem_slot, 2 * ncols);
     tc_fence_before();
     __syncthreads();
+    if (CS > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
     tc_fence_after();
     pdl_wait();
     pdl_launch_dependents();
+    if (threadIdx.x == 0) BFGSPAN(seq, 1);
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {  // ------------------------------------- TMA producer
-        Ring r(CONVERT ? SX : S);
+        Ring r(CONVERT ? SX : S), rb(CONVERT ? SB : 1);
         int tit = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tit) {
+        for (int t = cid; t < num_tiles; t += ncl, ++tit) {
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
-            int tap = 0, kc = 0;
-            for (int i = 0; i < iters; ++i, r.next()) {
+            int tap = i0 / g.kchunks, kc = i0 % g.kchunks;
+            for (int i = i0; i < i1; ++i, r.next()) {
                 if (CONVERT) {  // fp32 X: channels [64kc, 64kc+32) and [64kc+32, 64kc+64)
                     mbar_wait(&xempty[r.slot], r.phase ^ 1);
-                    if (i == 0 && lane == 0) BFTL(seq, tit, 0);  // producer issues tile
+                    if (i == i0 && lane == 0) BFTL(seq, tit, 0);  // producer issues tile
                     if (elect_one()) {
                         uint8_t *dst = xstage + (size_t)r.slot * kStage32;
                         mbar_arrive_expect_tx(&xfull[r.slot], kStage32);
                         tma_load_2d(dst, &mapA, &xfull[r.slot], kc * 64, m0 + g.a_off[tap]);
                         tma_load_2d(dst + kStage32 / 2, &mapA, &xfull[r.slot], kc * 64 + 32, m0 + g.a_off[tap]);
                     }
+                    __syncwarp();
+                    mbar_wait(&bempty[rb.slot], rb.phase ^ 1);
+                    if (elect_one()) {
+                        uint8_t *bs = bring + (size_t)rb.slot * bslot;
+                        mbar_arrive_expect_tx(&bfull[rb.slot], bslot);
+                        tma_load_2d(bs, &mapB, &bfull[rb.slot], kc * kBK16, g.b_off[tap] + n0);
+                        tma_load_2d(bs + b_tile, &mapBlo, &bfull[rb.slot], kc * kBK16, g.b_off[tap] + n0);
+                    }
+                    rb.next();
                 } else {
                     mbar_wait(&empty[r.slot], r.phase ^ 1);
-                    if (i == 0 && lane == 0) BFTL(seq, tit, 0);
+                    if (i == i0 && lane == 0) BFTL(seq, tit, 0);
                     if (elect_one()) {
                         uint8_t *base = ops + (size_t)r.slot * slot_bytes;
                         mbar_arrive_expect_tx(&full[r.slot], 2 * kATile16 + 2 * b_tile);
@@ -220,32 +279,38 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     } else if (warp == 1) {  // ------------------------------ MMA issuer
         const uint32_t idesc = idesc_bf16(kBM16, BN);
         const uint64_t da = sdesc_kmajor_sw128(smem_u32(ops));
-        const uint64_t db = sdesc_kmajor_sw128(smem_u32(ops + kATile16));
-        const uint32_t lo = half >> 4;
-        Ring r(S), acc(2);
+        const uint64_t db = sdesc_kmajor_sw128(smem_u32(CONVERT ? bring : ops + kATile16));
+        const uint32_t lo = half >> 4, blo = (CONVERT ? b_tile : half) >> 4;
+        Ring r(S), acc(2), rb(CONVERT ? SB : 1);
         int tit = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next(), ++tit) {
+        for (int t = cid; t < num_tiles; t += ncl, acc.next(), ++tit) {
             mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
             tc_fence_after();
             if (lane == 0) BFTL(seq, tit, 1);  // MMA: accumulator free
             const uint32_t d = tmem + acc.slot * ncols;
-            for (int i = 0; i < iters; ++i, r.next()) {
-                if (CONVERT) mbar_wait(&conv[r.slot], r.phase);
-                mbar_wait(&full[r.slot], r.phase);
+            for (int i = i0; i < i1; ++i, r.next()) {
+                if (CONVERT) {
+                    mbar_wait(&conv[r.slot], r.phase);
+                    mbar_wait(&bfull[rb.slot], rb.phase);
+                } else {
+                    mbar_wait(&full[r.slot], r.phase);
+                }
                 tc_fence_after();
-                if (i == 0 && lane == 0) BFTL(seq, tit, 2);  // MMA: operands ready
+                if (i == i0 && lane == 0) BFTL(seq, tit, 2);  // MMA: operands ready
                 if (elect_one()) {
                     const uint64_t a = da + ((r.slot * slot_bytes) >> 4);
-                    const uint64_t b = db + ((r.slot * slot_bytes) >> 4);
+                    const uint64_t b = db + (((CONVERT ? rb.slot * bslot : r.slot * slot_bytes)) >> 4);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {  // K = 16 bf16 = 32 B per MMA
-                        mma_bf16(d, a + j * 2, b + j * 2, idesc, (i | j) != 0);
-                        mma_bf16(d, a + j * 2, b + lo + j * 2, idesc, 1);  // hi * lo
-                        mma_bf16(d, a + lo + j * 2, b + j * 2, idesc, 1);  // lo * hi
+                        mma_bf16(d, a + j * 2, b + j * 2, idesc, (i != i0) || (j != 0));
+                        mma_bf16(d, a + j * 2, b + blo + j * 2, idesc, 1);  // hi * lo
+                        mma_bf16(d, a + lo + j * 2, b + j * 2, idesc, 1);   // lo * hi
                     }
                     mma_commit(&empty[r.slot]);
+                    if (CONVERT) mma_commit(&bempty[rb.slot]);
                 }
                 __syncwarp();
+                if (CONVERT) rb.next();
             }
             if (elect_one()) mma_commit(&tfull[acc.slot]);
             __syncwarp();
@@ -256,14 +321,78 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         float *scratch = epi_scratch + q * 1024;
         Ring acc(2);
         int tit = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next(), ++tit) {
+        for (int t = cid; t < num_tiles; t += ncl, acc.next(), ++tit) {
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
             mbar_wait(&tfull[acc.slot], acc.phase);
             tc_fence_after();
             if (warp == 2 && lane == 0) BFTL(seq, tit, 4);  // epilogue: accumulator ready
+            const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
+            if (CS > 1) {  // ---- split-K: partial -> own smem, reduce a row slice over the cluster
+                const int row = q * 32 + lane, tid = row;
+                const uint32_t red_a = smem_u32(red);
+                const uint32_t tpar = (uint32_t)(tit & 1);
+                mbar_wait_cluster(red_free, tpar ^ 1);  // peers done reading the previous partial
+                for (int c = 0; c < BN; c += 32) {
+                    uint32_t rr[32];
+                    tmem_ld_32x32b_x32(src + c, rr);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {  // float4 column j4 of row, swizzled by row % 8
+                        const int j4 = c / 4 + j;
+                        st_shared_v4(red_a + (uint32_t)(row * BN + 4 * (j4 ^ (row & 7))) * 4,
+                                     __uint_as_float(rr[4 * j]), __uint_as_float(rr[4 * j + 1]),
+                                     __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3]));
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive_relaxed(&tempty[acc.slot]);
+                fence_release_smem_cluster();
+                for (int k2 = 0; k2 < CS; ++k2) mbar_arrive_cluster(mapa_shared(smem_u32(red_ready), k2));
+                mbar_wait_cluster(red_ready, tpar);
+                // rows [r0, r1) of the tile: fixed-order sum over ranks 0..CS-1 (deterministic)
+                const int r0 = crank * 128 / CS, r1 = (crank + 1) * 128 / CS, nr = r1 - r0;
+                const int g8 = BN / 8;
+                for (int u = tid; u < nr * g8; u += 128) {
+                    // bf16 planar output: consecutive threads take consecutive rows of one plane;
+                    // fp32 row-major output: consecutive threads take consecutive columns of a row
+                    const int rl = g.out_bf16 ? u % nr : u / g8, c8 = g.out_bf16 ? u / nr : u % g8;
+                    const int rw = r0 + rl;
+                    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                    for (int k2 = 0; k2 < CS; ++k2) {
+                        const uint32_t base = mapa_shared(red_a, k2) + (uint32_t)(rw * BN) * 4;
+                        const float4 f0 = ld_dsmem_v4(base + (uint32_t)(4 * ((2 * c8) ^ (rw & 7))) * 4);
+                        const float4 f1 = ld_dsmem_v4(base + (uint32_t)(4 * ((2 * c8 + 1) ^ (rw & 7))) * 4);
+                        v[0] += f0.x; v[1] += f0.y; v[2] += f0.z; v[3] += f0.w;
+                        v[4] += f1.x; v[5] += f1.y; v[6] += f1.z; v[7] += f1.w;
+                    }
+                    long long dst_row = 0;
+                    const bool valid = remap_row(g, m0 + rw, &dst_row);
+                    const int n = n0 + 8 * c8;
+                    if (!valid || n >= g.Nn) continue;
+                    if (g.out_bf16) {
+                        uint4 h, l;
+                        split_bf16x8(v, h, l);
+                        const long long off = ((long long)(n >> 3) * g.planar_stride + dst_row) * 8;
+                        *reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(g.out) + off) = h;
+                        *reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(g.out_lo) + off) = l;
+                    } else {
+                        float *dst = g.out + dst_row * g.ldo + n;
+                        for (int j = 0; j < 8; ++j)
+                            if (g.bias && n + j < g.Nn) v[j] += __ldg(&g.bias[n + j]);
+                        if (n + 8 <= g.Nn && (g.ldo & 3) == 0) {
+                            st_global_v4(dst, make_float4(v[0], v[1], v[2], v[3]));
+                            st_global_v4(dst + 4, make_float4(v[4], v[5], v[6], v[7]));
+                        } else {
+                            for (int j = 0; j < 8 && n + j < g.Nn; ++j) dst[j] = v[j];
+                        }
+                    }
+                }
+                for (int k2 = 0; k2 < CS; ++k2) mbar_arrive_cluster(mapa_shared(smem_u32(red_free), k2));
+                if (warp == 2 && lane == 0) BFTL(seq, tit, 5);
+                continue;
+            }
             long long dst_row = 0;
             const bool valid = remap_row(g, m0 + q * 32 + lane, &dst_row);
-            const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
             for (int c = 0; c < BN; c += 32) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(src + c, r);
@@ -304,24 +433,16 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             mbar_arrive_relaxed(&tempty[acc.slot]);
             if (warp == 2 && lane == 0) BFTL(seq, tit, 5);  // epilogue: done
         }
-    } else if (CONVERT) {  // ------- converter: fp32 staging -> bf16 hi/lo tiles (+ B loads)
+    } else if (CONVERT) {  // ----------------- converter: fp32 staging -> bf16 hi/lo A tiles
         const int tid = threadIdx.x - 192;
         Ring r(S), rx(SX);
         int tit = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tit) {
-            const int n0 = (t / mtiles) * BN;
-            int tap = 0, kc = 0;
-            for (int i = 0; i < iters; ++i, r.next(), rx.next()) {
+        for (int t = cid; t < num_tiles; t += ncl, ++tit) {
+            for (int i = i0; i < i1; ++i, r.next(), rx.next()) {
                 mbar_wait(&empty[r.slot], r.phase ^ 1);  // operand slot free
                 const uint32_t base = smem_u32(ops + (size_t)r.slot * slot_bytes);
-                if (tid == 0) {  // B = U_in^T hi/lo into the operand slot
-                    uint8_t *bs = ops + (size_t)r.slot * slot_bytes + kATile16;
-                    mbar_arrive_expect_tx(&full[r.slot], 2 * b_tile);
-                    tma_load_2d(bs, &mapB, &full[r.slot], kc * kBK16, g.b_off[tap] + n0);
-                    tma_load_2d(bs + half, &mapBlo, &full[r.slot], kc * kBK16, g.b_off[tap] + n0);
-                }
                 mbar_wait(&xfull[rx.slot], rx.phase);
-                if (i == 0 && tid == 0) BFTL(seq, tit, 6);  // converter: X landed
+                if (i == i0 && tid == 0) BFTL(seq, tit, 6);  // converter: X landed
                 const uint32_t stage = smem_u32(xstage + (size_t)rx.slot * kStage32);
 #pragma unroll
                 for (int k = 0; k < 1024 / kConvThreads16; ++k) {
@@ -345,49 +466,55 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                 mbar_arrive(&xempty[rx.slot]);  // staging slot may be refilled
                 fence_proxy_async_smem();
                 mbar_arrive(&conv[r.slot]);
-                if (i == iters - 1 && tid == 0) BFTL(seq, tit, 7);  // converter: done
-                if (++kc == g.kchunks) {
-                    kc = 0;
-                    ++tap;
-                }
+                if (i == i1 - 1 && tid == 0) BFTL(seq, tit, 7);  // converter: done
             }
         }
     }
     tc_fence_before();
     __syncthreads();
+    if (CS > 1) cluster_sync();  // no CTA leaves while a peer may still read its partial
+    if (threadIdx.x == 0) BFGSPAN(seq, 2);
     if (warp == 1) tmem_dealloc(tmem, 2 * ncols);
 #ifdef TDC_TIMELINE
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_tdc_bf_seq, 1u);
 #endif
 }
 
-int bf_smem_bytes(int BN, int stages, int xstages) {
-    const int half = kATile16 + BN * kBK16 * 2;
-    return 1024 + xstages * kStage32 + stages * 2 * half + kEpiScratch16 +
-           (3 * stages + 4 + 2 * xstages) * 8 + 16;
+// xstages > 0 (converting stage 1): xstages fp32 staging slots, `stages` A slots and
+// bstages weight slots; otherwise `stages` combined A|B slots.
+int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages) {
+    const int b_tile = BN * kBK16 * 2;
+    const int ops = xstages ? stages * 2 * kATile16 + bstages * 2 * b_tile : stages * 2 * (kATile16 + b_tile);
+    return 1024 + xstages * kStage32 + ops + kEpiScratch16 + (ksplit > 1 ? 128 * BN * 4 : 0) +
+           (3 * stages + 4 + 2 * xstages + 2 * bstages + 2) * 8 + 16;
 }
 
-// Operand-ring depth (and, for the converting stage 1, the fp32 staging depth).
-int bf_pick_stages(int BN, int max_smem, int convert, int *xstages) {
-    int s = convert ? 2 : 6, sx = convert ? 4 : 0;
-    while (sx > 2 && bf_smem_bytes(BN, s, sx) > max_smem) --sx;
-    while (s > 2 && bf_smem_bytes(BN, s, sx) > max_smem) --s;
+// Ring depths: operand slots (and, for the converting stage 1, the fp32 staging and
+// weight rings).
+int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, int *bstages) {
+    int s = convert ? 2 : 6, sx = convert ? 4 : 0, sb = convert ? 4 : 0;
+    while (sx > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb) > max_smem) --sx;
+    while (sb > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb) > max_smem) --sb;
+    while (s > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb) > max_smem) --s;
     if (xstages) *xstages = sx;
+    if (bstages) *bstages = sb;
     return s;
 }
 
 cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, const CUtensorMap &mapB,
                            const CUtensorMap &mapBlo, const TcGemmArgs &g, int grid, cudaStream_t st) {
-    const int smem = bf_smem_bytes(g.BN, g.stages, g.a_convert ? g.xstages : 0);
+    const int smem = bf_smem_bytes(g.BN, g.stages, g.a_convert ? g.xstages : 0, g.ksplit, g.a_convert ? g.bstages : 0);
     cudaError_t e;
     if (g.a_convert) {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        return launch_pdl(tdc_bf_gemm_kernel<true>, grid, 192 + kConvThreads16, smem, st, mapA, mapAlo, mapB, mapBlo, g);
+        return launch_pdl_cluster(tdc_bf_gemm_kernel<true>, grid, 192 + kConvThreads16, smem, st, g.ksplit, mapA,
+                                  mapAlo, mapB, mapBlo, g);
     } else {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        return launch_pdl(tdc_bf_gemm_kernel<false>, grid, 192, smem, st, mapA, mapAlo, mapB, mapBlo, g);
+        return launch_pdl_cluster(tdc_bf_gemm_kernel<false>, grid, 192, smem, st, g.ksplit, mapA, mapAlo, mapB,
+                                  mapBlo, g);
     }
     return cudaGetLastError();
 }
@@ -492,12 +619,14 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         if (F3) mbar_init(w3_full, 1);
         fence_mbar_init();
     }
+    if (threadIdx.x == 0) BFCSPAN(0);
     if (warp == 1) tmem_alloc(tmem_slot, tcols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     pdl_wait();
     pdl_launch_dependents();
+    if (threadIdx.x == 0) BFCSPAN(1);
     const uint32_t tmem = *tmem_slot;
 
     // phase-grid row m -> compact output row (b, oy, ox), or invalid
@@ -770,6 +899,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) BFCSPAN(2);
     if (warp == 1) tmem_dealloc(tmem, tcols);
 }
 

@@ -47,3 +47,27 @@ if len(tp):
     print("--- core kernel CTA 0 tile 0 per (kc, tap): producer-issue  mma-ready (us)")
     for i, r in enumerate(tp[:80]):
         print(i, " ".join(f"{(v - t0) / 1000:7.2f}" for v in r))
+bufs = (ctypes.c_ulonglong * 4096)()
+tdc.lib.tdc_debug_bfc_span(bufs, 4096)
+sp = np.array(bufs, dtype=np.int64).reshape(1024, 4)[:, :3]
+sp = sp[sp[:, 0] > 0]
+if len(sp):
+    t0 = sp[:, 0].min()
+    st, pro, en = (sp[:, 0] - t0) / 1e3, (sp[:, 1] - t0) / 1e3, (sp[:, 2] - t0) / 1e3
+    print(f"--- core kernel per-CTA spans ({len(sp)} CTAs, us from first start): start max {st.max():.2f}, "
+          f"prologue-done min/med/max {pro.min():.2f}/{np.median(pro):.2f}/{pro.max():.2f}, "
+          f"end min/med/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f}")
+    print("   end percentiles 10/50/90/99:", np.percentile(en, [10, 50, 90, 99]).round(2))
+bufg = (ctypes.c_ulonglong * (4 * 1024 * 4))()
+tdc.lib.tdc_debug_bfg_span(bufg, 4 * 1024 * 4)
+gs = np.array(bufg, dtype=np.int64).reshape(4, 1024, 4)[:, :, :3]
+for seq in range(4):
+    sp = gs[seq]
+    sp = sp[sp[:, 0] > 0]
+    if not len(sp):
+        continue
+    t0 = sp[:, 0].min()
+    st, pro, en = (sp[:, 0] - t0) / 1e3, (sp[:, 1] - t0) / 1e3, (sp[:, 2] - t0) / 1e3
+    print(f"--- gemm launch seq {seq} per-CTA spans ({len(sp)} CTAs): start max {st.max():.2f}, "
+          f"prologue-done min/med/max {pro.min():.2f}/{np.median(pro):.2f}/{pro.max():.2f}, "
+          f"end min/med/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f}")

@@ -196,6 +196,10 @@ def test_forward_rejects_bad_calls(env):
     LayerShape(3, 64, 40, 13, 11, 24, 20, 3, 1, 1),
     LayerShape(2, 32, 48, 15, 9, 16, 32, 3, 2, 1),
     LayerShape(2, 40, 72, 12, 10, 40, 48, 5, 1, 2),
+    # small M, long K: split-K over clusters (stages 1 and 3)
+    LayerShape(2, 512, 256, 5, 7, 256, 128, 3, 1, 1),
+    LayerShape(3, 256, 512, 4, 4, 128, 256, 3, 2, 1),
+    LayerShape(1, 320, 96, 3, 3, 192, 64, 1, 1, 0),
 ], ids=lambda s: s.name or f"{s.C}_{s.N}_{s.H}x{s.W}_k{s.K}_s{s.stride}")
 def test_3xbf16_core3_and_three_launch(env, shape, fuse3, monkeypatch):
     """3xBF16 with stage 3 fused into the core kernel (Z on chip) where it fits,
@@ -219,3 +223,22 @@ def test_3xbf16_variant_names(env, shape, count):
     assert info.variant_name in ("tc2_3xbf16_core3", "tc3_3xbf16_band")
     assert info.launches_per_forward == (2 if info.variant_name == "tc2_3xbf16_core3" else 3)
     plan.close()
+
+
+@pytest.mark.parametrize("shape", [
+    LayerShape(2, 512, 256, 5, 7, 256, 128, 3, 1, 1),
+    LayerShape(3, 256, 512, 4, 4, 128, 256, 3, 2, 1),
+], ids=lambda s: f"{s.C}_{s.N}_{s.H}x{s.W}_s{s.stride}")
+def test_3xbf16_split_k_matches_unsplit(env, shape, monkeypatch):
+    """Split-K (cluster DSMEM reduction) and the unsplit path agree to rounding, and
+    the split result is deterministic run to run (fixed reduction order, R10)."""
+    s = shape.with_batch(shape.B)
+    d = synth.make_layer(s, seed=5, bias=True)
+    monkeypatch.setenv("TDC_SPLITK", "1")
+    a, _ = run_layer(env, s, d, "nhwc", "3xbf16")
+    b, _ = run_layer(env, s, d, "nhwc", "3xbf16")
+    assert np.array_equal(a, b)
+    monkeypatch.setenv("TDC_SPLITK", "0")
+    c, _ = run_layer(env, s, d, "nhwc", "3xbf16")
+    ref = ref_of(s, d)
+    assert err(a, ref) <= TOL["3xbf16"] and err(c, ref) <= TOL["3xbf16"]
