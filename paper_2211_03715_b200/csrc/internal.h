@@ -140,8 +140,9 @@ struct BfCoreArgs {
     const float *bias;
     float *y;                 // Y [B*Ho*Wo][N3]
     int N3, N3p, ncat3;       // output channels, padded (mult. of 16), hi|lo concat in one MMA
+    int ksplit;               // >1: split the D1 chunks over a cluster (stage 2 alone, not fused)
 };
-int bf_core_smem_bytes(int BN, int nphase, int band_rows, int tg, int w_slots);
+int bf_core_smem_bytes(int BN, int nphase, int band_rows, int tg, int w_slots, int ksplit);
 int bf_core3_smem_bytes(const BfCoreArgs &g);
 int bf_core3_tmem_cols(const BfCoreArgs &g);
 cudaError_t bf_core3_launch(const BfCoreArgs &g, int grid, cudaStream_t st);

@@ -421,7 +421,7 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
             for (; b >= 32; b /= 2) {
                 const long long tiles = (long long)div_up((int)mrows, 128) * div_up(nn, b);
                 int cs = 1;
-                for (int c = 2; c <= 8 && c <= iters; ++c)
+                for (int c = 2; c <= 4 && c <= iters; ++c)
                     if (tiles * c <= p->num_sms) cs = c;
                 const long long u = std::min<long long>(tiles * cs, p->num_sms);
                 if (u > best_u) {
@@ -496,9 +496,39 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
             }
         }
     }
+    // Stage-2 split-K (opt-in, TDC_SPLITK=1): when the output tiles leave SMs idle, pick
+    // (BN2, cluster size) minimising a simple cost model: waves x chunks-per-CTA x MMA
+    // cycles per chunk (measured issue cost) + a handshake overhead.
+    int ks2 = 1;
+    {
+        const char *ev = std::getenv("TDC_SPLITK");
+        const bool on = ev && ev[0] && ev[0] != '0';
+        const long long mt = div_up((int)M2, 128);
+        if (on && !fuse3 && mt * div_up(D2s, BN2) < p->num_sms) {
+            auto mma = [](int n) { return n <= 64 ? (n <= 32 ? 44.0 : 48.0) : n / 2.0; };
+            double best = 1e30;
+            int bn_top = 32;
+            while (bn_top < D2s && bn_top < 128) bn_top *= 2;
+            for (int bn = bn_top; bn >= 32; bn /= 2) {
+                const double per_kc = 2.0 * KK * (2 * bn <= 128 ? 2 * mma(2 * bn) : 3 * mma(bn));
+                const long long tiles = mt * div_up(D2s, bn);
+                for (int cs = 1; cs <= 4 && cs <= k2chunks; ++cs) {
+                    if (cs > 1 && tiles * cs > p->num_sms) break;
+                    const long long per_cta = div_up((int)tiles, std::max(1, p->num_sms / cs));
+                    const double t = per_cta * div_up(k2chunks, cs) * per_kc + (cs > 1 ? 3000.0 : 0.0);
+                    if (t < best - 1.0) {
+                        best = t;
+                        BN2 = bn;
+                        ks2 = cs;
+                    }
+                }
+            }
+        }
+    }
     for (; !fuse3 && BN2 >= 32; BN2 /= 2) {
         nt2 = div_up(D2s, BN2);
-        if (nt2 == 1 && tdc::bf_core_smem_bytes(BN2, nphase, band_rows, KK, k2chunks) <= p->max_smem) {
+        if (ks2 == 1 && nt2 == 1 &&
+            tdc::bf_core_smem_bytes(BN2, nphase, band_rows, KK, k2chunks, 1) <= p->max_smem) {
             tg = KK;
             w_slots = k2chunks;
             resident = 1;
@@ -507,7 +537,7 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         for (int g = KK; g >= 1 && !tg; --g) {
             if (KK % g) continue;
             for (int ws = 4; ws >= 2; --ws)
-                if (tdc::bf_core_smem_bytes(BN2, nphase, band_rows, g, ws) <= p->max_smem) {
+                if (tdc::bf_core_smem_bytes(BN2, nphase, band_rows, g, ws, ks2) <= p->max_smem) {
                     tg = g;
                     w_slots = ws;
                     break;
@@ -628,6 +658,7 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         g.ldz = D2p; g.Nn = D2s; g.M = (int)M2; g.kchunks = k2chunks; g.taps = KK;
         g.ntiles = nt2; g.BN = BN2; g.nphase = nphase; g.band_rows = band_rows;
         g.tg = tg; g.ngroups = ngroups; g.w_slots = w_slots; g.w_resident = resident; g.ncat = ncat;
+        g.ksplit = ks2;
         g.phase_rows = phase_rows;
         for (int r = 0; r < K; ++r)
             for (int t = 0; t < K; ++t) {
@@ -704,8 +735,8 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
         return TDC_OK;
     }
     e = tdc::bf_core_launch(
-        c, grid(c.M, c.ntiles, tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots),
-                c.ncat ? 2 * c.BN : c.BN), st);
+        c, grid_ks(c.M, c.ntiles, tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots, c.ksplit),
+                   c.ncat ? 2 * c.BN : c.BN, c.ksplit), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-2 launch");
     e = tdc::bf_gemm_launch(
         s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, a3,
@@ -1111,7 +1142,8 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
         info->tile_w = c.BN;
         info->threads_per_cta = p->fuse3 ? 320 : 192;
         info->smem_bytes_per_cta = p->fuse3 ? tdc::bf_core3_smem_bytes(c)
-                                            : tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots);
+                                            : tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots,
+                                                                      c.ksplit);
     }
     if (fz) {
         info->tile_h = p->fargs.R;

@@ -138,6 +138,46 @@ __device__ __forceinline__ void warp_store_block32_b16(float *scratch, const uin
     __syncwarp();
 }
 
+// ------------------------------------------------ split-K over a cluster (DSMEM)
+// Each CTA of a cluster of CS (<= kMaxSplit) CTAs accumulates a K range of the same
+// output tile; the fp32 partials go to shared memory ([128 rows][W cols], 16-byte
+// chunks swizzled by row % 8), and after a cluster handshake CTA r sums rows
+// [r*128/CS, (r+1)*128/CS) over ranks 0..CS-1 in that fixed order (deterministic).
+constexpr int kMaxSplit = 4;
+
+__device__ __forceinline__ void red_store_row32(uint32_t red_a, int W, int row, int c, const float *v) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int j4 = c / 4 + j;
+        st_shared_v4(red_a + (uint32_t)(row * W + 4 * (j4 ^ (row & 7))) * 4, v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                     v[4 * j + 3]);
+    }
+}
+// v[0..7] = sum over ranks of columns [8*c8, 8*c8 + 8) of row rw (all loads issued first)
+__device__ __forceinline__ void red_sum8(uint32_t red_a, int W, int CS, int rw, int c8, float *v) {
+    float4 f[2 * kMaxSplit];
+    const uint32_t o0 = (uint32_t)(rw * W + 4 * ((2 * c8) ^ (rw & 7))) * 4;
+    const uint32_t o1 = (uint32_t)(rw * W + 4 * ((2 * c8 + 1) ^ (rw & 7))) * 4;
+#pragma unroll
+    for (int k = 0; k < kMaxSplit; ++k)
+        if (k < CS) {
+            const uint32_t base = mapa_shared(red_a, k);
+            f[2 * k] = ld_dsmem_v4(base + o0);
+            f[2 * k + 1] = ld_dsmem_v4(base + o1);
+        }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxSplit; ++k)
+        if (k < CS) {
+            v[0] += f[2 * k].x; v[1] += f[2 * k].y; v[2] += f[2 * k].z; v[3] += f[2 * k].w;
+            v[4] += f[2 * k + 1].x; v[5] += f[2 * k + 1].y; v[6] += f[2 * k + 1].z; v[7] += f[2 * k + 1].w;
+        }
+}
+__device__ __forceinline__ void red_signal(uint64_t *bar, int CS) {
+    for (int k = 0; k < CS; ++k) mbar_arrive_cluster(mapa_shared(smem_u32(bar), k));
+}
+
 // ============================================================ GEMM (stages 1, 3)
 constexpr int kConvThreads16 = 256;  // 8 converter warps (stage 1 is converter-paced otherwise)
 
@@ -336,20 +376,13 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                     uint32_t rr[32];
                     tmem_ld_32x32b_x32(src + c, rr);
                     tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {  // float4 column j4 of row, swizzled by row % 8
-                        const int j4 = c / 4 + j;
-                        st_shared_v4(red_a + (uint32_t)(row * BN + 4 * (j4 ^ (row & 7))) * 4,
-                                     __uint_as_float(rr[4 * j]), __uint_as_float(rr[4 * j + 1]),
-                                     __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3]));
-                    }
+                    red_store_row32(red_a, BN, row, c, reinterpret_cast<const float *>(rr));
                 }
                 tc_fence_before();
                 mbar_arrive_relaxed(&tempty[acc.slot]);
                 fence_release_smem_cluster();
-                for (int k2 = 0; k2 < CS; ++k2) mbar_arrive_cluster(mapa_shared(smem_u32(red_ready), k2));
+                red_signal(red_ready, CS);
                 mbar_wait_cluster(red_ready, tpar);
-                // rows [r0, r1) of the tile: fixed-order sum over ranks 0..CS-1 (deterministic)
                 const int r0 = crank * 128 / CS, r1 = (crank + 1) * 128 / CS, nr = r1 - r0;
                 const int g8 = BN / 8;
                 for (int u = tid; u < nr * g8; u += 128) {
@@ -357,14 +390,8 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                     // fp32 row-major output: consecutive threads take consecutive columns of a row
                     const int rl = g.out_bf16 ? u % nr : u / g8, c8 = g.out_bf16 ? u / nr : u % g8;
                     const int rw = r0 + rl;
-                    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                    for (int k2 = 0; k2 < CS; ++k2) {
-                        const uint32_t base = mapa_shared(red_a, k2) + (uint32_t)(rw * BN) * 4;
-                        const float4 f0 = ld_dsmem_v4(base + (uint32_t)(4 * ((2 * c8) ^ (rw & 7))) * 4);
-                        const float4 f1 = ld_dsmem_v4(base + (uint32_t)(4 * ((2 * c8 + 1) ^ (rw & 7))) * 4);
-                        v[0] += f0.x; v[1] += f0.y; v[2] += f0.z; v[3] += f0.w;
-                        v[4] += f1.x; v[5] += f1.y; v[6] += f1.z; v[7] += f1.w;
-                    }
+                    float v[8];
+                    red_sum8(red_a, BN, CS, rw, c8, v);
                     long long dst_row = 0;
                     const bool valid = remap_row(g, m0 + rw, &dst_row);
                     const int n = n0 + 8 * c8;
@@ -387,7 +414,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                         }
                     }
                 }
-                for (int k2 = 0; k2 < CS; ++k2) mbar_arrive_cluster(mapa_shared(smem_u32(red_free), k2));
+                red_signal(red_free, CS);
                 if (warp == 2 && lane == 0) BFTL(seq, tit, 5);
                 continue;
             }
@@ -530,9 +557,9 @@ __host__ __device__ inline uint32_t bf_core_a_half(int nphase, int band_rows) {
     return (uint32_t)nphase * 4 * band_rows * 16;  // 4 planes of 8 bf16 channels per chunk
 }
 
-int bf_core_smem_bytes(int BN, int nphase, int band_rows, int tg, int w_slots) {
+int bf_core_smem_bytes(int BN, int nphase, int band_rows, int tg, int w_slots, int ksplit) {
     return 1024 + 2 * 2 * (int)bf_core_a_half(nphase, band_rows) + w_slots * tg * BN * 128 + kEpiScratch16 +
-           (8 + 2 * w_slots) * 8 + 16;
+           (ksplit > 1 ? 128 * BN * 4 : 0) + (10 + 2 * w_slots) * 8 + 16;
 }
 
 __host__ __device__ inline int bf_pow2_cols(int c) {
@@ -545,7 +572,7 @@ __host__ __device__ inline int bf_pow2_cols(int c) {
 __host__ __device__ inline int bf_core3_zbuf(const BfCoreArgs &g) { return (g.BN / 8) * 128 * 16 * 2; }
 __host__ __device__ inline int bf_core3_w3(const BfCoreArgs &g) { return (g.BN / 8) * 2 * g.N3p * 16; }
 int bf_core3_smem_bytes(const BfCoreArgs &g) {
-    return bf_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.tg, g.w_slots) + 2 * bf_core3_zbuf(g) +
+    return bf_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.tg, g.w_slots, 1) + 2 * bf_core3_zbuf(g) +
            bf_core3_w3(g) + 9 * 8;
 }
 __host__ __device__ inline int bf_core3_tmem(const BfCoreArgs &g) {
@@ -576,14 +603,19 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
     uint8_t *w_slots = smem + 2 * (size_t)a_bytes;
     float *epi_scratch = reinterpret_cast<float *>(w_slots + (size_t)WS * w_slot);
     uint8_t *zs = reinterpret_cast<uint8_t *>(epi_scratch) + kEpiScratch16;  // F3: 2 Z buffers
-    uint8_t *w3s = zs + 2 * (size_t)zbuf;                                    // F3: U_out panel
+    const int CS = (!F3 && g.ksplit > 1) ? g.ksplit : 1;                      // split-K cluster size
+    float *red = reinterpret_cast<float *>(zs);                              // split-K partial [128][BN]
+    const uint32_t red_bytes = CS > 1 ? (uint32_t)128 * BN * 4 : 0u;
+    uint8_t *w3s = zs + 2 * (size_t)zbuf + red_bytes;                        // F3: U_out panel
     uint64_t *a_full = reinterpret_cast<uint64_t *>(w3s + w3_bytes);
     uint64_t *a_empty = a_full + 2;
     uint64_t *tfull = a_empty + 2;
     uint64_t *tempty = tfull + 2;
     uint64_t *w_full = tempty + 2;
     uint64_t *w_empty = w_full + WS;
-    uint64_t *z_full = w_empty + WS;   // F3 only from here on
+    uint64_t *red_ready = w_empty + WS;  // split-K handshake
+    uint64_t *red_free = red_ready + 1;
+    uint64_t *z_full = red_free + 1;   // F3 only from here on
     uint64_t *z_empty = z_full + 2;
     uint64_t *t3full = z_empty + 2;
     uint64_t *t3empty = t3full + 2;
@@ -598,6 +630,9 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
     const int mtiles = (g.M + kBM16 - 1) / kBM16;
     const int num_tiles = mtiles * g.ntiles;
     const bool resident = g.w_resident != 0;
+    const int crank = CS > 1 ? (int)cluster_ctarank() : 0;
+    const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;                 // cluster id / count
+    const int k0 = crank * g.kchunks / CS, k1 = (crank + 1) * g.kchunks / CS;  // this CTA's chunks
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -617,12 +652,15 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             mbar_init(&w_empty[i], 1);
         }
         if (F3) mbar_init(w3_full, 1);
+        mbar_init(red_ready, CS * 128);
+        mbar_init(red_free, CS * 128);
         fence_mbar_init();
     }
     if (threadIdx.x == 0) BFCSPAN(0);
     if (warp == 1) tmem_alloc(tmem_slot, tcols);
     tc_fence_before();
     __syncthreads();
+    if (CS > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
     tc_fence_after();
     pdl_wait();
     pdl_launch_dependents();
@@ -657,11 +695,11 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                 load_split(w_slots + (size_t)i * w_slot, wsrc + (size_t)i * w_slot, w_slot, &w_full[i]);
         Ring ra(2), rw(WS);
         int tit = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++tit) {
+        for (int t = cid; t < num_tiles; t += ncl, ++tit) {
             const int m0 = (t % mtiles) * kBM16, nt = t / mtiles;
-            for (int kc = 0; kc < g.kchunks; ++kc, ra.next()) {
+            for (int kc = k0; kc < k1; ++kc, ra.next()) {
                 mbar_wait(&a_empty[ra.slot], ra.phase ^ 1);
-                if (kc == 0 && lane == 0) BFCTL(tit, 0);  // producer: band issue
+                if (kc == k0 && lane == 0) BFCTL(tit, 0);  // producer: band issue
                 if (lane == 0) mbar_arrive_expect_tx(&a_full[ra.slot], a_bytes);
                 __syncwarp();
                 uint8_t *dst = a_slots + (size_t)ra.slot * a_bytes;
@@ -698,7 +736,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         int tit = 0;
         bool pending = false;  // F3: S3 of the previous tile still to issue
         if (F3) mbar_wait(w3_full, 0);
-        for (int t = blockIdx.x;; t += gridDim.x, ++tit) {
+        for (int t = cid;; t += ncl, ++tit) {
             const bool have = t < num_tiles;
             if (have) {
                 mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
@@ -706,9 +744,9 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                 if (lane == 0) BFCTL(tit, 1);  // MMA: accumulator free
                 const uint32_t d = tmem + acc.slot * ncols;
                 uint32_t accum = 0;
-                for (int kc = 0; kc < g.kchunks; ++kc, ra.next()) {
+                for (int kc = k0; kc < k1; ++kc, ra.next()) {
                     mbar_wait(&a_full[ra.slot], ra.phase);
-                    if (kc == 0 && lane == 0) BFCTL(tit, 2);  // MMA: band landed
+                    if (kc == k0 && lane == 0) BFCTL(tit, 2);  // MMA: band landed
                     for (int grp = 0; grp < g.ngroups; ++grp) {
                         int ws;
                         if (resident) {
@@ -793,11 +831,53 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         const int r = q * 32 + lane;  // tile row = TMEM lane
         Ring acc(2), zr(2);
         int tit = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, acc.next(), zr.next(), ++tit) {
+        for (int t = cid; t < num_tiles; t += ncl, acc.next(), zr.next(), ++tit) {
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
             mbar_wait(&tfull[acc.slot], acc.phase);
             tc_fence_after();
             if (warp == 2 && lane == 0) BFCTL(tit, 4);  // epilogue: accumulator ready
+            if (!F3 && CS > 1) {  // ---- split-K: partial -> own smem, reduce a row slice
+                const uint32_t red_a = smem_u32(red), tpar = (uint32_t)(tit & 1);
+                const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
+                mbar_wait_cluster(red_free, tpar ^ 1);
+                for (int c = 0; c < BN; c += 32) {
+                    uint32_t rr[32];
+                    float v[32];
+                    tmem_ld_32x32b_x32(src + c, rr);
+                    if (g.ncat) {
+                        uint32_t r2[32];
+                        tmem_ld_32x32b_x32(src + BN + c, r2);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]) + __uint_as_float(r2[j]);
+                    } else {
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
+                    }
+                    red_store_row32(red_a, BN, r, c, v);
+                }
+                tc_fence_before();
+                mbar_arrive_relaxed(&tempty[acc.slot]);
+                fence_release_smem_cluster();
+                red_signal(red_ready, CS);
+                mbar_wait_cluster(red_ready, tpar);
+                const int r0 = crank * 128 / CS, r1 = (crank + 1) * 128 / CS, nr = r1 - r0, g8 = BN / 8;
+                for (int u = r; u < nr * g8; u += 128) {  // Z row-major: threads along columns
+                    const int rw = r0 + u / g8, c8 = u % g8;
+                    float v[8];
+                    red_sum8(red_a, BN, CS, rw, c8, v);
+                    long long dr = 0;
+                    const int n = n0 + 8 * c8;
+                    if (!out_row(m0 + rw, &dr) || n >= g.Nn) continue;
+                    uint4 h, l;
+                    split_bf16x8(v, h, l);
+                    *reinterpret_cast<uint4 *>(z + dr * g.ldz + n) = h;
+                    *reinterpret_cast<uint4 *>(z_lo + dr * g.ldz + n) = l;
+                }
+                red_signal(red_free, CS);
+                continue;
+            }
             long long dst_row = 0;
             const bool valid = out_row(m0 + r, &dst_row);
             if (F3) mbar_wait(&z_empty[zr.slot], zr.phase ^ 1);
@@ -858,7 +938,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         const int q = warp & 3;
         float *scratch = epi_scratch + q * 1024;
         Ring a3(2);
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, a3.next()) {
+        for (int t = cid; t < num_tiles; t += ncl, a3.next()) {
             const int m0 = (t % mtiles) * kBM16;
             mbar_wait(&t3full[a3.slot], a3.phase);
             tc_fence_after();
@@ -899,16 +979,17 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
     }
     tc_fence_before();
     __syncthreads();
+    if (CS > 1) cluster_sync();  // no CTA leaves while a peer may still read its partial
     if (threadIdx.x == 0) BFCSPAN(2);
     if (warp == 1) tmem_dealloc(tmem, tcols);
 }
 
 cudaError_t bf_core_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
-    const int smem = bf_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.tg, g.w_slots);
+    const int smem = bf_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.tg, g.w_slots, g.ksplit);
     cudaError_t e =
         cudaFuncSetAttribute(tdc_bf_core_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(tdc_bf_core_kernel<false>, grid, 192, smem, st, g);
+    return launch_pdl_cluster(tdc_bf_core_kernel<false>, grid, 192, smem, st, g.ksplit, g);
 }
 
 cudaError_t bf_core3_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {

@@ -12,11 +12,19 @@ from scripts.parse_launches import load  # noqa: E402
 
 math, path = sys.argv[1], sys.argv[2]
 ks = load(path)
-# group launches into layer forwards: fused/simt = 1 launch, tc3 = gemm, (core|gemm), gemm
+# group launches into layer forwards: 3xBF16 = a stage-1 launch (tdc_bf_gemm_kernel<1>)
+# followed by core3, or core + stage-3 gemm; TF32/3xTF32 three-launch = gemm, (core|gemm),
+# gemm; fused/simt = 1 launch
 groups, i = [], 0
 while i < len(ks):
     n = ks[i]["name"]
-    if "tc_gemm" in n:
+    if "tdc_bf_gemm_kernel<1>" in n:
+        j = i + 1
+        while j < len(ks) and "tdc_bf_gemm_kernel<1>" not in ks[j]["name"] and j - i < 3:
+            j += 1
+        groups.append(ks[i:j])
+        i = j
+    elif "tc_gemm" in n:
         groups.append(ks[i:i + 3])
         i += 3
     else:
@@ -37,8 +45,9 @@ data[math] = {nm: int(statistics.mean(b for b, _, _ in v)) for nm, v in per.item
 data[math + "_ncu_us"] = {nm: round(statistics.mean(t for _, t, _ in v) / 1e3, 2) for nm, v in per.items()}
 data[math + "_kernels"] = {nm: v[0][2] for nm, v in per.items()}
 data["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per layer forward, from the ncu "
-                 "launch list of one bench step (cold-cache, serialised replay); ncu_us is the "
-                 "ncu duration of the same launches (not a bench number)")
+                 "launch list of one bench step (cold-cache, serialised replay); writes that stay in "
+                 "the 126 MB L2 past the kernel's end are not counted, so this is mostly read "
+                 "traffic; ncu_us is the ncu duration of the same launches (not a bench number)")
 json.dump(data, open(out_path, "w"), indent=1)
 print(json.dumps({k: data[k] for k in (math, math + "_ncu_us")}, indent=1))
 print("steps seen:", steps, "groups:", len(groups))
