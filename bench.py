@@ -55,6 +55,9 @@ def parse():
                          "tf32: 1e-2 mode; fp32: CUDA-core FFMA")
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-model", action="store_true",
+                    help="skip the Tucker ResNet-50 whole-model images/s measurement")
+    ap.add_argument("--model-batch", type=int, default=32)
     ap.add_argument("--no-graph", action="store_true",
                     help="issue the timed steps as individual launches instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")
@@ -341,6 +344,49 @@ def impl_tdc(args):
                  "timing": "layer alone, back-to-back forwards between CUDA events on the launching stream, "
                            "inputs rotated over > 2x L2"})
 
+    # ---- Tucker ResNet-50 whole-model inference (BASELINE metric part 2, config 3):
+    # each rank runs the full model on its own batch shard (weak scaling, no collective
+    # beyond the timing barrier); images/s = all ranks' images / max-over-ranks time.
+    model = None
+    if not args.no_model:
+        import synth.models as sm
+        ops = sm.tucker_resnet(50, seed=synth.BASE_SEED + 1000 * rank)
+        mb = args.model_batch
+        net = tdc.Model(ops, max_batch=mb, device=local)
+        mh, mw, mc = net.output_shape()
+        mx = torch.from_numpy(sm.model_input(mb, 224, seed=synth.BASE_SEED + rank)).cuda()
+        mo = torch.empty((mb, mh, mw, mc), device="cuda")
+        with torch.cuda.stream(stream):
+            for _ in range(max(args.warmup, 3)):
+                net.forward(mx, mo, stream=stream)
+        torch.cuda.synchronize()
+        mgraph = None
+        if not args.no_graph:
+            mgraph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(mgraph, stream=stream):
+                net.forward(mx, mo, stream=stream)
+            torch.cuda.synchronize()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tdist.barrier()
+        torch.cuda.synchronize()
+        m0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                if mgraph is not None:
+                    mgraph.replay()
+                else:
+                    net.forward(mx, mo, stream=stream)
+        m1.record(stream)
+        torch.cuda.synchronize()
+        tdist.barrier()
+        mms = tdist.max_over_ranks(m0.elapsed_time(m1), "cuda") / args.steps
+        model = {"arch": "tucker_resnet50", "ranks": "paper-style r = 1/4 (D = C/4) on every 3x3 conv",
+                 "input": "224x224x3 synthetic, NHWC fp32", "math": "3xbf16 (fp32-grade)",
+                 "batch_per_gpu": mb, "n_gpus": world, "ms_per_batch": round(mms, 4),
+                 "images_per_s": round(mb * world / (mms * 1e-3), 1),
+                 "launch": "cuda_graph_replay" if mgraph is not None else "stream_launches"}
+        net.close()
+
     # ---- end to end through the host-buffer C-ABI call ----
     e2e = None
     if not args.no_e2e:
@@ -389,7 +435,7 @@ def impl_tdc(args):
                              "3xbf16": "hi*hi+hi*lo+lo*hi bf16 split, fp32 accumulate; fp32-grade, "
                                        "tolerance 1e-4"}[args.math],
                 "data": "synthetic", "config": config_dict(args, world),
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "model": model,
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": sampler.summary(), "layers": layer_rows,
                 "step_bytes": step_bytes, "step_flops": sum(rl.tkd_flops(L["shape"]) for L in layers)}

@@ -125,6 +125,73 @@ tdc_status tdc_conv_forward_host(tdc_conv_plan_t plan, const float *x_host,
 
 tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t plan);
 
+/* Forward with the model-path epilogue fused into the last stage (SURVEY §8(f)
+ * NEXT-1: "BN folded into U_out and bias; ReLU and residual fused into stage-3
+ * epilogues"): y = act(layer(x) + bias + residual), act = ReLU if relu != 0.
+ * residual: DEVICE fp32 with y's shape and layout, or NULL; it may not alias y.
+ * Only NHWC plans in TDC_MATH_3XBF16 support residual/relu (UNSUPPORTED
+ * otherwise); with residual == NULL and relu == 0 this is tdc_conv_forward. */
+tdc_status tdc_conv_forward_ex(tdc_conv_plan_t plan, const float *x, float *y,
+                               int32_t batch, const float *residual, int32_t relu,
+                               void *stream);
+
+/* ------------------------------------------------------------------ models
+ * Whole-network inference (Tucker ResNet / VGG) as an
+ * ordered list of ops over NHWC fp32 activations.  Activation ids: 0 is the
+ * model input (batch x H x W x C), op i (0-based) writes id i + 1; the output of
+ * the last op is the model output.  Every op computes in 3xBF16 (fp32-grade
+ * tensor-core products, tolerance 1e-4 per layer) or FP32 where noted.
+ *   TDC_OP_CONV    dense K x K conv (stride, pad) of src; w = [c_out][c_in][K][K]
+ *                  (im2col + tcgen05 GEMM; 1 x 1 stride 1 is a plain GEMM)
+ *   TDC_OP_TKD     Tucker-2 conv (the TKD layer): w = core [D2][D1][K][K],
+ *                  u_in [c_in][D1], u_out [c_out][D2]
+ *   TDC_OP_MAXPOOL K x K max pool (stride, pad; padding never wins), fp32
+ *   TDC_OP_AVGPOOL global average pool -> batch x 1 x 1 x c_in, fp32
+ *   TDC_OP_FC      fully connected on a batch x 1 x 1 x c_in input; w = [c_out][c_in]
+ * Conv/TKD/FC outputs: y = act(BN(conv(src)) + bias + res), BN folded at create
+ * time from bn = [4][c_out] (gamma, beta, mean, var; eps 1e-5) or none (NULL);
+ * res = activation id added before the activation (same shape as the output)
+ * or -1; act = ReLU if relu. */
+typedef enum {
+    TDC_OP_CONV = 0,
+    TDC_OP_TKD = 1,
+    TDC_OP_MAXPOOL = 2,
+    TDC_OP_AVGPOOL = 3,
+    TDC_OP_FC = 4
+} tdc_op_kind;
+
+typedef struct {
+    int32_t kind;
+    int32_t src, res;                    /* activation ids (res = -1: none) */
+    int32_t c_in, c_out, height, width;  /* input geometry of one image */
+    int32_t kernel, stride, pad;
+    int32_t rank_in, rank_out;           /* TDC_OP_TKD: D1, D2 */
+    int32_t relu;
+    const float *w, *u_in, *u_out;       /* HOST, see above */
+    const float *bias;                   /* HOST [c_out] or NULL */
+    const float *bn;                     /* HOST [4][c_out] or NULL */
+} tdc_model_op;
+
+typedef struct tdc_model_s *tdc_model_t;
+
+/* Build a model on `device` for batches up to max_batch: validates the op graph
+ * (geometry of every src/res id), folds BN, plans every layer and allocates every
+ * activation buffer (device memory owned by the model).  Host arrays are copied. */
+tdc_status tdc_model_create(const tdc_model_op *ops, int32_t n_ops, int32_t max_batch,
+                            int32_t device, tdc_model_t *out);
+
+/* x: DEVICE fp32 NHWC batch x H x W x C (the first op's input geometry);
+ * out: DEVICE fp32, batch x (last op's output) NHWC, fully overwritten.
+ * Asynchronous on `stream`; 1 <= batch <= max_batch. */
+tdc_status tdc_model_forward(tdc_model_t model, const float *x, int32_t batch, float *out,
+                             void *stream);
+
+/* Output geometry of op `op` (or of the model if op < 0): per-image H, W, C. */
+tdc_status tdc_model_output_shape(tdc_model_t model, int32_t op, int32_t *h, int32_t *w,
+                                  int32_t *c);
+
+tdc_status tdc_model_destroy(tdc_model_t model);
+
 #ifdef __cplusplus
 }
 #endif

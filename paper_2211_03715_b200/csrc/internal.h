@@ -57,6 +57,8 @@ struct TcGemmArgs {
     int xstages;      // 3xBF16 stage 1: depth of the fp32 staging ring (separate from `stages`)
     int ksplit;       // 3xBF16: >1 = split K over a cluster of ksplit CTAs, DSMEM reduction
     int bstages;      // 3xBF16 stage 1: depth of the weight (B) ring
+    const float *res; // fp32 output only: residual added before the activation (ld = ldo), or null
+    int relu;         // fp32 output only: ReLU after bias/residual
 };
 
 // Stage-2 core convolution with a shared-memory-resident X' band (tkd_tc.cu):
@@ -141,6 +143,9 @@ struct BfCoreArgs {
     float *y;                 // Y [B*Ho*Wo][N3]
     int N3, N3p, ncat3;       // output channels, padded (mult. of 16), hi|lo concat in one MMA
     int ksplit;               // >1: split the D1 chunks over a cluster (stage 2 alone, not fused)
+    int y_direct;             // fused stage 3: lanes store their own Y rows (no smem transpose)
+    const float *res;         // fused stage 3: residual [B*Ho*Wo][N3] added before the activation
+    int relu;                 // fused stage 3: ReLU after bias/residual
 };
 int bf_core_smem_bytes(int BN, int nphase, int band_rows, int tg, int w_slots, int ksplit);
 int bf_core3_smem_bytes(const BfCoreArgs &g);

@@ -668,6 +668,8 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         for (int i = 0; i < nphase; ++i) g.phase_src[i] = phase_src[i];
         g.Hq = Hq; g.Wq = Wq; g.Ho = Ho; g.Wo = Wo;
         if (fuse3) {
+            const char *yd = std::getenv("TDC_Y_DIRECT");
+            g.y_direct = yd && yd[0] && yd[0] != '0';
             g.w3 = dB2 + 2 * n2;
             g.bias = dbias;
             g.N3 = N; g.N3p = N3p; g.ncat3 = ncat3;
@@ -696,7 +698,8 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
     return TDC_OK;
 }
 
-tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch, cudaStream_t st) {
+tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch, cudaStream_t st,
+                        const float *res = nullptr, int relu = 0) {
     const tdc::LayerDims &d = p->dims;
     auto &s1 = p->tc[0], &s3 = p->tc[2];
     if (x != p->tc_last_x) {
@@ -709,7 +712,11 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
     a1.M = batch * d.H * d.W;
     a3.M = batch * d.Ho * d.Wo;
     a3.out = y;
+    a3.res = res;
+    a3.relu = relu;
     tdc::BfCoreArgs c = p->bf_core;
+    c.res = res;
+    c.relu = relu;
     c.M = batch * a1.Hq * a1.Wq;
     auto grid = [&](long long M, int ntiles, int smem, int bn) {
         const long long tiles = (long long)div_up((int)M, 128) * ntiles;
@@ -1202,6 +1209,23 @@ tdc_status tdc_conv_forward(tdc_conv_plan_t p, const float *x, float *y, int32_t
     return TDC_OK;
 }
 
+tdc_status tdc_conv_forward_ex(tdc_conv_plan_t p, const float *x, float *y, int32_t batch,
+                               const float *residual, int32_t relu, void *stream) {
+    if (!residual && !relu) return tdc_conv_forward(p, x, y, batch, stream);
+    if (!p) return fail(TDC_ERR_INVALID_ARGUMENT, "plan is NULL");
+    if (!x || !y) return fail(TDC_ERR_INVALID_ARGUMENT, "x/y is NULL");
+    if (batch < 1 || batch > p->desc.batch)
+        return fail(TDC_ERR_INVALID_ARGUMENT, "batch %d outside [1, %d] of this plan", batch, p->desc.batch);
+    if (p->variant != 4 || p->desc.layout != TDC_LAYOUT_NHWC)
+        return fail(TDC_ERR_UNSUPPORTED,
+                    "residual/relu epilogue needs an NHWC plan in TDC_MATH_3XBF16 (this plan: variant %d)",
+                    p->variant);
+    if (residual == y) return fail(TDC_ERR_INVALID_ARGUMENT, "residual must not alias y");
+    DeviceGuard guard(p->device);
+    if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+    return forward_bf16(p, x, y, batch, (cudaStream_t)stream, residual, relu);
+}
+
 tdc_status tdc_conv_forward_host(tdc_conv_plan_t p, const float *x_host, float *y_host,
                                  int32_t batch, void *stream) {
     if (!p) return fail(TDC_ERR_INVALID_ARGUMENT, "plan is NULL");
@@ -1251,3 +1275,20 @@ tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t p) {
 }
 
 }  // extern "C"
+
+// ---- helpers for the model runtime (tdc_model.cu)
+namespace tdc {
+uint16_t bf16_bits(float x) { return bf16_bits_host(x); }
+float bf16_float(uint16_t b) { return bf16_to_float_host(b); }
+tdc_status set_error(tdc_status s, const char *msg) { return fail(s, "%s", msg); }
+int num_sms_of(int device) {
+    int v = 148;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) v = 148;
+    return v;
+}
+int max_smem_of(int device) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess) v = 232448;
+    return v;
+}
+}  // namespace tdc

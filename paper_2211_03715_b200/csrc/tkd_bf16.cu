@@ -44,12 +44,12 @@ extern "C" int tdc_debug_bf_timeline(unsigned long long *host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_tdc_bf_tl, sizeof(unsigned long long) * n);
 }
 #define BFTL(seq, it, ev) bftl((seq), (it), (ev))
-__device__ unsigned long long g_tdc_bfc_tl[64 * 8];
+__device__ unsigned long long g_tdc_bfc_tl[64 * 12];
 __device__ __forceinline__ void bfctl(int it, int ev) {
     if (blockIdx.x == 0 && it < 64) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_tdc_bfc_tl[it * 8 + ev] = t;
+        g_tdc_bfc_tl[it * 12 + ev] = t;
     }
 }
 extern "C" int tdc_debug_bfc_timeline(unsigned long long *host, int n) {
@@ -404,8 +404,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                         *reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(g.out_lo) + off) = l;
                     } else {
                         float *dst = g.out + dst_row * g.ldo + n;
-                        for (int j = 0; j < 8; ++j)
-                            if (g.bias && n + j < g.Nn) v[j] += __ldg(&g.bias[n + j]);
+                        epi_bias_res_relu<8>(v, n, g.Nn, g.bias, g.res ? g.res + dst_row * g.ldo : nullptr, g.relu);
                         if (n + 8 <= g.Nn && (g.ldo & 3) == 0) {
                             st_global_v4(dst, make_float4(v[0], v[1], v[2], v[3]));
                             st_global_v4(dst + 4, make_float4(v[4], v[5], v[6], v[7]));
@@ -442,12 +441,9 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                             *reinterpret_cast<uint4 *>(lo + off) = l;
                         }
                     }
-                } else {  // fp32 Y (+bias), row-major, coalesced through shared memory
-                    if (g.bias) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (n + j < g.Nn) v[j] += __ldg(&g.bias[n + j]);
-                    }
+                } else {  // fp32 Y (+bias, +residual, ReLU), row-major, coalesced through shared memory
+                    epi_bias_res_relu<32>(v, n, g.Nn, g.bias, (g.res && valid) ? g.res + dst_row * g.ldo : nullptr,
+                                          g.relu);
                     float *dst = g.out + dst_row * g.ldo;
                     if (n + 32 <= g.Nn && (g.ldo & 3) == 0) {
                         warp_store_block32(scratch, v, valid ? dst + n : nullptr, lane);
@@ -732,6 +728,16 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         const uint64_t dw3 = sdesc_kmajor_none(smem_u32(w3s), 2 * g.N3p * 16, 128);
         const uint32_t z_lo = zhalf >> 4, b3_lo = (g.N3p * 16) >> 4;
         const int k3 = BN / 16;
+        // Per-tap A start offsets (16-byte units, relative to a band slot), hoisted out of
+        // the tile loop: with the 3x3 core (one group of 9 taps) the tap loop below is
+        // fully unrolled, so each MMA costs one uniform add -- the issuing thread must
+        // keep up with ~48-cycle MMAs.
+        uint32_t aoff9[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i)
+            aoff9[i] = i < g.taps ? ((uint32_t)g.tap_phase[i] * 4 * band_bytes + (uint32_t)g.tap_off[i] * 16) >> 4
+                                  : 0u;
+        const uint32_t wtap16 = w_tap >> 4, plane2a = (2 * band_bytes) >> 4, plane2b = (2 * 2 * BN * 16) >> 4;
         Ring ra(2), rw(WS), acc(2), zr(2), a3(2);
         int tit = 0;
         bool pending = false;  // F3: S3 of the previous tile still to issue
@@ -758,7 +764,31 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                         }
                         tc_fence_after();
                         if (tit == 0 && lane == 0) BFCTAP(kc * g.ngroups + grp, 1);
-                        if (elect_one()) {
+                        if (TG == 9 && g.ngroups == 1) {  // 3x3 core: fully unrolled taps
+                            if (elect_one()) {
+                                const uint64_t aslot = da + ((ra.slot * a_bytes) >> 4);
+                                const uint64_t bslot = db + ((ws * w_slot) >> 4);
+#pragma unroll
+                                for (int tt = 0; tt < 9; ++tt) {
+                                    const uint64_t a = aslot + aoff9[tt];
+                                    const uint64_t b = bslot + tt * wtap16;
+#pragma unroll
+                                    for (int j = 0; j < 2; ++j) {
+                                        const uint64_t aj = a + j * plane2a, bj = b + j * plane2b;
+                                        if (g.ncat) {
+                                            mma_bf16(d, aj, bj, idesc, accum);
+                                            mma_bf16(d, aj + a_lo, bj, idesc, 1);
+                                        } else {
+                                            mma_bf16(d, aj, bj, idesc, accum);
+                                            mma_bf16(d, aj, bj + b_lo, idesc, 1);
+                                            mma_bf16(d, aj + a_lo, bj, idesc, 1);
+                                        }
+                                        accum = 1;
+                                    }
+                                }
+                                if (!resident) mma_commit(&w_empty[ws]);
+                            }
+                        } else if (elect_one()) {
                             for (int tt = 0; tt < TG; ++tt) {
                                 const int tap = grp * TG + tt;
                                 const uint64_t a =
@@ -796,8 +826,10 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             }
             if (F3 && pending) {  // ---- stage 3 of the previous tile
                 mbar_wait(&t3empty[a3.slot], a3.phase ^ 1);
+                if (lane == 0) BFCTL(tit - 1, 6);  // S3: acc3 buffer free
                 mbar_wait(&z_full[zr.slot], zr.phase);
                 tc_fence_after();
+                if (lane == 0) BFCTL(tit - 1, 7);  // S3: Z ready, issuing
                 if (elect_one()) {
                     const uint32_t d3 = tmem + 2 * ncols + a3.slot * ncols3;
                     const uint64_t az = dz + ((zr.slot * zbuf) >> 4);
@@ -938,10 +970,12 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         const int q = warp & 3;
         float *scratch = epi_scratch + q * 1024;
         Ring a3(2);
-        for (int t = cid; t < num_tiles; t += ncl, a3.next()) {
+        int tit = 0;
+        for (int t = cid; t < num_tiles; t += ncl, a3.next(), ++tit) {
             const int m0 = (t % mtiles) * kBM16;
             mbar_wait(&t3full[a3.slot], a3.phase);
             tc_fence_after();
+            if (warp == 6 && lane == 0) BFCTL(tit, 8);  // E3: acc3 ready
             long long dst_row = 0;
             const bool valid = out_row(m0 + q * 32 + lane, &dst_row);
             const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + 2 * ncols + a3.slot * ncols3;
@@ -962,19 +996,24 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
                 }
                 if (c >= g.N3) continue;  // warp-uniform
-                if (g.bias) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (c + j < g.N3) v[j] += __ldg(&g.bias[c + j]);
-                }
+                epi_bias_res_relu<32>(v, c, g.N3, g.bias, (g.res && valid) ? g.res + dst_row * g.N3 : nullptr, g.relu);
                 if (c + 32 <= g.N3 && (g.N3 & 3) == 0) {
-                    warp_store_block32(scratch, v, valid ? dst + c : nullptr, lane);
+                    if (g.y_direct) {  // each lane stores its own row: no shared-memory traffic
+                        if (valid)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+                                st_global_v4(dst + c + 4 * j, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                                                                          v[4 * j + 3]));
+                    } else {
+                        warp_store_block32(scratch, v, valid ? dst + c : nullptr, lane);
+                    }
                 } else if (valid) {
                     for (int j = 0; j < 32 && c + j < g.N3; ++j) dst[c + j] = v[j];
                 }
             }
             tc_fence_before();
             mbar_arrive_relaxed(&t3empty[a3.slot]);
+            if (warp == 6 && lane == 0) BFCTL(tit, 9);  // E3: Y stored
         }
     }
     tc_fence_before();

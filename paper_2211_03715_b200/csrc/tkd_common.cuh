@@ -57,4 +57,26 @@ __device__ __forceinline__ void split_bf16x8(const float *v, uint4 &hi, uint4 &l
                     pack_bf16x2(v[4] - h[4], v[5] - h[5]), pack_bf16x2(v[6] - h[6], v[7] - h[7]));
 }
 
+// Model-path epilogue (tdc_model_*): y = v + bias[n] + residual[row][n], then ReLU.
+// `res_row` points at the residual row (same layout as the output) or is null; the
+// tail beyond nn is left untouched.
+template <int W>
+__device__ __forceinline__ void epi_bias_res_relu(float *v, int n, int nn, const float *bias, const float *res_row,
+                                                  int relu) {
+    if (bias) {
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (n + j < nn) v[j] += __ldg(&bias[n + j]);
+    }
+    if (res_row) {
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (n + j < nn) v[j] += __ldg(&res_row[n + j]);
+    }
+    if (relu) {
+#pragma unroll
+        for (int j = 0; j < W; ++j) v[j] = fmaxf(v[j], 0.f);
+    }
+}
+
 }  // namespace tdc

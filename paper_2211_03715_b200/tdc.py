@@ -25,8 +25,10 @@ MATH_NAMES = {"fp32": TDC_MATH_FP32, "3xtf32": TDC_MATH_3XTF32, "tf32": TDC_MATH
 EXPORTED = [
     "tdc_version", "tdc_status_string", "tdc_last_error", "tdc_conv_output_shape",
     "tdc_conv_plan", "tdc_conv_plan_query", "tdc_conv_forward", "tdc_conv_forward_host",
-    "tdc_conv_plan_destroy",
+    "tdc_conv_plan_destroy", "tdc_conv_forward_ex", "tdc_model_create", "tdc_model_forward",
+    "tdc_model_output_shape", "tdc_model_destroy",
 ]
+TDC_OP_CONV, TDC_OP_TKD, TDC_OP_MAXPOOL, TDC_OP_AVGPOOL, TDC_OP_FC = range(5)
 
 
 class tdc_conv_desc(ctypes.Structure):
@@ -43,6 +45,13 @@ class tdc_plan_info(ctypes.Structure):
                 ("threads_per_cta", ctypes.c_int32), ("smem_bytes_per_cta", ctypes.c_int32),
                 ("ctas_per_image", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
                 ("weight_bytes", ctypes.c_int64)]
+
+
+class tdc_model_op(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "kind", "src", "res", "c_in", "c_out", "height", "width", "kernel", "stride", "pad",
+        "rank_in", "rank_out", "relu")] + [
+        (n, ctypes.POINTER(ctypes.c_float)) for n in ("w", "u_in", "u_out", "bias", "bn")]
 
 
 class TdcError(RuntimeError):
@@ -69,6 +78,12 @@ def _load():
     lib.tdc_conv_forward.argtypes = [vp, vp, vp, i32, vp]
     lib.tdc_conv_forward_host.argtypes = [vp, vp, vp, i32, vp]
     lib.tdc_conv_plan_destroy.argtypes = [vp]
+    lib.tdc_conv_forward_ex.argtypes = [vp, vp, vp, i32, vp, i32, vp]
+    lib.tdc_model_create.argtypes = [ctypes.POINTER(tdc_model_op), i32, i32, i32, ctypes.POINTER(vp)]
+    lib.tdc_model_forward.argtypes = [vp, vp, i32, vp, vp]
+    lib.tdc_model_output_shape.argtypes = [vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32),
+                                           ctypes.POINTER(i32)]
+    lib.tdc_model_destroy.argtypes = [vp]
     for name in EXPORTED:
         getattr(lib, name).restype = getattr(lib, name).restype or ctypes.c_int
     return lib
@@ -207,6 +222,64 @@ class ConvPlan:
     def close(self):
         if getattr(self, "_h", None):
             tdc_conv_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def tdc_conv_forward_ex(plan, x_ptr: int, y_ptr: int, batch: int, res_ptr: int = 0, relu: int = 0,
+                        stream: int = 0) -> None:
+    _check(_lib.tdc_conv_forward_ex(plan, ctypes.c_void_p(x_ptr), ctypes.c_void_p(y_ptr), batch,
+                                    ctypes.c_void_p(res_ptr or None), relu, ctypes.c_void_p(stream)))
+
+
+class Model:
+    """RAII wrapper of tdc_model_*: an op list (dicts as built by ``synth.models``) planned
+    on one device for batches up to ``max_batch``; ``forward(x, out)`` takes NHWC fp32
+    CUDA tensors."""
+
+    def __init__(self, ops: list, max_batch: int, device: int = 0):
+        import numpy as np
+        self._keep = []
+        arr = (tdc_model_op * len(ops))()
+        for i, o in enumerate(ops):
+            a = arr[i]
+            for k in ("kind", "src", "res", "c_in", "c_out", "height", "width", "kernel", "stride", "pad",
+                      "relu"):
+                setattr(a, k, int(o[k]))
+            a.rank_in, a.rank_out = int(o.get("rank_in", 0)), int(o.get("rank_out", 0))
+            for k in ("w", "u_in", "u_out", "bias", "bn"):
+                v = o.get(k)
+                if v is not None:
+                    v = np.ascontiguousarray(v, dtype=np.float32)
+                    self._keep.append(v)
+                setattr(a, k, _fptr(v))
+        self.ops = ops
+        self._h = ctypes.c_void_p()
+        _check(_lib.tdc_model_create(arr, len(ops), max_batch, device, ctypes.byref(self._h)))
+        self.max_batch = max_batch
+        self._keep = None
+
+    def output_shape(self, op: int = -1):
+        h, w, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(_lib.tdc_model_output_shape(self._h, op, ctypes.byref(h), ctypes.byref(w), ctypes.byref(c)))
+        return h.value, w.value, c.value
+
+    def forward(self, x, out, batch: int | None = None, stream=None) -> None:
+        for t, name in ((x, "x"), (out, "out")):
+            if not (t.is_cuda and t.is_contiguous() and str(t.dtype) == "torch.float32"):
+                raise TypeError(f"{name} must be a contiguous float32 CUDA tensor")
+        b = int(x.shape[0]) if batch is None else batch
+        _check(_lib.tdc_model_forward(self._h, ctypes.c_void_p(x.data_ptr()), b, ctypes.c_void_p(out.data_ptr()),
+                                      ctypes.c_void_p(ConvPlan._stream_handle(stream))))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.tdc_model_destroy(self._h)
             self._h = None
 
     def __del__(self):

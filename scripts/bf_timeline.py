@@ -27,17 +27,17 @@ for seq in (2, 3):
     print("tile prod mma_free mma_opnd mma_iss epi_acc epi_done cv_land cv_done")
     for i, r in enumerate(rows[:8]):
         print(i, " ".join(f"{(v - t0) / 1000:7.2f}" if v else "    -  " for v in r))
-n2 = 64 * 8
+n2 = 64 * 12
 buf2 = (ctypes.c_ulonglong * n2)()
 tdc.lib.tdc_debug_bfc_timeline(buf2, n2)
-c = np.array(buf2, dtype=np.int64).reshape(64, 8)
+c = np.array(buf2, dtype=np.int64).reshape(64, 12)
 rows = c[c[:, 1] > 0]
 if len(rows):
     t0 = rows[rows > 0].min()
     print(f"--- core kernel (last launch), CTA 0: tiles {len(rows)}")
-    print("tile band_iss mma_free band_land mma_iss epi_acc epi_done")
+    print("tile band_iss mma_free band_land S2_iss  E2_acc  E2_done S3_free S3_iss  E3_acc  E3_done")
     for i, r in enumerate(rows[:12]):
-        print(i, " ".join(f"{(v - t0) / 1000:7.2f}" if v else "    -  " for v in r[:6]))
+        print(i, " ".join(f"{(v - t0) / 1000:7.2f}" if v else "    -  " for v in r[:10]))
 buf3 = (ctypes.c_ulonglong * 256)()
 tdc.lib.tdc_debug_bfc_taps(buf3, 256)
 tp = np.array(buf3, dtype=np.int64).reshape(128, 2)

@@ -209,6 +209,176 @@ void run_off(long long *d, int off) {
            mx / iters, e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
+// The core kernel's exact MMA pattern: A = X' band planes (no swizzle, LBO = band plane
+// stride 3968 B), per-tap row-shifted start (tap_off = r*58 + t rows), hi/lo halves
+// 63.5 KB apart; B = [hi|lo] weight rows (N = 64, LBO = 1 KB); 2 K16 steps x 2 MMAs per
+// tap, 9 taps, commit per tile.  VAR 0: as the kernel; 1: no row shift; 2: A_hi only.
+template <int VAR>
+__global__ void bench_core(int tiles, long long *out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t slot;
+    for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x)
+        reinterpret_cast<float *>(smem)[i] = 0.001f * (i % 7);
+    const int warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    fence_proxy_async_smem();
+    if (warp == 0) tmem_alloc(&slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    if (threadIdx.x == 0) {
+        const uint32_t band_bytes = 248 * 16, a_half = 4 * band_bytes;
+        const uint64_t da = sdesc_kmajor_none(smem_u32(smem), band_bytes, 128);
+        const uint64_t db = sdesc_kmajor_none(smem_u32(smem + 2 * 2 * a_half), 2 * 32 * 16, 128);
+        const uint32_t id = idesc_bf16(128, 64);
+        long long t0 = clock64();
+        for (int t = 0; t < tiles; ++t) {
+            uint32_t accum = 0;
+            for (int tap = 0; tap < 9; ++tap) {
+                const uint32_t off = VAR == 1 ? 0u : (uint32_t)((tap / 3) * 58 + tap % 3) * 16;
+                const uint64_t a = da + (off >> 4);
+                const uint64_t b = db + ((tap * 32 * 128) >> 4);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const uint64_t aj = a + ((j * 2 * band_bytes) >> 4);
+                    const uint64_t bj = b + ((j * 2 * 2 * 32 * 16) >> 4);
+                    mma_bf16(tmem + (t & 1) * 64, aj, bj, id, accum);
+                    mma_bf16(tmem + (t & 1) * 64, VAR == 2 ? aj : aj + (a_half >> 4), bj, id, 1);
+                    accum = 1;
+                }
+            }
+            mma_commit(&bar);
+        }
+        mbar_wait(&bar, (tiles - 1) & 1);
+        long long t1 = clock64();
+        out[blockIdx.x] = t1 - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// Same MMA stream with interference from 4 other warps: INT 1 = tcgen05.ld x32 loops on
+// other TMEM columns; 2 = ld/st.shared.v4 streams; 3 = both; 4 = 1-D bulk copies
+// (global -> smem, 16 KB) issued by one other warp.
+template <int INT>
+__global__ void bench_core_int(int tiles, long long *out, const uint8_t *gsrc, volatile int *stop) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar, cbar;
+    __shared__ uint32_t slot;
+    __shared__ volatile int done;
+    for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x)
+        reinterpret_cast<float *>(smem)[i] = 0.001f * (i % 7);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_init(&cbar, 1);
+        fence_mbar_init();
+        done = 0;
+    }
+    fence_proxy_async_smem();
+    if (warp == 0) tmem_alloc(&slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = slot;
+    if (threadIdx.x == 0) {
+        const uint32_t band_bytes = 248 * 16, a_half = 4 * band_bytes;
+        const uint64_t da = sdesc_kmajor_none(smem_u32(smem), band_bytes, 128);
+        const uint64_t db = sdesc_kmajor_none(smem_u32(smem + 2 * 2 * a_half), 2 * 32 * 16, 128);
+        const uint32_t id = idesc_bf16(128, 64);
+        long long t0 = clock64();
+        for (int t = 0; t < tiles; ++t) {
+            uint32_t accum = 0;
+            for (int tap = 0; tap < 9; ++tap) {
+                const uint32_t off = (uint32_t)((tap / 3) * 58 + tap % 3) * 16;
+                const uint64_t a = da + (off >> 4);
+                const uint64_t b = db + ((tap * 32 * 128) >> 4);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const uint64_t aj = a + ((j * 2 * band_bytes) >> 4);
+                    const uint64_t bj = b + ((j * 2 * 2 * 32 * 16) >> 4);
+                    mma_bf16(tmem + (t & 1) * 64, aj, bj, id, accum);
+                    mma_bf16(tmem + (t & 1) * 64, aj + (a_half >> 4), bj, id, 1);
+                    accum = 1;
+                }
+            }
+            mma_commit(&bar);
+        }
+        mbar_wait(&bar, (tiles - 1) & 1);
+        long long t1 = clock64();
+        out[blockIdx.x] = t1 - t0;
+        done = 1;
+    } else if (warp >= 4 && warp < 8) {
+        const int q = warp & 3;
+        float acc = 0.f;
+        uint32_t it = 0;
+        while (!done) {
+            if (INT & 1) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + 256 + (it & 3) * 32, r);
+                tmem_ld_wait();
+                acc += __uint_as_float(r[lane & 31]);
+            }
+            if (INT & 2) {
+                const uint32_t base = smem_u32(smem + 150 * 1024) + (uint32_t)((q * 32 + lane) * 16);
+                float4 v = ld_shared_v4(base + (it & 7) * 2048);
+                st_shared_v4(base + ((it + 3) & 7) * 2048, v.x + 1.f, v.y, v.z, v.w);
+                acc += v.x;
+            }
+            if (INT == 4 && warp == 4 && lane == 0) {
+                mbar_arrive_expect_tx(&cbar, 16384);
+                bulk_load(smem + 160 * 1024, gsrc + (size_t)((blockIdx.x * 131 + it) & 1023) * 16384, 16384, &cbar);
+                mbar_wait(&cbar, it & 1);
+            }
+            ++it;
+        }
+        if (acc == 12345.f) out[1000] = 1;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int INT>
+void run_core_int(long long *d, const uint8_t *g) {
+    auto k = bench_core_int<INT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 201 * 1024);
+    const int tiles = 64, grid = 148;
+    k<<<grid, 256, 201 * 1024>>>(tiles, d, g, nullptr);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h[512];
+    cudaMemcpy(h, d, 8 * grid, cudaMemcpyDeviceToHost);
+    double mx = 0;
+    for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
+    printf("core pattern + interference %d: %7.1f cyc/tile  %6.1f cyc/mma %s\\n", INT, mx / tiles, mx / tiles / 36,
+           e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
+template <int VAR>
+void run_core(long long *d) {
+    auto k = bench_core<VAR>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 201 * 1024);
+    const int tiles = 64, grid = 148;
+    k<<<grid, 128, 201 * 1024>>>(tiles, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h[512];
+    cudaMemcpy(h, d, 8 * grid, cudaMemcpyDeviceToHost);
+    double mx = 0;
+    for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
+    printf("core pattern VAR %d: %7.1f cyc/tile  %6.1f cyc/mma %s\n", VAR, mx / tiles, mx / tiles / 36,
+           e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
 template <int BF, int M, int N, int TS, int ELECT>
 void run(long long *d, int ctas_per_sm) {
     auto k = ctas_per_sm == 1 ? bench<BF, M, N, TS, ELECT, 512> : bench<BF, M, N, TS, ELECT, 256>;
@@ -235,6 +405,16 @@ int main() {
     cudaMalloc(&d, 8 * 512);
 #define ALLN(BF, M, TS, E) run<BF, M, 32, TS, E>(d, 1); run<BF, M, 64, TS, E>(d, 1); \
     run<BF, M, 128, TS, E>(d, 1); run<BF, M, 256, TS, E>(d, 1);
+    run_core<0>(d); run_core<1>(d); run_core<2>(d);
+    {
+        uint8_t *g;
+        cudaMalloc(&g, 17 << 20);
+        cudaMemset(g, 0, 17 << 20);
+        long long *d2;
+        cudaMalloc(&d2, 8 * 1024);
+        run_core_int<0>(d2, g); run_core_int<1>(d2, g); run_core_int<2>(d2, g); run_core_int<3>(d2, g);
+        run_core_int<4>(d2, g);
+    }
     for (int off : {0, 16, 32, 48, 64, 112}) run_off<32, 1>(d, off);
     for (int off : {0, 16, 32, 64}) run_off<64, 1>(d, off);
     for (int off : {0, 16, 64}) run_off<128, 1>(d, off);

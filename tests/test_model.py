@@ -1,0 +1,143 @@
+"""Whole-model path: the fp64 model oracle pinned against torch
+fp64 reference ops, and (GPU) Tucker ResNet-18/-50 through tdc_model_forward against it.
+
+Model tolerance (reading R19): max-normalized error <= 1e-3 on the model
+output -- every TKD / dense layer is fp32-grade (3xBF16, <= 1e-4 each) and the error
+compounds over up to 54 layers."""
+import numpy as np
+import pytest
+
+import oracle
+import oracle.model as om
+import synth
+import synth.models as sm
+
+MODEL_TOL = 1e-3
+
+
+def torch_ref(ops, x_nhwc):
+    """Independent fp64 reference of the op list with torch.nn.functional."""
+    import torch
+    import torch.nn.functional as F
+    acts = {0: torch.from_numpy(np.transpose(x_nhwc, (0, 3, 1, 2)).astype(np.float64))}
+    for i, o in enumerate(ops):
+        x = acts[o["src"]]
+        k = o["kind"]
+        if k == sm.OP_CONV:
+            y = F.conv2d(x, torch.from_numpy(o["w"].astype(np.float64)), stride=o["stride"], padding=o["pad"])
+        elif k == sm.OP_TKD:
+            w = np.einsum("nq,qart,ca->ncrt", o["u_out"].astype(np.float64), o["w"].astype(np.float64),
+                          o["u_in"].astype(np.float64))
+            y = F.conv2d(x, torch.from_numpy(w), stride=o["stride"], padding=o["pad"])
+        elif k == sm.OP_MAXPOOL:
+            y = F.max_pool2d(x, o["kernel"], o["stride"], o["pad"])
+        elif k == sm.OP_AVGPOOL:
+            y = F.adaptive_avg_pool2d(x, 1)
+        else:
+            y = F.linear(x.flatten(1), torch.from_numpy(o["w"].astype(np.float64)))[:, :, None, None]
+        if k in (sm.OP_CONV, sm.OP_TKD, sm.OP_FC):
+            if o.get("bias") is not None:
+                y = y + torch.from_numpy(o["bias"].astype(np.float64))[None, :, None, None]
+            if o.get("bn") is not None:
+                g, b, m, v = (torch.from_numpy(a.astype(np.float64)) for a in o["bn"])
+                y = F.batch_norm(y, m, v, g, b, training=False, eps=1e-5)
+            if o.get("res", -1) >= 0:
+                y = y + acts[o["res"]]
+            if o.get("relu"):
+                y = torch.relu(y)
+        acts[i + 1] = y
+    return np.transpose(acts[len(ops)].numpy(), (0, 2, 3, 1))
+
+
+def maxerr(got, ref):
+    return float(np.max(np.abs(np.asarray(got, np.float64) - ref)) / np.max(np.abs(ref)))
+
+
+@pytest.mark.parametrize("depth", [18, 50])
+def test_model_oracle_against_torch(depth):
+    ops = sm.tucker_resnet(depth, image=32, num_classes=10, width=8)
+    x = sm.model_input(2, 32)
+    assert maxerr(om.forward(ops, x), torch_ref(ops, x)) < 1e-12
+
+
+def test_model_oracle_pool_semantics():
+    x = np.arange(2 * 5 * 5 * 3, dtype=np.float64).reshape(2, 3, 5, 5) - 40
+    y = om.maxpool(x, 3, 2, 1)
+    assert y.shape == (2, 3, 3, 3)
+    assert y[0, 0, 0, 0] == max(x[0, 0, 0, 0], x[0, 0, 0, 1], x[0, 0, 1, 0], x[0, 0, 1, 1])  # padding never wins
+    assert y[1, 2, 2, 2] == x[1, 2, 4, 4]
+
+
+def test_builder_geometry_and_ranks():
+    ops = sm.tucker_resnet(18)
+    tkd = [o for o in ops if o["kind"] == sm.OP_TKD]
+    assert len(tkd) == 16 and all(o["rank_in"] == o["c_in"] // 2 for o in tkd)   # paper-style r = 1/2
+    ops50 = sm.tucker_resnet(50)
+    assert sum(o["kind"] == sm.OP_TKD for o in ops50) == 16
+    assert sum(o["kind"] == sm.OP_CONV and o["kernel"] == 1 for o in ops50) == 36  # 32 + 4 downsample
+    assert ops50[-1]["kind"] == sm.OP_FC and ops50[-1]["c_out"] == 1000
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2211_03715_b200 import tdc
+    return torch, tdc
+
+
+def run_model(gpu, ops, x, batch=None):
+    torch, tdc = gpu
+    m = tdc.Model(ops, max_batch=x.shape[0])
+    h, w, c = m.output_shape()
+    b = x.shape[0] if batch is None else batch
+    xd = torch.from_numpy(x).cuda()
+    out = torch.full((x.shape[0], h, w, c), float("nan"), device="cuda")
+    m.forward(xd, out, batch=b)
+    torch.cuda.synchronize()
+    m.close()
+    return out.cpu().numpy()[:b]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("depth,width,image", [(18, 16, 32), (50, 16, 32), (18, 32, 64)])
+def test_small_tucker_resnet(gpu, depth, width, image):
+    ops = sm.tucker_resnet(depth, image=image, num_classes=37, width=width, seed=7)
+    x = sm.model_input(3, image, seed=7)
+    assert maxerr(run_model(gpu, ops, x), om.forward(ops, x)) <= MODEL_TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("depth", [18, 50])
+def test_full_tucker_resnet_224(gpu, depth):
+    """BASELINE config 3 architecture at full size (224 x 224 x 3, 1000 classes)."""
+    ops = sm.tucker_resnet(depth)
+    x = sm.model_input(2, 224)
+    got = run_model(gpu, ops, x)
+    assert got.shape == (2, 1, 1, 1000)
+    assert maxerr(got, om.forward(ops, x)) <= MODEL_TOL
+
+
+@pytest.mark.gpu
+def test_model_partial_batch_and_determinism(gpu):
+    ops = sm.tucker_resnet(18, image=32, num_classes=10, width=16)
+    x = sm.model_input(4, 32)
+    full = run_model(gpu, ops, x)
+    part = run_model(gpu, ops, x, batch=2)
+    assert np.array_equal(full[:2], part)
+    assert np.array_equal(full, run_model(gpu, ops, x))
+
+
+@pytest.mark.gpu
+def test_model_rejects_bad_graphs(gpu):
+    torch, tdc = gpu
+    ops = sm.tucker_resnet(18, image=32, num_classes=10, width=16)
+    bad = [dict(o) for o in ops]
+    bad[3]["src"] = 7            # refers to a later op
+    with pytest.raises(tdc.TdcError):
+        tdc.Model(bad, 2)
+    bad = [dict(o) for o in ops]
+    bad[2]["c_in"] += 4          # geometry mismatch with its source
+    with pytest.raises(tdc.TdcError):
+        tdc.Model(bad, 2)
