@@ -344,16 +344,15 @@ def impl_tdc(args):
                  "timing": "layer alone, back-to-back forwards between CUDA events on the launching stream, "
                            "inputs rotated over > 2x L2"})
 
-    # ---- Tucker ResNet-50 whole-model inference (BASELINE metric part 2, config 3):
-    # each rank runs the full model on its own batch shard (weak scaling, no collective
-    # beyond the timing barrier); images/s = all ranks' images / max-over-ranks time.
-    model = None
-    if not args.no_model:
-        import synth.models as sm
-        ops = sm.tucker_resnet(50, seed=synth.BASE_SEED + 1000 * rank)
-        mb = args.model_batch
+    # ---- whole-model inference (BASELINE metric part 2): Tucker ResNet-50 (config 3,
+    # batch 32 per GPU, weak scaling) and Tucker VGG-16 (config 4, global batch 64
+    # sharded over the ranks, strong scaling).  Each rank runs the whole model on its own
+    # shard (no collective beyond the timing barrier); images/s = all ranks' images /
+    # max-over-ranks time.
+    def time_model(ops, mb):
         net = tdc.Model(ops, max_batch=mb, device=local)
         mh, mw, mc = net.output_shape()
+        import synth.models as sm
         mx = torch.from_numpy(sm.model_input(mb, 224, seed=synth.BASE_SEED + rank)).cuda()
         mo = torch.empty((mb, mh, mw, mc), device="cuda")
         with torch.cuda.stream(stream):
@@ -380,12 +379,27 @@ def impl_tdc(args):
         torch.cuda.synchronize()
         tdist.barrier()
         mms = tdist.max_over_ranks(m0.elapsed_time(m1), "cuda") / args.steps
-        model = {"arch": "tucker_resnet50", "ranks": "paper-style r = 1/4 (D = C/4) on every 3x3 conv",
-                 "input": "224x224x3 synthetic, NHWC fp32", "math": "3xbf16 (fp32-grade)",
-                 "batch_per_gpu": mb, "n_gpus": world, "ms_per_batch": round(mms, 4),
-                 "images_per_s": round(mb * world / (mms * 1e-3), 1),
-                 "launch": "cuda_graph_replay" if mgraph is not None else "stream_launches"}
         net.close()
+        del mgraph
+        return mms, "cuda_graph_replay" if mgraph is not None else "stream_launches"
+
+    model = None
+    if not args.no_model:
+        import synth.models as sm
+        mb = args.model_batch
+        mms, how = time_model(sm.tucker_resnet(50, seed=synth.BASE_SEED + 1000 * rank), mb)
+        model = {"tucker_resnet50": {
+            "ranks": "paper-style r = 1/4 (D = C/4) on every 3x3 conv", "input": "224x224x3 synthetic, NHWC fp32",
+            "math": "3xbf16 (fp32-grade)", "batch_per_gpu": mb, "global_batch": mb * world, "n_gpus": world,
+            "scaling": "weak", "ms_per_batch": round(mms, 4), "images_per_s": round(mb * world / (mms * 1e-3), 1),
+            "launch": how}}
+        vb = max(1, 64 // world)
+        vms, how = time_model(sm.tucker_vgg16(seed=synth.BASE_SEED + 1000 * rank), vb)
+        model["tucker_vgg16"] = {
+            "ranks": "paper-style r = 3/8 on the 12 3x3 convs after the first", "input": "224x224x3 synthetic",
+            "math": "3xbf16 (fp32-grade)", "batch_per_gpu": vb, "global_batch": vb * world, "n_gpus": world,
+            "scaling": "strong (global batch 64 sharded)", "ms_per_batch": round(vms, 4),
+            "images_per_s": round(vb * world / (vms * 1e-3), 1), "launch": how}
 
     # ---- end to end through the host-buffer C-ABI call ----
     e2e = None

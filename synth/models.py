@@ -118,6 +118,30 @@ def tucker_resnet(depth: int = 18, image: int = 224, num_classes: int = 1000, ra
     return b.ops
 
 
+def tucker_vgg16(image: int = 224, num_classes: int = 1000, ratio: float = 3 / 8, seed: int = 42,
+                 width: int = 64, hidden: int = 4096):
+    """Op list of a Tucker VGG-16 (BN variant): the first 3x3 conv dense, the other 12
+    TKD with r = 3/8 (reading A15); classifier = a dense (image/32) x (image/32) conv
+    (FC1 on the flattened NHWC feature map), FC2, FC3."""
+    b = _Builder(seed, image, image, 3)
+    cfg = [1, 1, "M", 2, 2, "M", 4, 4, 4, "M", 8, 8, 8, "M", 8, 8, 8, "M"]
+    x, first = 0, True
+    for v in cfg:
+        if v == "M":
+            x = b.maxpool(x, 2, 2, 0)
+            continue
+        x = b.conv(x, width * v, 3, 1, 1, tkd_ratio=None if first else ratio)
+        first = False
+    h, _, _ = b.geo[x]
+    x = b.conv(x, hidden, h, 1, 0)                       # FC1 as a valid conv over the feature map
+    b.ops[-1]["bn"] = None
+    b.ops[-1]["bias"] = _rng(seed, len(b.ops) - 1, 4).uniform(-0.1, 0.1, hidden).astype(np.float32)
+    x = b.fc(x, hidden)
+    b.ops[-1]["relu"] = 1
+    b.fc(x, num_classes)
+    return b.ops
+
+
 def model_input(batch: int, image: int = 224, seed: int = 42) -> np.ndarray:
     """Synthetic ImageNet-shaped input, NHWC fp32 ~ N(0, 1) (normalised pixels)."""
     return np.random.Generator(np.random.PCG64(seed + 999_999)).standard_normal(

@@ -53,9 +53,10 @@ def maxerr(got, ref):
     return float(np.max(np.abs(np.asarray(got, np.float64) - ref)) / np.max(np.abs(ref)))
 
 
-@pytest.mark.parametrize("depth", [18, 50])
-def test_model_oracle_against_torch(depth):
-    ops = sm.tucker_resnet(depth, image=32, num_classes=10, width=8)
+@pytest.mark.parametrize("arch", ["r18", "r50", "vgg16"])
+def test_model_oracle_against_torch(arch):
+    ops = (sm.tucker_vgg16(image=32, num_classes=10, width=8, hidden=64) if arch == "vgg16"
+           else sm.tucker_resnet(18 if arch == "r18" else 50, image=32, num_classes=10, width=8))
     x = sm.model_input(2, 32)
     assert maxerr(om.forward(ops, x), torch_ref(ops, x)) < 1e-12
 
@@ -74,6 +75,9 @@ def test_builder_geometry_and_ranks():
     assert len(tkd) == 16 and all(o["rank_in"] == o["c_in"] // 2 for o in tkd)   # paper-style r = 1/2
     ops50 = sm.tucker_resnet(50)
     assert sum(o["kind"] == sm.OP_TKD for o in ops50) == 16
+    vgg = sm.tucker_vgg16()
+    assert sum(o["kind"] == sm.OP_TKD for o in vgg) == 12
+    assert all(o["rank_in"] == -(-3 * o["c_in"] // 8) for o in vgg if o["kind"] == sm.OP_TKD)
     assert sum(o["kind"] == sm.OP_CONV and o["kernel"] == 1 for o in ops50) == 36  # 32 + 4 downsample
     assert ops50[-1]["kind"] == sm.OP_FC and ops50[-1]["c_out"] == 1000
 
@@ -117,6 +121,21 @@ def test_full_tucker_resnet_224(gpu, depth):
     got = run_model(gpu, ops, x)
     assert got.shape == (2, 1, 1, 1000)
     assert maxerr(got, om.forward(ops, x)) <= MODEL_TOL
+
+
+@pytest.mark.gpu
+def test_small_tucker_vgg16(gpu):
+    ops = sm.tucker_vgg16(image=64, num_classes=21, width=16, hidden=128, seed=3)
+    x = sm.model_input(3, 64, seed=3)
+    assert maxerr(run_model(gpu, ops, x), om.forward(ops, x)) <= MODEL_TOL
+
+
+@pytest.mark.gpu
+def test_full_tucker_vgg16_224(gpu):
+    """BASELINE config 4 architecture at full size (one image per shard)."""
+    ops = sm.tucker_vgg16()
+    x = sm.model_input(1, 224, seed=5)
+    assert maxerr(run_model(gpu, ops, x), om.forward(ops, x)) <= MODEL_TOL
 
 
 @pytest.mark.gpu
