@@ -379,9 +379,10 @@ def impl_tdc(args):
         torch.cuda.synchronize()
         tdist.barrier()
         mms = tdist.max_over_ranks(m0.elapsed_time(m1), "cuda") / args.steps
+        how = "cuda_graph_replay" if mgraph is not None else "stream_launches"
+        mgraph = None
         net.close()
-        del mgraph
-        return mms, "cuda_graph_replay" if mgraph is not None else "stream_launches"
+        return mms, how
 
     model = None
     if not args.no_model:

@@ -436,6 +436,19 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         ks1 = split_pick(M1, D1s, 64, C64 / 64, &BN1);
         ks3 = split_pick(M3, N, 128, D2p / 64, &BN3);
     }
+    // narrow N tiles until the GEMM kernels' rings fit shared memory (stage 1 also holds
+    // the fp32 staging ring: BN <= 128 there)
+    for (;;) {
+        int xs = 0, bs = 0;
+        const int st = tdc::bf_pick_stages(BN1, p->max_smem, 1, &xs, ks1, &bs);
+        if (BN1 <= 32 || tdc::bf_smem_bytes(BN1, st, xs, ks1, bs) <= p->max_smem) break;
+        BN1 /= 2;
+    }
+    for (;;) {
+        const int st = tdc::bf_pick_stages(BN3, p->max_smem, 0, nullptr, ks3, nullptr);
+        if (BN3 <= 32 || tdc::bf_smem_bytes(BN3, st, 0, ks3, 0) <= p->max_smem) break;
+        BN3 /= 2;
+    }
     const int KK = K * K;
     const int maxoff = ((K - 1) / s) * Wq + (K - 1) / s;
     const int band_rows = round_up(128 + maxoff, 8);

@@ -242,3 +242,17 @@ def test_3xbf16_split_k_matches_unsplit(env, shape, monkeypatch):
     c, _ = run_layer(env, s, d, "nhwc", "3xbf16")
     ref = ref_of(s, d)
     assert err(a, ref) <= TOL["3xbf16"] and err(c, ref) <= TOL["3xbf16"]
+
+
+@pytest.mark.parametrize("shape", [LayerShape(16, 512, 512, 28, 28, 192, 192, 3, 1, 1, "28x28_512_D192_b16")],
+                         ids=lambda s: s.name)
+def test_3xbf16_wide_rank_large_m(env, shape):
+    """Large M with D1 = D2 = 192: the stage-1 N tile must shrink until its rings fit
+    shared memory (a Tucker VGG-16 28x28x512 layer at batch 64 hit this).  Sampled
+    outputs against the oracle evaluated point by point."""
+    d = synth.make_layer(shape, seed=9)
+    got, _ = run_layer(env, shape, d, "nhwc", "3xbf16")
+    pts = synth.sample_points(shape, 200, seed=1)
+    ref = oracle.tkd_points(d["x"], d["core"], d["u_in"], d["u_out"], pts, None, shape.stride, shape.pad)
+    vals = np.array([got[p] for p in pts], dtype=np.float64)
+    assert np.max(np.abs(vals - ref)) / np.max(np.abs(ref)) <= TOL["3xbf16"]
