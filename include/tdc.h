@@ -87,7 +87,24 @@ typedef struct {
     int64_t ctas_per_image;        /* CTAs launched per image by the main kernel       */
     int64_t workspace_bytes;       /* device bytes owned by the plan beyond weights    */
     int64_t weight_bytes;          /* packed device weight bytes                       */
+    /* TDC_MATH_3XBF16 tile choices (0 elsewhere): N tile of stage 1 / the core / stage 3,
+     * cluster split-K sizes, 1 if stage 3 is fused into the core kernel */
+    int32_t bn_stage1, bn_core, bn_stage3;
+    int32_t ksplit_stage1, ksplit_core, ksplit_stage3;
+    int32_t core3;
 } tdc_plan_info;
+
+/* Planner overrides for TDC_MATH_3XBF16 (the analytical planner
+ * vs exhaustive measured autotune).  -1 / 0 = the planner's own choice.  Requested N
+ * tiles (32/64/128/256) are narrowed if they do not fit shared memory / TMEM; a
+ * requested fusion that does not fit falls back to the unfused kernels; split-K
+ * sizes are clamped to [1, 4] and to the number of K chunks.  The chosen values are
+ * reported by tdc_conv_plan_query. */
+typedef struct {
+    int32_t core3;                         /* -1 auto, 0 never, 1 when it fits      */
+    int32_t bn_stage1, bn_core, bn_stage3; /* 0 auto                               */
+    int32_t ksplit_stage1, ksplit_core, ksplit_stage3; /* 0 auto, 1 off, 2..4     */
+} tdc_plan_hints;
 
 const char *tdc_version(void);
 const char *tdc_status_string(tdc_status s);
@@ -108,6 +125,12 @@ tdc_status tdc_conv_plan(const tdc_conv_desc *desc, const float *core,
                          const float *bias, int32_t device, tdc_conv_plan_t *out);
 
 tdc_status tdc_conv_plan_query(tdc_conv_plan_t plan, tdc_plan_info *info);
+
+/* tdc_conv_plan with planner overrides (hints may be NULL = tdc_conv_plan). */
+tdc_status tdc_conv_plan_ex(const tdc_conv_desc *desc, const float *core,
+                            const float *u_in, const float *u_out, const float *bias,
+                            const tdc_plan_hints *hints, int32_t device,
+                            tdc_conv_plan_t *out);
 
 /* Forward (§8(a) rows a1-a4), asynchronous on `stream` (a cudaStream_t; NULL =
  * legacy default stream).  x: DEVICE fp32, batch x C x H x W in desc.layout;

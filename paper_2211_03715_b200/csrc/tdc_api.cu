@@ -126,6 +126,7 @@ struct tdc_conv_plan_s {
     tdc::TcCoreArgs core_args;
     tdc::BfCoreArgs bf_core;
     bool fuse3 = false;            // 3xBF16: core + stage 3 in one kernel (Z on chip)
+    tdc_plan_hints hints = {-1, 0, 0, 0, 0, 0, 0};  // planner overrides (tdc_conv_plan_ex)
     float *d_tc_w = nullptr;       // Bt1 | Bt2 | Bt3 | bias
     float *d_xg = nullptr;         // X' phase grids (zero borders)
     float *d_z = nullptr;          // Z compact
@@ -436,6 +437,18 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         ks1 = split_pick(M1, D1s, 64, C64 / 64, &BN1);
         ks3 = split_pick(M3, N, 128, D2p / 64, &BN3);
     }
+    {   // planner overrides (tdc_conv_plan_ex; NEXT-3 autotune)
+        const tdc_plan_hints &h = p->hints;
+        auto pow2 = [](int v) {
+            int b = 32;
+            while (b < v && b < 256) b *= 2;
+            return b;
+        };
+        if (h.bn_stage1 > 0) BN1 = pow2(h.bn_stage1);
+        if (h.bn_stage3 > 0) BN3 = pow2(h.bn_stage3);
+        if (h.ksplit_stage1 > 0) ks1 = std::max(1, std::min({h.ksplit_stage1, 4, C64 / 64}));
+        if (h.ksplit_stage3 > 0) ks3 = std::max(1, std::min({h.ksplit_stage3, 4, D2p / 64}));
+    }
     // narrow N tiles until the GEMM kernels' rings fit shared memory (stage 1 also holds
     // the fp32 staging ring: BN <= 128 there)
     for (;;) {
@@ -477,7 +490,8 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
     int fuse3 = 0;
     {
         const char *ev = std::getenv("TDC_NO_FUSE3");
-        const bool off = ev && ev[0] && ev[0] != '0';
+        const bool off = (ev && ev[0] && ev[0] != '0') || p->hints.core3 == 0 ||
+                         (p->hints.bn_core > 0 && p->hints.bn_core < D2s) || p->hints.ksplit_core > 1;
         int bn = 32;
         while (bn < D2s) bn *= 2;
         if (!off && bn <= 128 && (ncat3 ? 2 * N3p : N3p) <= 256) {
@@ -537,6 +551,14 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
                 }
             }
         }
+    }
+    if (!fuse3) {
+        const tdc_plan_hints &h = p->hints;
+        if (h.bn_core > 0) {
+            BN2 = 32;
+            while (BN2 < h.bn_core && BN2 < 256) BN2 *= 2;
+        }
+        if (h.ksplit_core > 0) ks2 = std::max(1, std::min({h.ksplit_core, 4, k2chunks}));
     }
     for (; !fuse3 && BN2 >= 32; BN2 /= 2) {
         nt2 = div_up(D2s, BN2);
@@ -1008,6 +1030,12 @@ tdc_status tdc_conv_output_shape(const tdc_conv_desc *desc, int32_t *h_out, int3
 tdc_status tdc_conv_plan(const tdc_conv_desc *desc, const float *core, const float *u_in,
                          const float *u_out, const float *bias, int32_t device,
                          tdc_conv_plan_t *out) {
+    return tdc_conv_plan_ex(desc, core, u_in, u_out, bias, nullptr, device, out);
+}
+
+tdc_status tdc_conv_plan_ex(const tdc_conv_desc *desc, const float *core, const float *u_in,
+                            const float *u_out, const float *bias, const tdc_plan_hints *hints,
+                            int32_t device, tdc_conv_plan_t *out) {
     if (!out) return fail(TDC_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;
     int ho, wo;
@@ -1034,6 +1062,7 @@ tdc_status tdc_conv_plan(const tdc_conv_desc *desc, const float *core, const flo
     if (!p) return fail(TDC_ERR_OUT_OF_MEMORY, "host allocation of plan failed");
     p->desc = *desc;
     p->device = device;
+    if (hints) p->hints = *hints;
     const tdc_conv_desc &d = *desc;
     p->dims = tdc::LayerDims{d.batch, d.c_in, d.height, d.width, d.c_out, d.kernel,
                              d.stride, d.pad, ho, wo};
@@ -1159,6 +1188,13 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
     }
     if (p->variant == 4) {  // stage-2 (core) kernel geometry
         const tdc::BfCoreArgs &c = p->bf_core;
+        info->bn_stage1 = p->tc[0].args.BN;
+        info->ksplit_stage1 = std::max(1, p->tc[0].args.ksplit);
+        info->bn_core = c.BN;
+        info->ksplit_core = std::max(1, c.ksplit);
+        info->bn_stage3 = p->fuse3 ? c.N3p : p->tc[2].args.BN;
+        info->ksplit_stage3 = p->fuse3 ? 1 : std::max(1, p->tc[2].args.ksplit);
+        info->core3 = p->fuse3 ? 1 : 0;
         info->tile_w = c.BN;
         info->threads_per_cta = p->fuse3 ? 320 : 192;
         info->smem_bytes_per_cta = p->fuse3 ? tdc::bf_core3_smem_bytes(c)

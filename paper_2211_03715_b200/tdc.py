@@ -26,7 +26,7 @@ EXPORTED = [
     "tdc_version", "tdc_status_string", "tdc_last_error", "tdc_conv_output_shape",
     "tdc_conv_plan", "tdc_conv_plan_query", "tdc_conv_forward", "tdc_conv_forward_host",
     "tdc_conv_plan_destroy", "tdc_conv_forward_ex", "tdc_model_create", "tdc_model_forward",
-    "tdc_model_output_shape", "tdc_model_destroy",
+    "tdc_model_output_shape", "tdc_model_destroy", "tdc_conv_plan_ex",
 ]
 TDC_OP_CONV, TDC_OP_TKD, TDC_OP_MAXPOOL, TDC_OP_AVGPOOL, TDC_OP_FC = range(5)
 
@@ -44,7 +44,16 @@ class tdc_plan_info(ctypes.Structure):
                 ("tile_h", ctypes.c_int32), ("tile_w", ctypes.c_int32),
                 ("threads_per_cta", ctypes.c_int32), ("smem_bytes_per_cta", ctypes.c_int32),
                 ("ctas_per_image", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
-                ("weight_bytes", ctypes.c_int64)]
+                ("weight_bytes", ctypes.c_int64)] + [(n, ctypes.c_int32) for n in (
+                    "bn_stage1", "bn_core", "bn_stage3", "ksplit_stage1", "ksplit_core", "ksplit_stage3",
+                    "core3")]
+
+
+HINT_FIELDS = ("core3", "bn_stage1", "bn_core", "bn_stage3", "ksplit_stage1", "ksplit_core", "ksplit_stage3")
+
+
+class tdc_plan_hints(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in HINT_FIELDS]
 
 
 class tdc_model_op(ctypes.Structure):
@@ -79,6 +88,8 @@ def _load():
     lib.tdc_conv_forward_host.argtypes = [vp, vp, vp, i32, vp]
     lib.tdc_conv_plan_destroy.argtypes = [vp]
     lib.tdc_conv_forward_ex.argtypes = [vp, vp, vp, i32, vp, i32, vp]
+    lib.tdc_conv_plan_ex.argtypes = [desc_p, fp, fp, fp, fp, ctypes.POINTER(tdc_plan_hints), i32,
+                                     ctypes.POINTER(vp)]
     lib.tdc_model_create.argtypes = [ctypes.POINTER(tdc_model_op), i32, i32, i32, ctypes.POINTER(vp)]
     lib.tdc_model_forward.argtypes = [vp, vp, i32, vp, vp]
     lib.tdc_model_output_shape.argtypes = [vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32),
@@ -138,6 +149,23 @@ def tdc_conv_plan(desc: tdc_conv_desc, core, u_in, u_out, bias=None, device: int
     return h
 
 
+def make_hints(**kw) -> tdc_plan_hints:
+    """Planner overrides; unspecified fields = the planner's own choice."""
+    h = tdc_plan_hints(core3=-1)
+    for k, v in kw.items():
+        if k not in HINT_FIELDS:
+            raise KeyError(k)
+        setattr(h, k, int(v))
+    return h
+
+
+def tdc_conv_plan_ex(desc: tdc_conv_desc, core, u_in, u_out, bias=None, hints=None, device: int = 0):
+    h = ctypes.c_void_p()
+    _check(_lib.tdc_conv_plan_ex(ctypes.byref(desc), _fptr(core), _fptr(u_in), _fptr(u_out), _fptr(bias),
+                                 ctypes.byref(hints) if hints is not None else None, device, ctypes.byref(h)))
+    return h
+
+
 def tdc_conv_plan_query(plan) -> tdc_plan_info:
     info = tdc_plan_info()
     _check(_lib.tdc_conv_plan_query(plan, ctypes.byref(info)))
@@ -175,6 +203,13 @@ class PlanInfo:
     ctas_per_image: int
     workspace_bytes: int
     weight_bytes: int
+    bn_stage1: int = 0
+    bn_core: int = 0
+    bn_stage3: int = 0
+    ksplit_stage1: int = 0
+    ksplit_core: int = 0
+    ksplit_stage3: int = 0
+    core3: int = 0
 
 
 class ConvPlan:
@@ -184,21 +219,22 @@ class ConvPlan:
     enqueues the kernels on ``stream`` (a torch.cuda.Stream or raw handle)."""
 
     def __init__(self, shape, weights: dict, layout: int = TDC_LAYOUT_NHWC,
-                 math: int = TDC_MATH_FP32, device: int = 0):
+                 math: int = TDC_MATH_FP32, device: int = 0, hints: dict | None = None):
         self.shape = shape
         self.desc = make_desc(shape.B, shape.C, shape.H, shape.W, shape.N, shape.D1,
                               shape.D2, shape.K, shape.stride, shape.pad, layout, math)
         self.layout = layout
         self.device = device
-        self._h = tdc_conv_plan(self.desc, weights["core"], weights["u_in"], weights["u_out"],
-                                weights.get("bias"), device)
+        self._h = tdc_conv_plan_ex(self.desc, weights["core"], weights["u_in"], weights["u_out"],
+                                   weights.get("bias"), make_hints(**hints) if hints else None, device)
 
     def info(self) -> PlanInfo:
         i = tdc_conv_plan_query(self._h)
         return PlanInfo(i.h_out, i.w_out, i.variant, i.variant_name.decode(),
                         i.launches_per_forward, i.concurrent_forward, i.tile_h, i.tile_w,
                         i.threads_per_cta, i.smem_bytes_per_cta, i.ctas_per_image,
-                        i.workspace_bytes, i.weight_bytes)
+                        i.workspace_bytes, i.weight_bytes, i.bn_stage1, i.bn_core, i.bn_stage3,
+                        i.ksplit_stage1, i.ksplit_core, i.ksplit_stage3, i.core3)
 
     @staticmethod
     def _stream_handle(stream) -> int:
