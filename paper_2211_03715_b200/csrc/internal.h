@@ -146,6 +146,8 @@ struct BfCoreArgs {
     int y_direct;             // fused stage 3: lanes store their own Y rows (no smem transpose)
     const float *res;         // fused stage 3: residual [B*Ho*Wo][N3] added before the activation
     int relu;                 // fused stage 3: ReLU after bias/residual
+    int dbg;                  // debug (TDC_CORE_DBG): 1 skip Y stores, 2 skip Z smem writes,
+                              // 4 skip band reloads after the first tile, 8 skip S3 MMAs
 };
 int bf_core_smem_bytes(int BN, int nphase, int band_rows, int tg, int w_slots, int ksplit);
 int bf_core3_smem_bytes(const BfCoreArgs &g);

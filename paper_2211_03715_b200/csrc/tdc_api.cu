@@ -703,6 +703,8 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         for (int i = 0; i < nphase; ++i) g.phase_src[i] = phase_src[i];
         g.Hq = Hq; g.Wq = Wq; g.Ho = Ho; g.Wo = Wo;
         if (fuse3) {
+            const char *dbg = std::getenv("TDC_CORE_DBG");
+            g.dbg = dbg ? std::atoi(dbg) : 0;
             const char *yd = std::getenv("TDC_Y_DIRECT");
             g.y_direct = yd && yd[0] && yd[0] != '0';
             g.w3 = dB2 + 2 * n2;

@@ -694,12 +694,13 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         for (int t = cid; t < num_tiles; t += ncl, ++tit) {
             const int m0 = (t % mtiles) * kBM16, nt = t / mtiles;
             for (int kc = k0; kc < k1; ++kc, ra.next()) {
-                mbar_wait(&a_empty[ra.slot], ra.phase ^ 1);
+                mbar_wait_sleep(&a_empty[ra.slot], ra.phase ^ 1);
                 if (kc == k0 && lane == 0) BFCTL(tit, 0);  // producer: band issue
-                if (lane == 0) mbar_arrive_expect_tx(&a_full[ra.slot], a_bytes);
+                const bool stale = (g.dbg & 4) && tit >= 2;  // debug: keep the stale band
+                if (lane == 0) mbar_arrive_expect_tx(&a_full[ra.slot], stale ? 0u : a_bytes);
                 __syncwarp();
                 uint8_t *dst = a_slots + (size_t)ra.slot * a_bytes;
-                for (int c = lane; c < g.nphase * 8; c += 32) {  // (phase, plane, hi/lo)
+                for (int c = stale ? 32 * 64 : lane; c < g.nphase * 8; c += 32) {  // (phase, plane, hi/lo)
                     const int ph = c >> 3, kg = (c >> 1) & 3, lo = c & 1;
                     const long long off =
                         ((long long)(kc * 4 + kg) * g.plane_rows + (long long)g.phase_src[ph] * g.phase_rows + m0) * 8;
@@ -732,11 +733,6 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         // the tile loop: with the 3x3 core (one group of 9 taps) the tap loop below is
         // fully unrolled, so each MMA costs one uniform add -- the issuing thread must
         // keep up with ~48-cycle MMAs.
-        uint32_t aoff9[9];
-#pragma unroll
-        for (int i = 0; i < 9; ++i)
-            aoff9[i] = i < g.taps ? ((uint32_t)g.tap_phase[i] * 4 * band_bytes + (uint32_t)g.tap_off[i] * 16) >> 4
-                                  : 0u;
         const uint32_t wtap16 = w_tap >> 4, plane2a = (2 * band_bytes) >> 4, plane2b = (2 * 2 * BN * 16) >> 4;
         Ring ra(2), rw(WS), acc(2), zr(2), a3(2);
         int tit = 0;
@@ -745,7 +741,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         for (int t = cid;; t += ncl, ++tit) {
             const bool have = t < num_tiles;
             if (have) {
-                mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
+                if (!(g.dbg & 16)) mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
                 tc_fence_after();
                 if (lane == 0) BFCTL(tit, 1);  // MMA: accumulator free
                 const uint32_t d = tmem + acc.slot * ncols;
@@ -770,7 +766,11 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                                 const uint64_t bslot = db + ((ws * w_slot) >> 4);
 #pragma unroll
                                 for (int tt = 0; tt < 9; ++tt) {
-                                    const uint64_t a = aslot + aoff9[tt];
+                                    // tap offsets straight from the kernel parameters (constant
+                                    // index -> uniform loads), so the descriptors stay in uniform
+                                    // registers without per-MMA register->uniform moves
+                                    const uint64_t a = aslot + (((uint32_t)g.tap_phase[tt] * 4 * band_bytes +
+                                                                 (uint32_t)g.tap_off[tt] * 16) >> 4);
                                     const uint64_t b = bslot + tt * wtap16;
 #pragma unroll
                                     for (int j = 0; j < 2; ++j) {
@@ -832,6 +832,10 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                 if (lane == 0) BFCTL(tit - 1, 7);  // S3: Z ready, issuing
                 if (elect_one()) {
                     const uint32_t d3 = tmem + 2 * ncols + a3.slot * ncols3;
+                    if (g.dbg & 8) {  // debug: no stage-3 MMAs
+                        mma_commit(&z_empty[zr.slot]);
+                        mma_commit(&t3full[a3.slot]);
+                    } else {
                     const uint64_t az = dz + ((zr.slot * zbuf) >> 4);
                     for (int j = 0; j < k3; ++j) {
                         const uint64_t aj = az + ((j * 2 * 128 * 16) >> 4);
@@ -847,6 +851,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                     }
                     mma_commit(&z_empty[zr.slot]);
                     mma_commit(&t3full[a3.slot]);
+                    }
                 }
                 __syncwarp();
                 zr.next();
@@ -865,7 +870,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         int tit = 0;
         for (int t = cid; t < num_tiles; t += ncl, acc.next(), zr.next(), ++tit) {
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
-            mbar_wait(&tfull[acc.slot], acc.phase);
+            mbar_wait_sleep(&tfull[acc.slot], acc.phase);
             tc_fence_after();
             if (warp == 2 && lane == 0) BFCTL(tit, 4);  // epilogue: accumulator ready
             if (!F3 && CS > 1) {  // ---- split-K: partial -> own smem, reduce a row slice
@@ -912,10 +917,10 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             }
             long long dst_row = 0;
             const bool valid = out_row(m0 + r, &dst_row);
-            if (F3) mbar_wait(&z_empty[zr.slot], zr.phase ^ 1);
+            if (F3) mbar_wait_sleep(&z_empty[zr.slot], zr.phase ^ 1);
             const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
             const uint32_t zb = smem_u32(zs) + zr.slot * zbuf;
-            for (int c = 0; c < BN; c += 32) {
+            for (int c = 0; c < ((g.dbg & 32) ? 0 : BN); c += 32) {
                 uint32_t rr[32];
                 float v[32];
                 tmem_ld_32x32b_x32(src + c, rr);
@@ -930,7 +935,8 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
                 }
-                if (F3) {  // Z hi/lo planes [c/8 + pl][row r][16 B] (conflict-free: lanes = rows)
+                if (F3 && (g.dbg & 2)) {
+                } else if (F3) {  // Z hi/lo planes [c/8 + pl][row r][16 B] (conflict-free: lanes = rows)
 #pragma unroll
                     for (int pl = 0; pl < 4; ++pl) {
                         uint4 h, l;
@@ -973,7 +979,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         int tit = 0;
         for (int t = cid; t < num_tiles; t += ncl, a3.next(), ++tit) {
             const int m0 = (t % mtiles) * kBM16;
-            mbar_wait(&t3full[a3.slot], a3.phase);
+            mbar_wait_sleep(&t3full[a3.slot], a3.phase);
             tc_fence_after();
             if (warp == 6 && lane == 0) BFCTL(tit, 8);  // E3: acc3 ready
             long long dst_row = 0;
@@ -995,7 +1001,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
                 }
-                if (c >= g.N3) continue;  // warp-uniform
+                if (c >= g.N3 || (g.dbg & 1)) continue;  // warp-uniform
                 epi_bias_res_relu<32>(v, c, g.N3, g.bias, (g.res && valid) ? g.res + dst_row * g.N3 : nullptr, g.relu);
                 if (c + 32 <= g.N3 && (g.N3 & 3) == 0) {
                     if (g.y_direct) {  // each lane stores its own row: no shared-memory traffic

@@ -218,14 +218,25 @@ __global__ void bench_core(int tiles, long long *out) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, cbar0;
     __shared__ uint32_t slot;
-    for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x)
-        reinterpret_cast<float *>(smem)[i] = 0.001f * (i % 7);
+    for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) {
+        if (VAR >= 6) {  // random bf16 pairs (hash of the index), magnitudes ~ N(0,1) like real data
+            uint32_t h = (uint32_t)i * 2654435761u ^ (blockIdx.x * 40503u);
+            h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+            const uint32_t lo = 0x3c00u | (h & 0x807fu) | ((h >> 7) & 0x0180u);
+            const uint32_t hi = 0x3c00u | ((h >> 16) & 0x807fu) | ((h >> 23) & 0x0180u);
+            reinterpret_cast<uint32_t *>(smem)[i] = lo | (hi << 16);
+        } else {
+            reinterpret_cast<float *>(smem)[i] = 0.001f * (i % 7);
+        }
+    }
     const int warp = threadIdx.x / 32;
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
+        mbar_init(&cbar0, 1);
         fence_mbar_init();
+        mbar_arrive(&cbar0);
     }
     fence_proxy_async_smem();
     if (warp == 0) tmem_alloc(&slot, 512);
@@ -241,7 +252,12 @@ __global__ void bench_core(int tiles, long long *out) {
         long long t0 = clock64();
         for (int t = 0; t < tiles; ++t) {
             uint32_t accum = 0;
+            if (VAR == 4) {  // per tile: wait a completed barrier + tcgen05 fence (as the kernel)
+                mbar_wait(&cbar0, 0);
+                tc_fence_after();
+            }
             for (int tap = 0; tap < 9; ++tap) {
+                if (VAR == 3) tc_fence_after();
                 const uint32_t off = VAR == 1 ? 0u : (uint32_t)((tap / 3) * 58 + tap % 3) * 16;
                 const uint64_t a = da + (off >> 4);
                 const uint64_t b = db + ((tap * 32 * 128) >> 4);
@@ -255,6 +271,7 @@ __global__ void bench_core(int tiles, long long *out) {
                 }
             }
             mma_commit(&bar);
+            if (VAR == 5) mbar_wait(&bar, t & 1);  // serialize tiles: the pipe drains each tile
         }
         mbar_wait(&bar, (tiles - 1) & 1);
         long long t1 = clock64();
@@ -318,7 +335,8 @@ __global__ void bench_core_int(int tiles, long long *out, const uint8_t *gsrc, v
         long long t1 = clock64();
         out[blockIdx.x] = t1 - t0;
         done = 1;
-    } else if (warp >= 4 && warp < 8) {
+        if (INT == 5) mbar_arrive(&cbar);
+    } else if ((warp >= 4 && warp < 8) || (INT == 5 && warp != 0)) {
         const int q = warp & 3;
         float acc = 0.f;
         uint32_t it = 0;
@@ -334,6 +352,10 @@ __global__ void bench_core_int(int tiles, long long *out, const uint8_t *gsrc, v
                 float4 v = ld_shared_v4(base + (it & 7) * 2048);
                 st_shared_v4(base + ((it + 3) & 7) * 2048, v.x + 1.f, v.y, v.z, v.w);
                 acc += v.x;
+            }
+            if (INT == 5) {  // mbarrier try_wait spinning on a barrier that completes at the end
+                mbar_wait(&cbar, 0);
+                break;
             }
             if (INT == 4 && warp == 4 && lane == 0) {
                 mbar_arrive_expect_tx(&cbar, 16384);
@@ -354,7 +376,7 @@ void run_core_int(long long *d, const uint8_t *g) {
     auto k = bench_core_int<INT>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 201 * 1024);
     const int tiles = 64, grid = 148;
-    k<<<grid, 256, 201 * 1024>>>(tiles, d, g, nullptr);
+    k<<<grid, INT == 5 ? 320 : 256, 201 * 1024>>>(tiles, d, g, nullptr);
     cudaError_t e = cudaDeviceSynchronize();
     long long h[512];
     cudaMemcpy(h, d, 8 * grid, cudaMemcpyDeviceToHost);
@@ -405,7 +427,7 @@ int main() {
     cudaMalloc(&d, 8 * 512);
 #define ALLN(BF, M, TS, E) run<BF, M, 32, TS, E>(d, 1); run<BF, M, 64, TS, E>(d, 1); \
     run<BF, M, 128, TS, E>(d, 1); run<BF, M, 256, TS, E>(d, 1);
-    run_core<0>(d); run_core<1>(d); run_core<2>(d);
+    run_core<0>(d); run_core<1>(d); run_core<2>(d); run_core<3>(d); run_core<4>(d); run_core<5>(d); run_core<6>(d);
     {
         uint8_t *g;
         cudaMalloc(&g, 17 << 20);
@@ -414,6 +436,7 @@ int main() {
         cudaMalloc(&d2, 8 * 1024);
         run_core_int<0>(d2, g); run_core_int<1>(d2, g); run_core_int<2>(d2, g); run_core_int<3>(d2, g);
         run_core_int<4>(d2, g);
+        run_core_int<5>(d2, g);
     }
     for (int off : {0, 16, 32, 48, 64, 112}) run_off<32, 1>(d, off);
     for (int off : {0, 16, 32, 64}) run_off<64, 1>(d, off);
