@@ -298,6 +298,33 @@ __device__ __forceinline__ void warp_store_block32(float *scratch, const float (
     __syncwarp();
 }
 
+// Inverse of warp_store_block32: v = the 32 floats at row_ptr (row `lane`'s own pointer,
+// or null = zeros), read with coalesced 128-byte row segments (8 lanes per row) and
+// transposed through the warp's shared-memory scratch.
+__device__ __forceinline__ void warp_load_block32(float *scratch, float (&v)[32], const float *row_ptr, int lane) {
+    const uint32_t base = smem_u32(scratch);
+    const int c4 = lane & 7;
+    float4 val[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int r = i * 4 + (lane >> 3);
+        const unsigned long long src = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(row_ptr), r);
+        val[i] = src ? __ldg(reinterpret_cast<const float4 *>(src) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int r = i * 4 + (lane >> 3);
+        st_shared_v4(base + (uint32_t)(r * 8 + (c4 ^ (r & 7))) * 16, val[i].x, val[i].y, val[i].z, val[i].w);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const float4 f = ld_shared_v4(base + (uint32_t)(lane * 8 + (k ^ (lane & 7))) * 16);
+        v[4 * k] = f.x; v[4 * k + 1] = f.y; v[4 * k + 2] = f.z; v[4 * k + 3] = f.w;
+    }
+    __syncwarp();
+}
+
 // ------------------------------------------------------------ descriptors
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"):
 //   [0,14) start>>4, [16,30) LBO>>4, [32,46) SBO>>4, [46,48) version=1,

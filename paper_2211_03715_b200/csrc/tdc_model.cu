@@ -100,12 +100,67 @@ __global__ void tdc_avgpool_kernel(const float *__restrict__ x, float *__restric
     out[(long long)b * C + c] = s / (float)HW;
 }
 
+// Direct fp32 convolution for thin inputs (C <= 4: the stem), one thread per output
+// pixel and 64 output channels in registers; weights [K][K][C][N] (BN folded) staged in
+// shared memory and read as broadcasts.  Avoids a K*K*C-wide im2col round trip.
+constexpr int kDirectCo = 64;
+__global__ void __launch_bounds__(128) tdc_direct_conv_kernel(const float *__restrict__ x,
+                                                               const float *__restrict__ w,
+                                                               const float *__restrict__ bias, float *__restrict__ y,
+                                                               int B, int H, int W, int C, int N, int K, int s, int p,
+                                                               int Ho, int Wo, int relu) {
+    extern __shared__ float ws[];
+    const int KKC = K * K * C;
+    const int n0 = blockIdx.y * kDirectCo;
+    const int nc = min(kDirectCo, N - n0);
+    for (int i = threadIdx.x; i < KKC * kDirectCo; i += blockDim.x) {
+        const int n = i % kDirectCo, k = i / kDirectCo;
+        ws[i] = n < nc ? w[(size_t)k * N + n0 + n] : 0.f;
+    }
+    __syncthreads();
+    const long long pix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= (long long)B * Ho * Wo) return;
+    const int ox = (int)(pix % Wo), oy = (int)((pix / Wo) % Ho), b = (int)(pix / ((long long)Wo * Ho));
+    float acc[kDirectCo];
+#pragma unroll
+    for (int n = 0; n < kDirectCo; ++n) acc[n] = 0.f;
+    for (int r = 0; r < K; ++r) {
+        const int iy = oy * s - p + r;
+        if (iy < 0 || iy >= H) continue;
+        for (int t = 0; t < K; ++t) {
+            const int ix = ox * s - p + t;
+            if (ix < 0 || ix >= W) continue;
+            const float *xp = x + (((long long)b * H + iy) * W + ix) * C;
+            for (int c = 0; c < C; ++c) {
+                const float xv = __ldg(xp + c);
+                const float *wr = ws + ((r * K + t) * C + c) * kDirectCo;
+#pragma unroll
+                for (int n = 0; n < kDirectCo; ++n) acc[n] = fmaf(xv, wr[n], acc[n]);
+            }
+        }
+    }
+    float *yp = y + pix * N + n0;
+    for (int n = 0; n < nc; n += 4) {
+        float4 v;
+        v.x = acc[n] + (bias ? bias[n0 + n] : 0.f);
+        v.y = acc[n + 1] + (bias ? bias[n0 + n + 1] : 0.f);
+        v.z = acc[n + 2] + (bias ? bias[n0 + n + 2] : 0.f);
+        v.w = acc[n + 3] + (bias ? bias[n0 + n + 3] : 0.f);
+        if (relu) {
+            v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+        }
+        *reinterpret_cast<float4 *>(yp + n) = v;
+    }
+}
+
 int ew_grid(long long n) { return (int)std::min<long long>(div_up((int)std::min<long long>(n, 1LL << 30), 256), 148 * 16); }
 
 // ------------------------------------------------------------------ dense GEMM op
 struct DenseOp {
     int Kdim = 0;            // GEMM K (C for a plain 1x1, else the padded im2col row)
     bool im2col = false;
+    bool direct = false;     // thin input (C <= 4, N % 4 == 0): tdc_direct_conv_kernel
+    float *d_wdirect = nullptr;  // [K][K][C][N] fp32, BN folded, then the bias
     uint16_t *d_w = nullptr;  // [hi | lo] bf16 panels [R][K64], then fp32 bias
     float *d_bias = nullptr;
     tdc::TcGemmArgs args;
@@ -166,6 +221,24 @@ tdc_status plan_dense(tdc_model_s *m, ModelOp &op, const tdc_model_op &o) {
     DenseOp &g = op.dense;
     const int K = o.kind == TDC_OP_FC ? 1 : o.kernel;
     const int C = op.C, N = op.Co;
+    if (o.kind == TDC_OP_CONV && o.res < 0 && C <= 4 && N % 4 == 0 && K * K * C * kDirectCo * 4 <= 96 * 1024) {
+        g.direct = true;
+        std::vector<double> scale, bias;
+        bn_fold(o, N, scale, bias);
+        std::vector<float> h((size_t)K * K * C * N + N);
+        for (int n = 0; n < N; ++n) {
+            for (int c = 0; c < C; ++c)
+                for (int r = 0; r < K; ++r)
+                    for (int t = 0; t < K; ++t)
+                        h[((size_t)(r * K + t) * C + c) * N + n] =
+                            (float)(scale[n] * o.w[(((size_t)n * C + c) * K + r) * K + t]);
+            h[(size_t)K * K * C * N + n] = (float)bias[n];
+        }
+        cudaError_t e = cudaMalloc(&g.d_wdirect, h.size() * sizeof(float));
+        if (e == cudaSuccess) e = cudaMemcpy(g.d_wdirect, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return mcuda(e, "direct conv weights");
+        return TDC_OK;
+    }
     g.im2col = !(K == 1 && o.stride == 1 && o.pad == 0 && C % 4 == 0);
     g.Kdim = g.im2col ? round_up(K * K * C, 32) : C;
     const int K64 = round_up(g.Kdim, 64);
@@ -217,6 +290,19 @@ tdc_status run_dense(tdc_model_s *m, ModelOp &op, const float *src, float *dst, 
     DenseOp &g = op.dense;
     const tdc_model_op &o = op.d;
     const long long M = (long long)batch * op.Ho * op.Wo;
+    if (g.direct) {
+        const int K = o.kernel, C = op.C, N = op.Co;
+        const int smem = K * K * C * kDirectCo * 4;
+        cudaError_t e = cudaFuncSetAttribute(tdc_direct_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return mcuda(e, "direct conv attribute");
+        dim3 grid((unsigned)div_up((int)M, 128), (unsigned)div_up(N, kDirectCo));
+        tdc_direct_conv_kernel<<<grid, 128, smem, st>>>(src, g.d_wdirect, g.d_wdirect + (size_t)K * K * C * N, dst,
+                                                        batch, op.H, op.W, C, N, K, o.stride, o.pad, op.Ho, op.Wo,
+                                                        o.relu);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return mcuda(e, "direct conv launch");
+        return TDC_OK;
+    }
     const float *A = src;
     if (g.im2col) {
         const int K = o.kind == TDC_OP_FC ? 1 : o.kernel;
@@ -250,6 +336,7 @@ void destroy(tdc_model_s *m) {
     for (auto &op : m->ops) {
         if (op.tkd) tdc_conv_plan_destroy(op.tkd);
         if (op.dense.d_w) cudaFree(op.dense.d_w);
+        if (op.dense.d_wdirect) cudaFree(op.dense.d_wdirect);
     }
     for (size_t i = 1; i < m->act.size(); ++i)
         if (m->act[i]) cudaFree(m->act[i]);

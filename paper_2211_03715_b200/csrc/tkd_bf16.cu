@@ -442,8 +442,17 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                         }
                     }
                 } else {  // fp32 Y (+bias, +residual, ReLU), row-major, coalesced through shared memory
-                    epi_bias_res_relu<32>(v, n, g.Nn, g.bias, (g.res && valid) ? g.res + dst_row * g.ldo : nullptr,
-                                          g.relu);
+                    const bool full = n + 32 <= g.Nn && (g.ldo & 3) == 0;
+                    if (g.res && full) {  // residual block read coalesced, then per-lane rows
+                        float rv[32];
+                        warp_load_block32(scratch, rv, valid ? g.res + dst_row * g.ldo + n : nullptr, lane);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] += rv[j];
+                        epi_bias_res_relu<32>(v, n, g.Nn, g.bias, nullptr, g.relu);
+                    } else {
+                        epi_bias_res_relu<32>(v, n, g.Nn, g.bias,
+                                              (g.res && valid) ? g.res + dst_row * g.ldo : nullptr, g.relu);
+                    }
                     float *dst = g.out + dst_row * g.ldo;
                     if (n + 32 <= g.Nn && (g.ldo & 3) == 0) {
                         warp_store_block32(scratch, v, valid ? dst + n : nullptr, lane);
@@ -1002,7 +1011,16 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
                 }
                 if (c >= g.N3 || (g.dbg & 1)) continue;  // warp-uniform
-                epi_bias_res_relu<32>(v, c, g.N3, g.bias, (g.res && valid) ? g.res + dst_row * g.N3 : nullptr, g.relu);
+                if (g.res && c + 32 <= g.N3 && (g.N3 & 3) == 0) {  // coalesced residual block
+                    float rv[32];
+                    warp_load_block32(scratch, rv, valid ? g.res + dst_row * g.N3 + c : nullptr, lane);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] += rv[j];
+                    epi_bias_res_relu<32>(v, c, g.N3, g.bias, nullptr, g.relu);
+                } else {
+                    epi_bias_res_relu<32>(v, c, g.N3, g.bias, (g.res && valid) ? g.res + dst_row * g.N3 : nullptr,
+                                          g.relu);
+                }
                 if (c + 32 <= g.N3 && (g.N3 & 3) == 0) {
                     if (g.y_direct) {  // each lane stores its own row: no shared-memory traffic
                         if (valid)
