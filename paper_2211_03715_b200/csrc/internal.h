@@ -59,6 +59,8 @@ struct TcGemmArgs {
     int bstages;      // 3xBF16 stage 1: depth of the weight (B) ring
     const float *res; // fp32 output only: residual added before the activation (ld = ldo), or null
     int relu;         // fp32 output only: ReLU after bias/residual
+    int dbg;          // debug (TDC_GEMM_DBG): 1 skip the fp32 output stores, 2 skip residual reads
+    int tma_y;        // fp32 output (remap 0, ldo == Nn): full 32x32 blocks stored by TMA (mapY)
 };
 
 // Stage-2 core convolution with a shared-memory-resident X' band (tkd_tc.cu):
@@ -121,7 +123,8 @@ cudaError_t fused_launch(const CUtensorMap &mapX, const FusedArgs &g, int grid, 
 int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages);
 int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, int *bstages);
 cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, const CUtensorMap &mapB,
-                           const CUtensorMap &mapBlo, const TcGemmArgs &g, int grid, cudaStream_t st);
+                           const CUtensorMap &mapBlo, const CUtensorMap &mapY, const TcGemmArgs &g, int grid,
+                           cudaStream_t st);
 // 3xBF16 stage-2 core convolution (tkd_bf16.cu).  X' hi/lo planar bf16
 // [D1s/8][rows_total][8]; weights blocked [kc][ntile][group][tg taps][plane 4][2BN][8]
 // with rows 0..BN-1 = hi and BN..2BN-1 = lo, so one bulk copy moves a whole

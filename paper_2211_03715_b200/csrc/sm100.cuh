@@ -92,6 +92,19 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+// 2-D tensor store shared -> global (bulk-group completion), and its group fences
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void *src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the shared-memory source of every committed store has been read (may be overwritten)
+__device__ __forceinline__ void bulk_wait_group_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // 1-D bulk copy global -> shared (size multiple of 16, both 16-aligned)
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes,
                                           uint64_t *bar) {
@@ -298,19 +311,24 @@ __device__ __forceinline__ void warp_store_block32(float *scratch, const float (
     __syncwarp();
 }
 
-// Inverse of warp_store_block32: v = the 32 floats at row_ptr (row `lane`'s own pointer,
-// or null = zeros), read with coalesced 128-byte row segments (8 lanes per row) and
-// transposed through the warp's shared-memory scratch.
-__device__ __forceinline__ void warp_load_block32(float *scratch, float (&v)[32], const float *row_ptr, int lane) {
-    const uint32_t base = smem_u32(scratch);
+// Inverse of warp_store_block32, split in two so the global loads of the next block can
+// be in flight while the current one is used: warp_load_block32_issue reads the 32 x 32
+// block whose row `lane` starts at row_ptr (null = zeros) with coalesced 128-byte row
+// segments (8 lanes per row); warp_load_block32_finish transposes it through the warp's
+// shared-memory scratch so that lane i gets row i.
+__device__ __forceinline__ void warp_load_block32_issue(float4 (&val)[8], const float *row_ptr, int lane) {
     const int c4 = lane & 7;
-    float4 val[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int r = i * 4 + (lane >> 3);
         const unsigned long long src = __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(row_ptr), r);
         val[i] = src ? __ldg(reinterpret_cast<const float4 *>(src) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+}
+__device__ __forceinline__ void warp_load_block32_finish(float *scratch, const float4 (&val)[8], float (&v)[32],
+                                                         int lane) {
+    const uint32_t base = smem_u32(scratch);
+    const int c4 = lane & 7;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int r = i * 4 + (lane >> 3);
@@ -323,6 +341,11 @@ __device__ __forceinline__ void warp_load_block32(float *scratch, float (&v)[32]
         v[4 * k] = f.x; v[4 * k + 1] = f.y; v[4 * k + 2] = f.z; v[4 * k + 3] = f.w;
     }
     __syncwarp();
+}
+__device__ __forceinline__ void warp_load_block32(float *scratch, float (&v)[32], const float *row_ptr, int lane) {
+    float4 val[8];
+    warp_load_block32_issue(val, row_ptr, lane);
+    warp_load_block32_finish(scratch, val, v, lane);
 }
 
 // ------------------------------------------------------------ descriptors

@@ -127,6 +127,8 @@ struct tdc_conv_plan_s {
     tdc::BfCoreArgs bf_core;
     bool fuse3 = false;            // 3xBF16: core + stage 3 in one kernel (Z on chip)
     tdc_plan_hints hints = {-1, 0, 0, 0, 0, 0, 0};  // planner overrides (tdc_conv_plan_ex)
+    CUtensorMap mapY3;             // 3xBF16 stage 3: TMA map of the output (per y pointer)
+    const float *last_y3 = nullptr;
     float *d_tc_w = nullptr;       // Bt1 | Bt2 | Bt3 | bias
     float *d_xg = nullptr;         // X' phase grids (zero borders)
     float *d_z = nullptr;          // Z compact
@@ -720,6 +722,10 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         st.args.BN = BN3; st.args.ldo = N; st.args.remap = 0; st.args.bias = dbias;
         st.args.ksplit = ks3;
         st.args.stages = tdc::bf_pick_stages(BN3, p->max_smem, 0, nullptr, ks3, nullptr);
+        {
+            const char *ev = std::getenv("TDC_NO_TMA_Y");
+            st.args.tma_y = ks3 == 1 && N % 4 == 0 && !(ev && ev[0] && ev[0] != '0');
+        }
         st.grid_n = R3 / BN3;
         st.args.ntiles = st.grid_n;
         if (!tdc::make_tma_2d_bf16(&st.mapA, z, M3, D2p, D2p, 128) ||
@@ -768,7 +774,7 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
         return (int)(std::max<long long>(1, std::min(tiles, cap)) * ks);
     };
     cudaError_t e = tdc::bf_gemm_launch(
-        s1.mapA, s1.mapA, s1.mapB, s1.mapBlo, a1,
+        s1.mapA, s1.mapA, s1.mapB, s1.mapBlo, s1.mapA, a1,
         grid_ks(a1.M, a1.ntiles, tdc::bf_smem_bytes(a1.BN, a1.stages, a1.xstages, a1.ksplit, a1.bstages), a1.BN, a1.ksplit), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-1 launch");
     if (p->fuse3) {
@@ -782,8 +788,13 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
         c, grid_ks(c.M, c.ntiles, tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots, c.ksplit),
                    c.ncat ? 2 * c.BN : c.BN, c.ksplit), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-2 launch");
+    if (a3.tma_y && y != p->last_y3) {
+        if (!tdc::make_tma_2d(&p->mapY3, y, (long long)p->desc.batch * d.Ho * d.Wo, d.N, d.N, 32))
+            return fail(TDC_ERR_INVALID_ARGUMENT, "cuTensorMapEncodeTiled rejected y (16-byte aligned pointer?)");
+        p->last_y3 = y;
+    }
     e = tdc::bf_gemm_launch(
-        s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, a3,
+        s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, p->mapY3, a3,
         grid_ks(a3.M, a3.ntiles, tdc::bf_smem_bytes(a3.BN, a3.stages, 0, a3.ksplit, 0), a3.BN, a3.ksplit), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-3 launch");
     return TDC_OK;

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -167,6 +168,8 @@ struct DenseOp {
     CUtensorMap mapA, mapB, mapBlo;
     const float *mapA_src = nullptr;
     long long mapA_rows = 0;
+    CUtensorMap mapY;        // TMA map of the output (tma_y), re-encoded when dst changes
+    const float *mapY_dst = nullptr;
 };
 
 }  // namespace
@@ -279,6 +282,11 @@ tdc_status plan_dense(tdc_model_s *m, ModelOp &op, const tdc_model_op &o) {
     a.Nn = N; a.kchunks = K64 / 64; a.taps = 1; a.BN = BN; a.remap = 0; a.a_convert = 1; a.out_bf16 = 0;
     a.ldo = N; a.bias = g.d_bias; a.relu = o.relu; a.ntiles = R / BN; a.ksplit = 1;
     a.stages = tdc::bf_pick_stages(BN, m->max_smem, 1, &a.xstages, 1, &a.bstages);
+    if (const char *dbg = std::getenv("TDC_GEMM_DBG")) a.dbg = std::atoi(dbg);
+    {
+        const char *ev = std::getenv("TDC_NO_TMA_Y");
+        a.tma_y = N % 4 == 0 && !(ev && ev[0] && ev[0] != '0');
+    }
     if (!tdc::make_tma_2d_bf16(&g.mapB, g.d_w, R, K64, K64, BN) ||
         !tdc::make_tma_2d_bf16(&g.mapBlo, g.d_w + nw, R, K64, K64, BN))
         return mfail(TDC_ERR_CUDA, "cuTensorMapEncodeTiled failed (dense weights)");
@@ -327,7 +335,12 @@ tdc_status run_dense(tdc_model_s *m, ModelOp &op, const float *src, float *dst, 
     const long long tiles = (long long)div_up((int)M, 128) * a.ntiles;
     const long long cap = (long long)m->num_sms * tdc::persistent_occupancy(smem, a.BN);
     const int grid = (int)std::max<long long>(1, std::min(tiles, cap));
-    cudaError_t e = tdc::bf_gemm_launch(g.mapA, g.mapA, g.mapB, g.mapBlo, a, grid, st);
+    if (a.tma_y && dst != g.mapY_dst) {
+        if (!tdc::make_tma_2d(&g.mapY, dst, rows, op.Co, op.Co, 32))
+            return mfail(TDC_ERR_INVALID_ARGUMENT, "cuTensorMapEncodeTiled rejected a dense-op output");
+        g.mapY_dst = dst;
+    }
+    cudaError_t e = tdc::bf_gemm_launch(g.mapA, g.mapA, g.mapB, g.mapBlo, a.tma_y ? g.mapY : g.mapA, a, grid, st);
     if (e != cudaSuccess) return mcuda(e, "dense GEMM launch");
     return TDC_OK;
 }

@@ -185,7 +185,7 @@ template <bool CONVERT>
 __global__ void __launch_bounds__(CONVERT ? 192 + kConvThreads16 : 192, 1)
 tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo,
-                   const TcGemmArgs g) {
+                   const __grid_constant__ CUtensorMap mapY, const TcGemmArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -443,7 +443,8 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                     }
                 } else {  // fp32 Y (+bias, +residual, ReLU), row-major, coalesced through shared memory
                     const bool full = n + 32 <= g.Nn && (g.ldo & 3) == 0;
-                    if (g.res && full) {  // residual block read coalesced, then per-lane rows
+                    if (g.dbg & 1) continue;
+                    if (g.res && full && !(g.dbg & 2)) {  // residual block read coalesced, then per-lane rows
                         float rv[32];
                         warp_load_block32(scratch, rv, valid ? g.res + dst_row * g.ldo + n : nullptr, lane);
 #pragma unroll
@@ -454,7 +455,21 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                                               (g.res && valid) ? g.res + dst_row * g.ldo : nullptr, g.relu);
                     }
                     float *dst = g.out + dst_row * g.ldo;
-                    if (n + 32 <= g.Nn && (g.ldo & 3) == 0) {
+                    if (g.tma_y && full) {  // stage the 32x32 block (128B-swizzled box) and TMA-store it
+                        const uint32_t sb = smem_u32(scratch);
+                        if (lane == 0) bulk_wait_group_read0();  // this warp's previous block was read
+                        __syncwarp();
+#pragma unroll
+                        for (int j4 = 0; j4 < 8; ++j4)
+                            st_shared_v4(sb + (uint32_t)(lane * 128 + ((j4 ^ (lane & 7)) << 4)), v[4 * j4],
+                                         v[4 * j4 + 1], v[4 * j4 + 2], v[4 * j4 + 3]);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&mapY, scratch, n, m0 + q * 32);
+                            bulk_commit_group();
+                        }
+                    } else if (n + 32 <= g.Nn && (g.ldo & 3) == 0) {
                         warp_store_block32(scratch, v, valid ? dst + n : nullptr, lane);
                     } else if (valid) {
                         for (int j = 0; j < 32 && n + j < g.Nn; ++j) dst[n + j] = v[j];
@@ -465,6 +480,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             mbar_arrive_relaxed(&tempty[acc.slot]);
             if (warp == 2 && lane == 0) BFTL(seq, tit, 5);  // epilogue: done
         }
+        if (g.tma_y && lane == 0) bulk_wait_group0();  // TMA stores complete before the CTA retires
     } else if (CONVERT) {  // ----------------- converter: fp32 staging -> bf16 hi/lo A tiles
         const int tid = threadIdx.x - 192;
         Ring r(S), rx(SX);
@@ -534,19 +550,20 @@ int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, 
 }
 
 cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, const CUtensorMap &mapB,
-                           const CUtensorMap &mapBlo, const TcGemmArgs &g, int grid, cudaStream_t st) {
+                           const CUtensorMap &mapBlo, const CUtensorMap &mapY, const TcGemmArgs &g, int grid,
+                           cudaStream_t st) {
     const int smem = bf_smem_bytes(g.BN, g.stages, g.a_convert ? g.xstages : 0, g.ksplit, g.a_convert ? g.bstages : 0);
     cudaError_t e;
     if (g.a_convert) {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         return launch_pdl_cluster(tdc_bf_gemm_kernel<true>, grid, 192 + kConvThreads16, smem, st, g.ksplit, mapA,
-                                  mapAlo, mapB, mapBlo, g);
+                                  mapAlo, mapB, mapBlo, mapY, g);
     } else {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         return launch_pdl_cluster(tdc_bf_gemm_kernel<false>, grid, 192, smem, st, g.ksplit, mapA, mapAlo, mapB,
-                                  mapBlo, g);
+                                  mapBlo, mapY, g);
     }
     return cudaGetLastError();
 }
