@@ -684,7 +684,8 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
     __syncthreads();
     if (CS > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
     tc_fence_after();
-    pdl_wait();
+    // pdl_wait() is taken by the producer alone, after it has issued the plan-owned weight
+    // loads: every other role only consumes what the producer's loads bring in.
     pdl_launch_dependents();
     if (threadIdx.x == 0) BFCSPAN(1);
     const uint32_t tmem = *tmem_slot;
@@ -715,6 +716,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         if (resident)  // ntiles == 1: every (kc, group) slice once, for the CTA's lifetime
             for (int i = 0; i < WS; ++i)
                 load_split(w_slots + (size_t)i * w_slot, wsrc + (size_t)i * w_slot, w_slot, &w_full[i]);
+        pdl_wait();  // X' is written by the previous kernel (stage 1)
         Ring ra(2), rw(WS);
         int tit = 0;
         for (int t = cid; t < num_tiles; t += ncl, ++tit) {
