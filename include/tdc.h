@@ -92,6 +92,8 @@ typedef struct {
     int32_t bn_stage1, bn_core, bn_stage3;
     int32_t ksplit_stage1, ksplit_core, ksplit_stage3;
     int32_t core3;
+    /* split-K through L2 (1 = off): K pieces of stage 1 / the core / stage 3 */
+    int32_t gsplit_stage1, gsplit_core, gsplit_stage3;
 } tdc_plan_info;
 
 /* Planner overrides for TDC_MATH_3XBF16 (the analytical planner
@@ -104,6 +106,8 @@ typedef struct {
     int32_t core3;                         /* -1 auto, 0 never, 1 when it fits      */
     int32_t bn_stage1, bn_core, bn_stage3; /* 0 auto                               */
     int32_t ksplit_stage1, ksplit_core, ksplit_stage3; /* 0 auto, 1 off, 2..4     */
+    int32_t gsplit_stage1, gsplit_core, gsplit_stage3; /* split-K through L2:
+                                              0 auto, 1 off, 2..8 pieces (clamped to K chunks) */
 } tdc_plan_hints;
 
 const char *tdc_version(void);

@@ -61,6 +61,9 @@ struct TcGemmArgs {
     int relu;         // fp32 output only: ReLU after bias/residual
     int dbg;          // debug (TDC_GEMM_DBG): 1 skip the fp32 output stores, 2 skip residual reads
     int tma_y;        // fp32 output (remap 0, ldo == Nn): full 32x32 blocks stored by TMA (mapY)
+    int gsplit;       // 3xBF16: >1 = split K into gsplit pieces, partials reduced through L2
+    float *part;      // gsplit: fp32 partial tiles [tiles][gsplit-1][BN/4][128][4]
+    int *flags;       // gsplit: one flag per (tile, piece > 0), zero between launches
 };
 
 // Stage-2 core convolution with a shared-memory-resident X' band (tkd_tc.cu):
@@ -151,6 +154,9 @@ struct BfCoreArgs {
     int relu;                 // fused stage 3: ReLU after bias/residual
     int dbg;                  // debug (TDC_CORE_DBG): 1 skip Y stores, 2 skip Z smem writes,
                               // 4 skip band reloads after the first tile, 8 skip S3 MMAs
+    int gsplit;               // stage 2 alone: >1 = split the D1 chunks into gsplit pieces (L2 partials)
+    float *part;              // gsplit: fp32 partial tiles [tiles][gsplit-1][BN/4][128][4]
+    int *flags;               // gsplit: one flag per (tile, piece > 0)
 };
 int bf_core_smem_bytes(int BN, int nphase, int band_rows, int tg, int w_slots, int ksplit);
 int bf_core3_smem_bytes(const BfCoreArgs &g);

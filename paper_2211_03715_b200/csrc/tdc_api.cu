@@ -126,12 +126,13 @@ struct tdc_conv_plan_s {
     tdc::TcCoreArgs core_args;
     tdc::BfCoreArgs bf_core;
     bool fuse3 = false;            // 3xBF16: core + stage 3 in one kernel (Z on chip)
-    tdc_plan_hints hints = {-1, 0, 0, 0, 0, 0, 0};  // planner overrides (tdc_conv_plan_ex)
+    tdc_plan_hints hints = {-1, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // planner overrides (tdc_conv_plan_ex)
     CUtensorMap mapY3;             // 3xBF16 stage 3: TMA map of the output (per y pointer)
     const float *last_y3 = nullptr;
     float *d_tc_w = nullptr;       // Bt1 | Bt2 | Bt3 | bias
     float *d_xg = nullptr;         // X' phase grids (zero borders)
     float *d_z = nullptr;          // Z compact
+    float *d_gs = nullptr;         // 3xBF16 split-K through L2: partial tiles | flags
     size_t tc_ws_bytes = 0;
     const float *tc_last_x = nullptr;
     int max_smem = 0;
@@ -464,6 +465,50 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         if (BN3 <= 32 || tdc::bf_smem_bytes(BN3, st, 0, ks3, 0) <= p->max_smem) break;
         BN3 /= 2;
     }
+    // Split-K through L2 (gsplit): when the output tiles alone leave SMs
+    // idle, pick (N tile, pieces) minimising waves x K iterations per piece x the cost of
+    // one iteration (measured MMA issue cost + operand loads) + a fix-up
+    // cost per split; the planner's own choice stands unless this is >= 5 % cheaper.
+    const char *gev = std::getenv("TDC_GSPLIT");
+    const bool gs_off = !(gev && gev[0] && gev[0] != '0');  // opt-in: measured slower on R18 (§8c)
+    auto mma_cyc = [](int n) { return n <= 64 ? (n <= 32 ? 44.0 : 48.0) : n / 2.0; };
+    auto gs_choose = [&](long long mrows, int nn, int iters, int bn_max, bool bn_fixed, int *bn, int hint,
+                         auto iter_cost) {
+        const long long mt = div_up((int)mrows, 128);
+        auto cost = [&](int b, int gsp) {
+            const long long units = mt * div_up(nn, b) * gsp;
+            return (double)div_up((int)units, p->num_sms) * div_up(iters, gsp) * iter_cost(b) +
+                   (gsp > 1 ? 2500.0 : 0.0);
+        };
+        if (hint > 0) return std::max(1, std::min(hint, std::min(iters, 8)));
+        if (gs_off) return 1;
+        int best_bn = *bn, best_gs = 1;
+        double best = cost(*bn, 1) * 0.95;
+        int top = 32;
+        while (top < nn && top < bn_max) top *= 2;
+        for (int b = bn_fixed ? *bn : top; b >= (bn_fixed ? *bn : 32); b /= 2)
+            for (int gsp = 1; gsp <= std::min(iters, 8); ++gsp) {
+                const double t = cost(b, gsp);
+                if (t < best) {
+                    best = t;
+                    best_bn = b;
+                    best_gs = gsp;
+                }
+            }
+        *bn = best_bn;
+        return best_gs;
+    };
+    auto gemm_iter = [&](int b) { return 12.0 * mma_cyc(b) + (32768.0 + 256.0 * b) / 64.0; };
+    int gs1 = 1, gs3 = 1, gs2 = 1;
+    if (ks1 == 1) {
+        gs1 = gs_choose(M1, D1s, C64 / 64, 128, p->hints.bn_stage1 > 0, &BN1, p->hints.gsplit_stage1, gemm_iter);
+        for (;;) {  // the chosen N tile must still fit
+            int xs = 0, bs = 0;
+            const int st = tdc::bf_pick_stages(BN1, p->max_smem, 1, &xs, 1, &bs);
+            if (BN1 <= 32 || tdc::bf_smem_bytes(BN1, st, xs, 1, bs) <= p->max_smem) break;
+            BN1 /= 2;
+        }
+    }
     const int KK = K * K;
     const int maxoff = ((K - 1) / s) * Wq + (K - 1) / s;
     const int band_rows = round_up(128 + maxoff, 8);
@@ -486,9 +531,12 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
     // lifetime when the whole N tile fits, otherwise a ring of w_slots slices.
     const int k2chunks = D1s / 32;
     int tg = 0, w_slots = 0, resident = 0, nt2 = 0;
+    // debug overrides of the streamed-weight ring: taps per slice / maximum ring depth
+    const int env_tg = std::getenv("TDC_CORE_TG") ? std::atoi(std::getenv("TDC_CORE_TG")) : 0;
+    const int ws_max = std::getenv("TDC_CORE_WS") ? std::max(2, std::atoi(std::getenv("TDC_CORE_WS"))) : 4;
     // Fused core + stage 3 (Z stays on chip) when the whole D2 fits one N tile, the
     // U_out panel is resident and both double-buffered accumulators fit in TMEM.
-    const int N3p = round_up(N, 32), ncat3 = 2 * N3p <= 128;
+    const int N3p = round_up(N, 32), ncat3 = 2 * N3p <= 128 && !std::getenv("TDC_NO_NCAT3");
     int fuse3 = 0;
     {
         const char *ev = std::getenv("TDC_NO_FUSE3");
@@ -507,8 +555,8 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
                     tg = KK; w_slots = k2chunks; resident = 1;
                 } else {
                     for (int g = KK; g >= 1 && !tg; --g) {
-                        if (KK % g) continue;
-                        for (int ws = 4; ws >= 2; --ws) {
+                        if (KK % g || (env_tg > 0 && g != env_tg)) continue;
+                        for (int ws = ws_max; ws >= 2; --ws) {
                             t.tg = g; t.w_slots = ws;
                             if (tdc::bf_core3_smem_bytes(t) <= p->max_smem) {
                                 tg = g; w_slots = ws;
@@ -561,6 +609,20 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
             while (BN2 < h.bn_core && BN2 < 256) BN2 *= 2;
         }
         if (h.ksplit_core > 0) ks2 = std::max(1, std::min({h.ksplit_core, 4, k2chunks}));
+        if (ks2 == 1) {
+            auto core_iter = [&](int b) {
+                return 2.0 * KK * (2 * b <= 128 ? 2 * mma_cyc(2 * b) : 3 * mma_cyc(b)) + KK * b * 128.0 / 48.0;
+            };
+            gs2 = gs_choose(M2, D2s, k2chunks, 128, h.bn_core > 0, &BN2, h.gsplit_core, core_iter);
+        }
+        if (ks3 == 1) {
+            gs3 = gs_choose(M3, N, D2p / 64, 128, h.bn_stage3 > 0, &BN3, h.gsplit_stage3, gemm_iter);
+            for (;;) {
+                const int stg = tdc::bf_pick_stages(BN3, p->max_smem, 0, nullptr, 1, nullptr);
+                if (BN3 <= 32 || tdc::bf_smem_bytes(BN3, stg, 0, 1, 0) <= p->max_smem) break;
+                BN3 /= 2;
+            }
+        }
     }
     for (; !fuse3 && BN2 >= 32; BN2 /= 2) {
         nt2 = div_up(D2s, BN2);
@@ -572,8 +634,8 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
             break;
         }
         for (int g = KK; g >= 1 && !tg; --g) {
-            if (KK % g) continue;
-            for (int ws = 4; ws >= 2; --ws)
+            if (KK % g || (env_tg > 0 && g != env_tg)) continue;
+            for (int ws = ws_max; ws >= 2; --ws)
                 if (tdc::bf_core_smem_bytes(BN2, nphase, band_rows, g, ws, ks2) <= p->max_smem) {
                     tg = g;
                     w_slots = ws;
@@ -661,6 +723,30 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
     p->tc_ws_bytes = 2 * (xg_elems + z_elems) * sizeof(uint16_t);
     uint16_t *xg = reinterpret_cast<uint16_t *>(p->d_xg), *xg_lo = xg + xg_elems;
     uint16_t *z = reinterpret_cast<uint16_t *>(p->d_z), *z_lo = z + z_elems;
+    // split-K through L2: fp32 partial tiles of pieces 1..gs-1 and one flag each (zeroed
+    // here; every launch leaves them zero)
+    const long long gt1 = (long long)div_up((int)M1, 128) * (R1 / BN1), gt2 = (long long)div_up((int)M2, 128) * nt2,
+                    gt3 = fuse3 ? 0 : (long long)div_up((int)M3, 128) * (R3 / BN3);
+    const size_t gp1 = gs1 > 1 ? (size_t)gt1 * (gs1 - 1) * 128 * BN1 : 0,
+                 gp2 = (!fuse3 && gs2 > 1) ? (size_t)gt2 * (gs2 - 1) * 128 * BN2 : 0,
+                 gp3 = gs3 > 1 ? (size_t)gt3 * (gs3 - 1) * 128 * BN3 : 0;
+    const size_t gf1 = gs1 > 1 ? (size_t)gt1 * (gs1 - 1) : 0, gf2 = gp2 ? (size_t)gt2 * (gs2 - 1) : 0,
+                 gf3 = gs3 > 1 ? (size_t)gt3 * (gs3 - 1) : 0;
+    float *gpart1 = nullptr, *gpart2 = nullptr, *gpart3 = nullptr;
+    int *gflag1 = nullptr, *gflag2 = nullptr, *gflag3 = nullptr;
+    if (gp1 + gp2 + gp3) {
+        const size_t gbytes = (gp1 + gp2 + gp3) * sizeof(float) + (gf1 + gf2 + gf3) * sizeof(int);
+        e = cudaMalloc(&p->d_gs, gbytes);
+        if (e == cudaSuccess) e = cudaMemset(p->d_gs, 0, gbytes);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(split-K workspace)");
+        p->tc_ws_bytes += gbytes;
+        gpart1 = p->d_gs;
+        gpart2 = gpart1 + gp1;
+        gpart3 = gpart2 + gp2;
+        gflag1 = reinterpret_cast<int *>(gpart3 + gp3);
+        gflag2 = gflag1 + gf1;
+        gflag3 = gflag2 + gf2;
+    }
 
     auto base_args = [&](tdc::TcGemmArgs &g) {
         std::memset(&g, 0, sizeof g);
@@ -676,6 +762,11 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         st.args.out = reinterpret_cast<float *>(xg); st.args.out_lo = reinterpret_cast<float *>(xg_lo);
         st.args.planar_stride = rows_total;  // rows
         st.args.ksplit = ks1;
+        if (gp1) {
+            st.args.gsplit = gs1;
+            st.args.part = gpart1;
+            st.args.flags = gflag1;
+        }
         st.args.stages = tdc::bf_pick_stages(BN1, p->max_smem, 1, &st.args.xstages, ks1, &st.args.bstages);
         st.grid_n = R1 / BN1;
         st.args.ntiles = st.grid_n;
@@ -696,6 +787,11 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         g.ntiles = nt2; g.BN = BN2; g.nphase = nphase; g.band_rows = band_rows;
         g.tg = tg; g.ngroups = ngroups; g.w_slots = w_slots; g.w_resident = resident; g.ncat = ncat;
         g.ksplit = ks2;
+        if (gp2) {
+            g.gsplit = gs2;
+            g.part = gpart2;
+            g.flags = gflag2;
+        }
         g.phase_rows = phase_rows;
         for (int r = 0; r < K; ++r)
             for (int t = 0; t < K; ++t) {
@@ -721,6 +817,11 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
         st.args.M = (int)M3; st.args.Nn = N; st.args.kchunks = D2p / 64; st.args.taps = 1;
         st.args.BN = BN3; st.args.ldo = N; st.args.remap = 0; st.args.bias = dbias;
         st.args.ksplit = ks3;
+        if (gp3) {
+            st.args.gsplit = gs3;
+            st.args.part = gpart3;
+            st.args.flags = gflag3;
+        }
         st.args.stages = tdc::bf_pick_stages(BN3, p->max_smem, 0, nullptr, ks3, nullptr);
         {
             const char *ev = std::getenv("TDC_NO_TMA_Y");
@@ -766,8 +867,13 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
         const long long cap = (long long)p->num_sms * tdc::persistent_occupancy(smem, bn);
         return (int)std::max<long long>(1, std::min(tiles, cap));
     };
-    // split-K launches: clusters of ksplit CTAs, one cluster per output tile (persistent)
-    auto grid_ks = [&](long long M, int ntiles, int smem, int bn, int ks) {
+    // split-K launches: clusters of ksplit CTAs, one cluster per output tile (persistent);
+    // split-K through L2 (gsplit): one unit per (tile, piece), at most one CTA per SM so that
+    // every CTA is co-resident (a piece-0 CTA waits for its other pieces)
+    auto grid_ks = [&](long long M, int ntiles, int smem, int bn, int ks, int gs = 1) {
+        if (gs > 1)
+            return (int)std::max<long long>(1, std::min<long long>((long long)div_up((int)M, 128) * ntiles * gs,
+                                                                   p->num_sms));
         if (ks <= 1) return grid(M, ntiles, smem, bn);
         const long long tiles = (long long)div_up((int)M, 128) * ntiles;
         const long long cap = (long long)p->num_sms * tdc::persistent_occupancy(smem, bn) / ks;
@@ -775,7 +881,8 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
     };
     cudaError_t e = tdc::bf_gemm_launch(
         s1.mapA, s1.mapA, s1.mapB, s1.mapBlo, s1.mapA, a1,
-        grid_ks(a1.M, a1.ntiles, tdc::bf_smem_bytes(a1.BN, a1.stages, a1.xstages, a1.ksplit, a1.bstages), a1.BN, a1.ksplit), st);
+        grid_ks(a1.M, a1.ntiles, tdc::bf_smem_bytes(a1.BN, a1.stages, a1.xstages, a1.ksplit, a1.bstages), a1.BN, a1.ksplit,
+                a1.gsplit), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-1 launch");
     if (p->fuse3) {
         c.y = y;
@@ -786,7 +893,7 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
     }
     e = tdc::bf_core_launch(
         c, grid_ks(c.M, c.ntiles, tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots, c.ksplit),
-                   c.ncat ? 2 * c.BN : c.BN, c.ksplit), st);
+                   c.ncat ? 2 * c.BN : c.BN, c.ksplit, c.gsplit), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-2 launch");
     if (a3.tma_y && y != p->last_y3) {
         if (!tdc::make_tma_2d(&p->mapY3, y, (long long)p->desc.batch * d.Ho * d.Wo, d.N, d.N, 32))
@@ -795,7 +902,7 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
     }
     e = tdc::bf_gemm_launch(
         s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, p->mapY3, a3,
-        grid_ks(a3.M, a3.ntiles, tdc::bf_smem_bytes(a3.BN, a3.stages, 0, a3.ksplit, 0), a3.BN, a3.ksplit), st);
+        grid_ks(a3.M, a3.ntiles, tdc::bf_smem_bytes(a3.BN, a3.stages, 0, a3.ksplit, 0), a3.BN, a3.ksplit, a3.gsplit), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-3 launch");
     return TDC_OK;
 }
@@ -1208,6 +1315,9 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
         info->bn_stage3 = p->fuse3 ? c.N3p : p->tc[2].args.BN;
         info->ksplit_stage3 = p->fuse3 ? 1 : std::max(1, p->tc[2].args.ksplit);
         info->core3 = p->fuse3 ? 1 : 0;
+        info->gsplit_stage1 = std::max(1, p->tc[0].args.gsplit);
+        info->gsplit_core = std::max(1, c.gsplit);
+        info->gsplit_stage3 = p->fuse3 ? 1 : std::max(1, p->tc[2].args.gsplit);
         info->tile_w = c.BN;
         info->threads_per_cta = p->fuse3 ? 320 : 192;
         info->smem_bytes_per_cta = p->fuse3 ? tdc::bf_core3_smem_bytes(c)
@@ -1332,6 +1442,7 @@ tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t p) {
     cudaFree(p->d_fw);
     cudaFree(p->d_xg);
     cudaFree(p->d_z);
+    cudaFree(p->d_gs);
     delete p;
     return TDC_OK;
 }

@@ -178,6 +178,45 @@ __device__ __forceinline__ void red_signal(uint64_t *bar, int CS) {
     for (int k = 0; k < CS; ++k) mbar_arrive_cluster(mapa_shared(smem_u32(bar), k));
 }
 
+// ------------------------------------------------ split-K through L2 ("gsplit")
+// The K loop of an output tile is cut into GS fixed pieces (independent of the batch,
+// so a B = 1 forward equals a slice of a B = 32 one bit for bit).  Each (tile, piece)
+// is a work unit of the persistent grid; piece p > 0 writes its fp32 partial tile to
+// a plan-owned L2 workspace ([c/4][row][4] float4 planes, lane = row: coalesced) and
+// raises a flag; piece 0 (the lowest unit index of the tile) waits for the flags,
+// adds the partials in piece order (deterministic) and runs the normal epilogue, then
+// clears the flags for the next launch.  Units are dealt round-robin, so a piece-0
+// CTA only ever waits on units of higher index held by other CTAs: with all CTAs
+// co-resident (persistent grid) and grid >= GS this cannot deadlock.
+__device__ __forceinline__ void epi_bar128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void gs_store32(float *slot, int c, int row, const float *v) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        st_global_v4(slot + ((size_t)(c / 4 + j) * 128 + row) * 4,
+                     make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+}
+__device__ __forceinline__ void gs_add32(const float *slot, int c, int row, float *v) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const float4 f = __ldcg(reinterpret_cast<const float4 *>(slot + ((size_t)(c / 4 + j) * 128 + row) * 4));
+        v[4 * j] += f.x; v[4 * j + 1] += f.y; v[4 * j + 2] += f.z; v[4 * j + 3] += f.w;
+    }
+}
+__device__ __forceinline__ void gs_wait(const int *flag) {
+    int v;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v) break;
+        __nanosleep(32);
+    }
+}
+// after every epilogue thread stored its part of the partial: publish it
+__device__ __forceinline__ void gs_publish(int *flag, bool leader) {
+    __threadfence();
+    epi_bar128();
+    if (leader) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(1) : "memory");
+}
+
 // ============================================================ GEMM (stages 1, 3)
 constexpr int kConvThreads16 = 256;  // 8 converter warps (stage 1 is converter-paced otherwise)
 
@@ -229,7 +268,9 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     const int iters = g.taps * g.kchunks;
     const int crank = CS > 1 ? (int)cluster_ctarank() : 0;
     const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;  // cluster id / count
-    const int i0 = crank * iters / CS, i1 = (crank + 1) * iters / CS;  // this CTA's K range
+    const int ci0 = crank * iters / CS, ci1 = (crank + 1) * iters / CS;  // cluster split: this CTA's K range
+    const int GS = (CS == 1 && g.gsplit > 1) ? g.gsplit : 1;              // split-K through L2
+    const int num_units = num_tiles * GS;
 #ifdef TDC_TIMELINE
     const int seq = (int)*(volatile unsigned int *)&g_tdc_bf_seq;
 #endif
@@ -274,7 +315,9 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     if (warp == 0) {  // ------------------------------------- TMA producer
         Ring r(CONVERT ? SX : S), rb(CONVERT ? SB : 1);
         int tit = 0;
-        for (int t = cid; t < num_tiles; t += ncl, ++tit) {
+        for (int u = cid; u < num_units; u += ncl, ++tit) {
+            const int t = u / GS, pc = u - t * GS;
+            const int i0 = GS > 1 ? pc * iters / GS : ci0, i1 = GS > 1 ? (pc + 1) * iters / GS : ci1;
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
             int tap = i0 / g.kchunks, kc = i0 % g.kchunks;
             for (int i = i0; i < i1; ++i, r.next()) {
@@ -323,7 +366,9 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         const uint32_t lo = half >> 4, blo = (CONVERT ? b_tile : half) >> 4;
         Ring r(S), acc(2), rb(CONVERT ? SB : 1);
         int tit = 0;
-        for (int t = cid; t < num_tiles; t += ncl, acc.next(), ++tit) {
+        for (int u = cid; u < num_units; u += ncl, acc.next(), ++tit) {
+            const int pc = u % GS;
+            const int i0 = GS > 1 ? pc * iters / GS : ci0, i1 = GS > 1 ? (pc + 1) * iters / GS : ci1;
             mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
             tc_fence_after();
             if (lane == 0) BFTL(seq, tit, 1);  // MMA: accumulator free
@@ -361,7 +406,8 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         float *scratch = epi_scratch + q * 1024;
         Ring acc(2);
         int tit = 0;
-        for (int t = cid; t < num_tiles; t += ncl, acc.next(), ++tit) {
+        for (int u = cid; u < num_units; u += ncl, acc.next(), ++tit) {
+            const int t = u / GS, pc = u - t * GS;
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
             mbar_wait(&tfull[acc.slot], acc.phase);
             tc_fence_after();
@@ -417,6 +463,21 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                 if (warp == 2 && lane == 0) BFTL(seq, tit, 5);
                 continue;
             }
+            if (GS > 1 && pc > 0) {  // ---- split-K piece: fp32 partial -> L2 workspace
+                float *slot = g.part + (size_t)(t * (GS - 1) + pc - 1) * 128 * BN;
+                for (int c = 0; c < BN; c += 32) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(src + c, r);
+                    tmem_ld_wait();
+                    gs_store32(slot, c, q * 32 + lane, reinterpret_cast<const float *>(r));
+                }
+                tc_fence_before();
+                mbar_arrive_relaxed(&tempty[acc.slot]);
+                gs_publish(g.flags + t * (GS - 1) + pc - 1, warp == 2 && lane == 0);
+                continue;
+            }
+            if (GS > 1)
+                for (int pp = 1; pp < GS; ++pp) gs_wait(g.flags + t * (GS - 1) + pp - 1);
             long long dst_row = 0;
             const bool valid = remap_row(g, m0 + q * 32 + lane, &dst_row);
             for (int c = 0; c < BN; c += 32) {
@@ -428,6 +489,8 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                 float v[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                for (int pp = 1; pp < GS; ++pp)  // partials in piece order (deterministic)
+                    gs_add32(g.part + (size_t)(t * (GS - 1) + pp - 1) * 128 * BN, c, q * 32 + lane, v);
                 if (g.out_bf16) {  // X' hi/lo planar bf16: plane n/8 at (plane * stride + row) * 8
                     if (valid) {
                         __nv_bfloat16 *hi = reinterpret_cast<__nv_bfloat16 *>(g.out);
@@ -478,6 +541,11 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             }
             tc_fence_before();
             mbar_arrive_relaxed(&tempty[acc.slot]);
+            if (GS > 1) {  // every epilogue thread has read the partials: clear the flags
+                epi_bar128();
+                if (warp == 2 && lane == 0)
+                    for (int pp = 1; pp < GS; ++pp) g.flags[t * (GS - 1) + pp - 1] = 0;
+            }
             if (warp == 2 && lane == 0) BFTL(seq, tit, 5);  // epilogue: done
         }
         if (g.tma_y && lane == 0) bulk_wait_group0();  // TMA stores complete before the CTA retires
@@ -485,7 +553,9 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         const int tid = threadIdx.x - 192;
         Ring r(S), rx(SX);
         int tit = 0;
-        for (int t = cid; t < num_tiles; t += ncl, ++tit) {
+        for (int u = cid; u < num_units; u += ncl, ++tit) {
+            const int pc = u % GS;
+            const int i0 = GS > 1 ? pc * iters / GS : ci0, i1 = GS > 1 ? (pc + 1) * iters / GS : ci1;
             for (int i = i0; i < i1; ++i, r.next(), rx.next()) {
                 mbar_wait(&empty[r.slot], r.phase ^ 1);  // operand slot free
                 const uint32_t base = smem_u32(ops + (size_t)r.slot * slot_bytes);
@@ -654,7 +724,9 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
     const bool resident = g.w_resident != 0;
     const int crank = CS > 1 ? (int)cluster_ctarank() : 0;
     const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;                 // cluster id / count
-    const int k0 = crank * g.kchunks / CS, k1 = (crank + 1) * g.kchunks / CS;  // this CTA's chunks
+    const int ck0 = crank * g.kchunks / CS, ck1 = (crank + 1) * g.kchunks / CS;  // cluster split: chunks
+    const int GS = (!F3 && CS == 1 && g.gsplit > 1) ? g.gsplit : 1;                // split-K through L2
+    const int num_units = num_tiles * GS;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -719,7 +791,9 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         pdl_wait();  // X' is written by the previous kernel (stage 1)
         Ring ra(2), rw(WS);
         int tit = 0;
-        for (int t = cid; t < num_tiles; t += ncl, ++tit) {
+        for (int u = cid; u < num_units; u += ncl, ++tit) {
+            const int t = u / GS, pc = u - t * GS;
+            const int k0 = GS > 1 ? pc * g.kchunks / GS : ck0, k1 = GS > 1 ? (pc + 1) * g.kchunks / GS : ck1;
             const int m0 = (t % mtiles) * kBM16, nt = t / mtiles;
             for (int kc = k0; kc < k1; ++kc, ra.next()) {
                 mbar_wait_sleep(&a_empty[ra.slot], ra.phase ^ 1);
@@ -766,8 +840,10 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         int tit = 0;
         bool pending = false;  // F3: S3 of the previous tile still to issue
         if (F3) mbar_wait(w3_full, 0);
-        for (int t = cid;; t += ncl, ++tit) {
-            const bool have = t < num_tiles;
+        for (int u = cid;; u += ncl, ++tit) {
+            const bool have = u < num_units;
+            const int pc = u % GS;
+            const int k0 = GS > 1 ? pc * g.kchunks / GS : ck0, k1 = GS > 1 ? (pc + 1) * g.kchunks / GS : ck1;
             if (have) {
                 if (!(g.dbg & 16)) mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
                 tc_fence_after();
@@ -896,7 +972,8 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         const int r = q * 32 + lane;  // tile row = TMEM lane
         Ring acc(2), zr(2);
         int tit = 0;
-        for (int t = cid; t < num_tiles; t += ncl, acc.next(), zr.next(), ++tit) {
+        for (int u = cid; u < num_units; u += ncl, acc.next(), zr.next(), ++tit) {
+            const int t = u / GS, pc = u - t * GS;
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
             mbar_wait_sleep(&tfull[acc.slot], acc.phase);
             tc_fence_after();
@@ -948,6 +1025,9 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             if (F3) mbar_wait_sleep(&z_empty[zr.slot], zr.phase ^ 1);
             const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
             const uint32_t zb = smem_u32(zs) + zr.slot * zbuf;
+            const bool gpart = GS > 1 && pc > 0;  // split-K piece: fp32 partial -> L2 workspace
+            if (GS > 1 && pc == 0)
+                for (int pp = 1; pp < GS; ++pp) gs_wait(g.flags + t * (GS - 1) + pp - 1);
             for (int c = 0; c < ((g.dbg & 32) ? 0 : BN); c += 32) {
                 uint32_t rr[32];
                 float v[32];
@@ -963,6 +1043,12 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
                 }
+                if (gpart) {
+                    gs_store32(g.part + (size_t)(t * (GS - 1) + pc - 1) * 128 * BN, c, r, v);
+                    continue;
+                }
+                for (int pp = 1; pp < GS; ++pp)  // partials in piece order (deterministic)
+                    gs_add32(g.part + (size_t)(t * (GS - 1) + pp - 1) * 128 * BN, c, r, v);
                 if (F3 && (g.dbg & 2)) {
                 } else if (F3) {  // Z hi/lo planes [c/8 + pl][row r][16 B] (conflict-free: lanes = rows)
 #pragma unroll
@@ -994,6 +1080,13 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             }
             tc_fence_before();
             mbar_arrive_relaxed(&tempty[acc.slot]);
+            if (gpart) {
+                gs_publish(g.flags + t * (GS - 1) + pc - 1, warp == 2 && lane == 0);
+            } else if (GS > 1) {  // every epilogue thread has read the partials: clear the flags
+                epi_bar128();
+                if (warp == 2 && lane == 0)
+                    for (int pp = 1; pp < GS; ++pp) g.flags[t * (GS - 1) + pp - 1] = 0;
+            }
             if (F3) {
                 fence_proxy_async_smem();  // Z (generic writes) -> visible to the MMA (async proxy)
                 mbar_arrive(&z_full[zr.slot]);

@@ -46,10 +46,11 @@ class tdc_plan_info(ctypes.Structure):
                 ("ctas_per_image", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
                 ("weight_bytes", ctypes.c_int64)] + [(n, ctypes.c_int32) for n in (
                     "bn_stage1", "bn_core", "bn_stage3", "ksplit_stage1", "ksplit_core", "ksplit_stage3",
-                    "core3")]
+                    "core3", "gsplit_stage1", "gsplit_core", "gsplit_stage3")]
 
 
-HINT_FIELDS = ("core3", "bn_stage1", "bn_core", "bn_stage3", "ksplit_stage1", "ksplit_core", "ksplit_stage3")
+HINT_FIELDS = ("core3", "bn_stage1", "bn_core", "bn_stage3", "ksplit_stage1", "ksplit_core", "ksplit_stage3",
+               "gsplit_stage1", "gsplit_core", "gsplit_stage3")
 
 
 class tdc_plan_hints(ctypes.Structure):
@@ -210,6 +211,9 @@ class PlanInfo:
     ksplit_core: int = 0
     ksplit_stage3: int = 0
     core3: int = 0
+    gsplit_stage1: int = 1
+    gsplit_core: int = 1
+    gsplit_stage3: int = 1
 
 
 class ConvPlan:
@@ -234,7 +238,8 @@ class ConvPlan:
                         i.launches_per_forward, i.concurrent_forward, i.tile_h, i.tile_w,
                         i.threads_per_cta, i.smem_bytes_per_cta, i.ctas_per_image,
                         i.workspace_bytes, i.weight_bytes, i.bn_stage1, i.bn_core, i.bn_stage3,
-                        i.ksplit_stage1, i.ksplit_core, i.ksplit_stage3, i.core3)
+                        i.ksplit_stage1, i.ksplit_core, i.ksplit_stage3, i.core3,
+                        i.gsplit_stage1, i.gsplit_core, i.gsplit_stage3)
 
     @staticmethod
     def _stream_handle(stream) -> int:

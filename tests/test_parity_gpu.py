@@ -256,3 +256,52 @@ def test_3xbf16_wide_rank_large_m(env, shape):
     ref = oracle.tkd_points(d["x"], d["core"], d["u_in"], d["u_out"], pts, None, shape.stride, shape.pad)
     vals = np.array([got[p] for p in pts], dtype=np.float64)
     assert np.max(np.abs(vals - ref)) / np.max(np.abs(ref)) <= TOL["3xbf16"]
+
+
+@pytest.mark.parametrize("gs", [2, 3, 5])
+@pytest.mark.parametrize("shape", [
+    LayerShape(2, 512, 256, 5, 7, 256, 128, 3, 1, 1),
+    LayerShape(3, 256, 512, 4, 4, 128, 256, 3, 2, 1),
+    LayerShape(2, 320, 240, 9, 6, 160, 224, 3, 1, 1),
+], ids=lambda s: f"{s.C}_{s.N}_{s.H}x{s.W}_s{s.stride}")
+def test_3xbf16_l2_split_k(env, shape, gs, monkeypatch):
+    """Split-K through L2 (every stage cut into `gs` K pieces, partials reduced by the
+    piece-0 CTA in piece order) against the oracle; deterministic run to run; a
+    partial batch equals the slice of the full batch bit for bit (the pieces are fixed
+    by the plan, not by the batch)."""
+    torch, tdc = env
+    monkeypatch.setenv("TDC_NO_FUSE3", "1")
+    s = shape.with_batch(shape.B)
+    d = synth.make_layer(s, seed=17, bias=True)
+    hints = dict(gsplit_stage1=gs, gsplit_core=gs, gsplit_stage3=gs)
+
+    def run(batch):
+        plan = tdc.ConvPlan(s, d, math=tdc.TDC_MATH_3XBF16, hints=hints)
+        x = torch.from_numpy(synth.nchw_to_nhwc(d["x"])).cuda()
+        y = torch.full((s.B, s.Ho, s.Wo, s.N), float("nan"), device="cuda")
+        plan.forward(x, y, batch=batch)
+        torch.cuda.synchronize()
+        info = plan.info()
+        plan.close()
+        return synth.nhwc_to_nchw(y.cpu().numpy())[:batch], info
+
+    a, info = run(s.B)
+    assert info.gsplit_core > 1 and info.gsplit_stage1 > 1 and info.gsplit_stage3 > 1
+    b, _ = run(s.B)
+    assert np.array_equal(a, b)
+    part, _ = run(1)
+    assert np.array_equal(part, a[:1])
+    assert err(a, ref_of(s, d)) <= TOL["3xbf16"]
+
+
+@pytest.mark.parametrize("shape,count", synth.R18_SHAPES[4:], ids=[s.name for s, _ in synth.R18_SHAPES[4:]])
+def test_3xbf16_r18_small_layers_planned_split(env, shape, count):
+    """The 14x14 / 7x7 ResNet-18 layers at batch 32 (few output tiles, long K) as planned
+    (split-K through L2 where the planner picks it), sampled against the oracle."""
+    s = shape.with_batch(32)
+    d = synth.make_layer(s, seed=2, bias=True)
+    got, info = run_layer(env, s, d, "nhwc", "3xbf16")
+    pts = synth.sample_points(s, 300, seed=4)
+    ref = oracle.tkd_points(d["x"], d["core"], d["u_in"], d["u_out"], pts, d["bias"], s.stride, s.pad)
+    vals = np.array([got[p] for p in pts], dtype=np.float64)
+    assert np.max(np.abs(vals - ref)) / np.max(np.abs(ref)) <= TOL["3xbf16"]
