@@ -107,6 +107,8 @@ struct tdc_conv_plan_s {
     float *d_ws_in = nullptr, *d_ws_out = nullptr;
     size_t ws_bytes = 0;
     float *d_stage_x = nullptr, *d_stage_y = nullptr;
+    cudaStream_t s_in = nullptr, s_out = nullptr;  // host-forward pipeline: copy streams
+    cudaEvent_t ev[17] = {};                       // per-chunk H2D / forward done, entry
     // tensor-core variant (variant 2): three tcgen05 GEMM-with-taps launches
     struct TcStage {
         tdc::TcGemmArgs args;
@@ -1414,18 +1416,49 @@ tdc_status tdc_conv_forward_host(tdc_conv_plan_t p, const float *x_host, float *
     if (!p->d_stage_x) {
         const size_t max_in = (size_t)p->desc.batch * d.C * d.H * d.W * sizeof(float);
         const size_t max_out = (size_t)p->desc.batch * d.N * d.Ho * d.Wo * sizeof(float);
-        e = cudaMalloc(&p->d_stage_x, max_in);
+        // + 256 pixel rows of slack: the last chunk of the pipeline below starts mid-buffer and
+        // the row-tiled TMA maps (extent = the plan's batch) may read a partial tile past it
+        e = cudaMalloc(&p->d_stage_x, max_in + (size_t)256 * d.C * sizeof(float));
         if (e == cudaSuccess) e = cudaMalloc(&p->d_stage_y, max_out);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(host-forward staging)");
     }
     cudaStream_t st = (cudaStream_t)stream;
-    e = cudaMemcpyAsync(p->d_stage_x, x_host, in_b, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(H2D)");
-    tdc_status s = tdc_conv_forward(p, p->d_stage_x, p->d_stage_y, batch, stream);
-    if (s != TDC_OK) return s;
-    e = cudaMemcpyAsync(y_host, p->d_stage_y, out_b, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(D2H)");
-    e = cudaStreamSynchronize(st);
+    // Pipeline over image chunks (images are independent): the H2D copy of
+    // chunk k+1 (copy stream s_in) and the D2H copy of chunk k-1 (s_out) overlap the
+    // forward of chunk k on the caller's stream, so the two link directions run
+    // concurrently instead of back to back.  Chunks of >= ~2 MB of traffic, at most 8.
+    const int nch = std::max(1, std::min<int>({batch, 8, (int)((in_b + out_b) / (2u << 20))}));
+    if (!p->s_in) {
+        e = cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking);
+        for (int i = 0; e == cudaSuccess && i < 17; ++i) e = cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate/cudaEventCreate (host-forward pipeline)");
+    }
+    const size_t in_img = in_b / batch, out_img = out_b / batch;
+    cudaEvent_t ev_start = p->ev[16];
+    e = cudaEventRecord(ev_start, st);  // earlier work on the caller's stream comes first
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_in, ev_start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_out, ev_start, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord/cudaStreamWaitEvent");
+    for (int k = 0; k < nch; ++k) {
+        const int b0 = (int)((long long)k * batch / nch), nb = (int)((long long)(k + 1) * batch / nch) - b0;
+        float *dx = p->d_stage_x + b0 * (in_img / sizeof(float)), *dy = p->d_stage_y + b0 * (out_img / sizeof(float));
+        e = cudaMemcpyAsync(dx, reinterpret_cast<const uint8_t *>(x_host) + b0 * in_img, nb * in_img,
+                            cudaMemcpyHostToDevice, p->s_in);
+        if (e == cudaSuccess) e = cudaEventRecord(p->ev[2 * k], p->s_in);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, p->ev[2 * k], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+        const tdc_status s = tdc_conv_forward(p, dx, dy, nb, stream);
+        if (s != TDC_OK) return s;
+        e = cudaEventRecord(p->ev[2 * k + 1], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_out, p->ev[2 * k + 1], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(reinterpret_cast<uint8_t *>(y_host) + b0 * out_img, dy, nb * out_img,
+                                cudaMemcpyDeviceToHost, p->s_out);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(D2H)");
+    }
+    e = cudaStreamSynchronize(p->s_out);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
     return TDC_OK;
 }
@@ -1438,6 +1471,11 @@ tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t p) {
     cudaFree(p->d_ws_out);
     cudaFree(p->d_stage_x);
     cudaFree(p->d_stage_y);
+    if (p->s_in) {
+        cudaStreamDestroy(p->s_in);
+        cudaStreamDestroy(p->s_out);
+        for (cudaEvent_t ev : p->ev) cudaEventDestroy(ev);
+    }
     cudaFree(p->d_tc_w);
     cudaFree(p->d_fw);
     cudaFree(p->d_xg);

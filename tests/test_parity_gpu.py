@@ -305,3 +305,30 @@ def test_3xbf16_r18_small_layers_planned_split(env, shape, count):
     ref = oracle.tkd_points(d["x"], d["core"], d["u_in"], d["u_out"], pts, d["bias"], s.stride, s.pad)
     vals = np.array([got[p] for p in pts], dtype=np.float64)
     assert np.max(np.abs(vals - ref)) / np.max(np.abs(ref)) <= TOL["3xbf16"]
+
+
+@pytest.mark.parametrize("math,layout", [("3xbf16", "nhwc"), ("tf32", "nhwc"), ("fp32", "nchw")])
+def test_forward_host_pipelined_chunks(env, math, layout):
+    """tdc_conv_forward_host splits a large batch into image chunks whose H2D copy,
+    forward and D2H copy overlap on three streams; the result equals the device-buffer
+    forward of the whole batch bit for bit (images are independent)."""
+    torch, tdc = env
+    s = synth.R18_SHAPES[0][0].with_batch(8)  # 56x56x64: ~13 MB of traffic -> 6 chunks
+    d = synth.make_layer(s, seed=31, bias=True)
+    lay = tdc.TDC_LAYOUT_NHWC if layout == "nhwc" else tdc.TDC_LAYOUT_NCHW
+    plan = tdc.ConvPlan(s, d, layout=lay, math=tdc.MATH_NAMES[math])
+    xn = synth.nchw_to_nhwc(d["x"]) if layout == "nhwc" else np.ascontiguousarray(d["x"])
+    yshape = (s.B, s.Ho, s.Wo, s.N) if layout == "nhwc" else (s.B, s.N, s.Ho, s.Wo)
+    xh = torch.from_numpy(xn).pin_memory()
+    yh = torch.full(yshape, float("nan")).pin_memory()
+    plan.forward_host(xh, yh)
+    plan.forward_host(xh, yh)  # twice: the pipeline's streams/events are reused
+    xd = torch.from_numpy(xn).cuda()
+    yd = torch.full(yshape, float("nan"), device="cuda")
+    plan.forward(xd, yd)
+    torch.cuda.synchronize()
+    plan.close()
+    assert np.array_equal(yh.numpy(), yd.cpu().numpy())
+    ref = ref_of(s, d)
+    got = synth.nhwc_to_nchw(yh.numpy()) if layout == "nhwc" else yh.numpy()
+    assert err(got, ref) <= TOL[math]
