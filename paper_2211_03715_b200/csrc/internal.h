@@ -123,11 +123,15 @@ bool fused_make_x_map(CUtensorMap *map, const float *x, const FusedArgs &g);
 cudaError_t fused_launch(const CUtensorMap &mapX, const FusedArgs &g, int grid, cudaStream_t st);
 
 // ---- 3xBF16 variant of the 3-launch path (tkd_bf16.cu) ----
-int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages);
-int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, int *bstages);
+// fp32_out: a converting (xstages > 0) GEMM with fp32 output (model dense convs) reserves
+// its TMA output ring; stage 1 (bf16 X' output) does not.
+int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages, int fp32_out = 0);
+int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, int *bstages, int fp32_out = 0);
+// mapR: fp32-output GEMMs with a residual and tma_y: TMA map of the residual (same
+// geometry as mapY); null = no residual map (mapY is passed in its place).
 cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, const CUtensorMap &mapB,
                            const CUtensorMap &mapBlo, const CUtensorMap &mapY, const TcGemmArgs &g, int grid,
-                           cudaStream_t st);
+                           cudaStream_t st, const CUtensorMap *mapR = nullptr);
 // 3xBF16 stage-2 core convolution (tkd_bf16.cu).  X' hi/lo planar bf16
 // [D1s/8][rows_total][8]; weights blocked [kc][ntile][group][tg taps][plane 4][2BN][8]
 // with rows 0..BN-1 = hi and BN..2BN-1 = lo, so one bulk copy moves a whole

@@ -131,12 +131,17 @@ struct tdc_conv_plan_s {
     tdc_plan_hints hints = {-1, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // planner overrides (tdc_conv_plan_ex)
     CUtensorMap mapY3;             // 3xBF16 stage 3: TMA map of the output (per y pointer)
     const float *last_y3 = nullptr;
+    long long last_y3_rows = 0;
+    CUtensorMap mapR3;             // 3xBF16 stage 3: TMA map of the residual (tdc_conv_forward_ex)
+    const float *last_r3 = nullptr;
+    long long last_r3_rows = 0;
     float *d_tc_w = nullptr;       // Bt1 | Bt2 | Bt3 | bias
     float *d_xg = nullptr;         // X' phase grids (zero borders)
     float *d_z = nullptr;          // Z compact
     float *d_gs = nullptr;         // 3xBF16 split-K through L2: partial tiles | flags
     size_t tc_ws_bytes = 0;
     const float *tc_last_x = nullptr;
+    int tc_last_x_batch = 0;
     int max_smem = 0;
 };
 
@@ -848,11 +853,13 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
                         const float *res = nullptr, int relu = 0) {
     const tdc::LayerDims &d = p->dims;
     auto &s1 = p->tc[0], &s3 = p->tc[2];
-    if (x != p->tc_last_x) {
-        if (!tdc::make_tma_2d(&s1.mapA, x, (long long)p->desc.batch * d.H * d.W, d.C, d.C, 128))
+    if (x != p->tc_last_x || batch != p->tc_last_x_batch) {
+        // extent = this call's images: a partial last tile is zero-filled, not read past x
+        if (!tdc::make_tma_2d(&s1.mapA, x, (long long)batch * d.H * d.W, d.C, d.C, 128))
             return fail(TDC_ERR_INVALID_ARGUMENT,
                         "cuTensorMapEncodeTiled rejected x (needs 16-byte aligned pointer)");
         p->tc_last_x = x;
+        p->tc_last_x_batch = batch;
     }
     tdc::TcGemmArgs a1 = s1.args, a3 = s3.args;
     a1.M = batch * d.H * d.W;
@@ -897,14 +904,23 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
         c, grid_ks(c.M, c.ntiles, tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots, c.ksplit),
                    c.ncat ? 2 * c.BN : c.BN, c.ksplit, c.gsplit), st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-2 launch");
-    if (a3.tma_y && y != p->last_y3) {
-        if (!tdc::make_tma_2d(&p->mapY3, y, (long long)p->desc.batch * d.Ho * d.Wo, d.N, d.N, 32))
+    if (a3.tma_y && (y != p->last_y3 || a3.M != p->last_y3_rows)) {
+        // extent = this call's rows, so the stores of the last tile clip at the batch end
+        if (!tdc::make_tma_2d(&p->mapY3, y, a3.M, d.N, d.N, 32))
             return fail(TDC_ERR_INVALID_ARGUMENT, "cuTensorMapEncodeTiled rejected y (16-byte aligned pointer?)");
         p->last_y3 = y;
+        p->last_y3_rows = a3.M;
+    }
+    if (a3.tma_y && res && (res != p->last_r3 || a3.M != p->last_r3_rows)) {  // residual blocks by TMA
+        if (!tdc::make_tma_2d(&p->mapR3, res, a3.M, d.N, d.N, 32))
+            return fail(TDC_ERR_INVALID_ARGUMENT, "cuTensorMapEncodeTiled rejected residual (16-byte aligned?)");
+        p->last_r3 = res;
+        p->last_r3_rows = a3.M;
     }
     e = tdc::bf_gemm_launch(
         s3.mapA, s3.mapAlo, s3.mapB, s3.mapBlo, p->mapY3, a3,
-        grid_ks(a3.M, a3.ntiles, tdc::bf_smem_bytes(a3.BN, a3.stages, 0, a3.ksplit, 0), a3.BN, a3.ksplit, a3.gsplit), st);
+        grid_ks(a3.M, a3.ntiles, tdc::bf_smem_bytes(a3.BN, a3.stages, 0, a3.ksplit, 0), a3.BN, a3.ksplit, a3.gsplit), st,
+        res ? &p->mapR3 : nullptr);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-3 launch");
     return TDC_OK;
 }
@@ -1076,11 +1092,13 @@ tdc_status forward_fused(tdc_conv_plan_s *p, const float *x, float *y, int batch
 tdc_status forward_tc(tdc_conv_plan_s *p, const float *x, float *y, int batch, cudaStream_t st) {
     const tdc::LayerDims &d = p->dims;
     auto &s1 = p->tc[0], &s2 = p->tc[1], &s3 = p->tc[2];
-    if (x != p->tc_last_x) {
-        if (!tdc::make_tma_2d(&s1.mapA, x, (long long)p->desc.batch * d.H * d.W, d.C, d.C, 128))
+    if (x != p->tc_last_x || batch != p->tc_last_x_batch) {
+        // extent = this call's images: a partial last tile is zero-filled, not read past x
+        if (!tdc::make_tma_2d(&s1.mapA, x, (long long)batch * d.H * d.W, d.C, d.C, 128))
             return fail(TDC_ERR_INVALID_ARGUMENT,
                         "cuTensorMapEncodeTiled rejected x (needs 16-byte aligned pointer)");
         p->tc_last_x = x;
+        p->tc_last_x_batch = batch;
     }
     tdc::TcGemmArgs a1 = s1.args, a2 = s2.args, a3 = s3.args;
     a1.M = batch * d.H * d.W;

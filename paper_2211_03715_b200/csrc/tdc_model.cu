@@ -170,6 +170,10 @@ struct DenseOp {
     long long mapA_rows = 0;
     CUtensorMap mapY;        // TMA map of the output (tma_y), re-encoded when dst changes
     const float *mapY_dst = nullptr;
+    long long mapY_rows = 0;  // the map's row extent = this call's rows (TMA stores clip there)
+    CUtensorMap mapR;        // TMA map of the residual (tma_y with a residual)
+    const float *mapR_src = nullptr;
+    long long mapR_rows = 0;
 };
 
 }  // namespace
@@ -281,7 +285,7 @@ tdc_status plan_dense(tdc_model_s *m, ModelOp &op, const tdc_model_op &o) {
     tdc::TcGemmArgs &a = g.args;
     a.Nn = N; a.kchunks = K64 / 64; a.taps = 1; a.BN = BN; a.remap = 0; a.a_convert = 1; a.out_bf16 = 0;
     a.ldo = N; a.bias = g.d_bias; a.relu = o.relu; a.ntiles = R / BN; a.ksplit = 1;
-    a.stages = tdc::bf_pick_stages(BN, m->max_smem, 1, &a.xstages, 1, &a.bstages);
+    a.stages = tdc::bf_pick_stages(BN, m->max_smem, 1, &a.xstages, 1, &a.bstages, 1);
     if (const char *dbg = std::getenv("TDC_GEMM_DBG")) a.dbg = std::atoi(dbg);
     {
         const char *ev = std::getenv("TDC_NO_TMA_Y");
@@ -331,16 +335,26 @@ tdc_status run_dense(tdc_model_s *m, ModelOp &op, const float *src, float *dst, 
     a.M = (int)M;
     a.out = dst;
     a.res = res;
-    const int smem = tdc::bf_smem_bytes(a.BN, a.stages, a.xstages, 1, a.bstages);
+    const int smem = tdc::bf_smem_bytes(a.BN, a.stages, a.xstages, 1, a.bstages, 1);
     const long long tiles = (long long)div_up((int)M, 128) * a.ntiles;
     const long long cap = (long long)m->num_sms * tdc::persistent_occupancy(smem, a.BN);
     const int grid = (int)std::max<long long>(1, std::min(tiles, cap));
-    if (a.tma_y && dst != g.mapY_dst) {
-        if (!tdc::make_tma_2d(&g.mapY, dst, rows, op.Co, op.Co, 32))
+    if (a.tma_y && (dst != g.mapY_dst || M != g.mapY_rows)) {
+        // extent = this call's rows: the last tile's 32-row blocks past M are clipped, not
+        // written past a partial batch
+        if (!tdc::make_tma_2d(&g.mapY, dst, M, op.Co, op.Co, 32))
             return mfail(TDC_ERR_INVALID_ARGUMENT, "cuTensorMapEncodeTiled rejected a dense-op output");
         g.mapY_dst = dst;
+        g.mapY_rows = M;
     }
-    cudaError_t e = tdc::bf_gemm_launch(g.mapA, g.mapA, g.mapB, g.mapBlo, a.tma_y ? g.mapY : g.mapA, a, grid, st);
+    if (a.tma_y && res && (res != g.mapR_src || M != g.mapR_rows)) {
+        if (!tdc::make_tma_2d(&g.mapR, res, M, op.Co, op.Co, 32))
+            return mfail(TDC_ERR_INVALID_ARGUMENT, "cuTensorMapEncodeTiled rejected a residual input");
+        g.mapR_src = res;
+        g.mapR_rows = M;
+    }
+    cudaError_t e = tdc::bf_gemm_launch(g.mapA, g.mapA, g.mapB, g.mapBlo, a.tma_y ? g.mapY : g.mapA, a, grid, st,
+                                        (a.tma_y && res) ? &g.mapR : nullptr);
     if (e != cudaSuccess) return mcuda(e, "dense GEMM launch");
     return TDC_OK;
 }

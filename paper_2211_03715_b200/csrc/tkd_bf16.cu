@@ -103,6 +103,17 @@ constexpr int kBK16 = 64;                       // bf16 elements per K chunk = o
 constexpr int kATile16 = kBM16 * kBK16 * 2;     // 16 KB per hi or lo tile
 constexpr int kStage32 = kBM16 * 32 * 4 * 2;    // fp32 staging of one 64-channel chunk (2 boxes)
 constexpr int kEpiScratch16 = 4 * 4096;
+// fp32-output GEMMs (stage 3, model dense convs): each epilogue warp owns a ring of
+// kYRing 4 KB buffers; 32 x 32 output blocks are staged there (128B-swizzled) and
+// stored by TMA with up to kYRing - 1 stores in flight, and the residual block of the
+// next chunk is TMA-loaded into the ring ahead of use (no synchronous global reads).
+// (ring of 4 for stage 3; 2 for the converting dense convs of the model path, whose fp32
+// staging ring already takes most of shared memory)
+constexpr int kYRing = 4;
+__host__ __device__ constexpr int bf_yring(bool convert) { return convert ? 2 : kYRing; }
+__host__ __device__ inline int bf_epi_bytes(bool convert, bool out_bf16) {
+    return (convert && out_bf16) ? kEpiScratch16 : 4 * bf_yring(convert) * 4096;
+}
 
 // 32 rows x 64 bytes (32 bf16) per warp, row `lane` held by lane `lane` as 16
 // packed words; transposed through shared memory so each global store covers
@@ -224,7 +235,8 @@ template <bool CONVERT>
 __global__ void __launch_bounds__(CONVERT ? 192 + kConvThreads16 : 192, 1)
 tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo,
-                   const __grid_constant__ CUtensorMap mapY, const TcGemmArgs g) {
+                   const __grid_constant__ CUtensorMap mapY, const __grid_constant__ CUtensorMap mapR,
+                   const TcGemmArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -245,7 +257,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     float *epi_scratch = reinterpret_cast<float *>(bring + (size_t)SB * bslot);
     // split-K (cluster of CS CTAs over K): fp32 partial tile [128][BN], float4-swizzled
     const int CS = g.ksplit > 1 ? g.ksplit : 1;
-    float *red = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(epi_scratch) + kEpiScratch16);
+    float *red = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(epi_scratch) + bf_epi_bytes(CONVERT, g.out_bf16));
     uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(red) +
                                                   (CS > 1 ? (size_t)128 * BN * 4 : 0));
     uint64_t *conv = full + S;       // CONVERT: A hi/lo written by the converter
@@ -258,7 +270,8 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     uint64_t *bempty = bfull + SB;
     uint64_t *red_ready = bempty + SB;  // split-K: all CS partials of the tile written
     uint64_t *red_free = red_ready + 1; // split-K: all CS readers done with this CTA's partial
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(red_free + 1);
+    uint64_t *rbar = red_free + 1;      // fp32 output: residual block landed in ring buffer [warp][slot]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rbar + 4 * kYRing);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t ncols = 32;
@@ -295,6 +308,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         }
         mbar_init(red_ready, CS * 128);
         mbar_init(red_free, CS * 128);
+        for (int i = 0; i < 4 * kYRing; ++i) mbar_init(&rbar[i], 1);
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -403,12 +417,32 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         }
     } else if (warp < 6) {  // --------------------------------- epilogue
         const int q = warp & 3;
-        float *scratch = epi_scratch + q * 1024;
+        constexpr int NR = bf_yring(CONVERT);
+        float *scratch = epi_scratch + q * (g.out_bf16 ? 1024 : NR * 1024);
+        // fp32 output ring (tma_y): chunk counter of this warp -> buffer and residual parity
+        const bool ring = !g.out_bf16 && g.tma_y && (g.ldo & 3) == 0;
+        const bool rres = ring && g.res && !(g.dbg & 2);
+        const uint32_t ring_s = smem_u32(scratch);
+        uint32_t yc = 0;
+        auto full_chunk = [&](int n) { return n + 32 <= g.Nn; };
+        // TMA-load the residual block (columns n, rows r0..r0+31) into ring buffer of chunk k;
+        // `pend` = TMA stores that may still be reading when the buffer's last store is done
+        auto res_load = [&](uint32_t k, int n, int r0, bool first) {
+            if (lane == 0) {
+                if (first) bulk_wait_group_read<NR - 1>();
+                else bulk_wait_group_read<NR - 2>();
+                const uint32_t b = k % NR;
+                mbar_arrive_expect_tx(&rbar[q * kYRing + b], 4096);
+                tma_load_2d(scratch + b * 1024, &mapR, &rbar[q * kYRing + b], n, r0);
+            }
+        };
         Ring acc(2);
         int tit = 0;
         for (int u = cid; u < num_units; u += ncl, acc.next(), ++tit) {
             const int t = u / GS, pc = u - t * GS;
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
+            // the tile's first residual block is in flight while the MMAs finish
+            if (rres && (GS == 1 || pc == 0) && full_chunk(n0)) res_load(yc, n0, m0 + q * 32, true);
             mbar_wait(&tfull[acc.slot], acc.phase);
             tc_fence_after();
             if (warp == 2 && lane == 0) BFTL(seq, tit, 4);  // epilogue: accumulator ready
@@ -504,6 +538,37 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                             *reinterpret_cast<uint4 *>(lo + off) = l;
                         }
                     }
+                } else if (ring && full_chunk(n)) {  // fp32 Y through the per-warp TMA ring
+                    const uint32_t b = yc % NR, buf = ring_s + b * 4096;
+                    const bool nxt = c + 32 < BN && full_chunk(n + 32);
+                    if (rres && nxt) res_load(yc + 1, n + 32, m0 + q * 32, false);
+                    else if (!rres && lane == 0) bulk_wait_group_read<NR - 1>();  // buffer b free
+                    __syncwarp();
+                    if (rres) {
+                        mbar_wait(&rbar[q * kYRing + b], (yc / NR) & 1);
+#pragma unroll
+                        for (int j4 = 0; j4 < 8; ++j4) {
+                            const float4 f = ld_shared_v4(buf + (uint32_t)(lane * 128 + ((j4 ^ (lane & 7)) << 4)));
+                            v[4 * j4] += f.x; v[4 * j4 + 1] += f.y; v[4 * j4 + 2] += f.z; v[4 * j4 + 3] += f.w;
+                        }
+                    }
+                    epi_bias_res_relu<32>(v, n, g.Nn, g.bias, nullptr, g.relu);
+                    if (!(g.dbg & 1)) {
+#pragma unroll
+                        for (int j4 = 0; j4 < 8; ++j4)
+                            st_shared_v4(buf + (uint32_t)(lane * 128 + ((j4 ^ (lane & 7)) << 4)), v[4 * j4],
+                                         v[4 * j4 + 1], v[4 * j4 + 2], v[4 * j4 + 3]);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&mapY, scratch + b * 1024, n, m0 + q * 32);
+                            bulk_commit_group();
+                        }
+                    } else {
+                        __syncwarp();
+                        if (lane == 0) bulk_commit_group();  // keep the group count in step
+                    }
+                    ++yc;
                 } else {  // fp32 Y (+bias, +residual, ReLU), row-major, coalesced through shared memory
                     const bool full = n + 32 <= g.Nn && (g.ldo & 3) == 0;
                     if (g.dbg & 1) continue;
@@ -549,6 +614,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             if (warp == 2 && lane == 0) BFTL(seq, tit, 5);  // epilogue: done
         }
         if (g.tma_y && lane == 0) bulk_wait_group0();  // TMA stores complete before the CTA retires
+        (void)res_load;
     } else if (CONVERT) {  // ----------------- converter: fp32 staging -> bf16 hi/lo A tiles
         const int tid = threadIdx.x - 192;
         Ring r(S), rx(SX);
@@ -600,20 +666,21 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
 
 // xstages > 0 (converting stage 1): xstages fp32 staging slots, `stages` A slots and
 // bstages weight slots; otherwise `stages` combined A|B slots.
-int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages) {
+int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages, int fp32_out) {
     const int b_tile = BN * kBK16 * 2;
     const int ops = xstages ? stages * 2 * kATile16 + bstages * 2 * b_tile : stages * 2 * (kATile16 + b_tile);
-    return 1024 + xstages * kStage32 + ops + kEpiScratch16 + (ksplit > 1 ? 128 * BN * 4 : 0) +
-           (3 * stages + 4 + 2 * xstages + 2 * bstages + 2) * 8 + 16;
+    return 1024 + xstages * kStage32 + ops + bf_epi_bytes(xstages > 0, xstages > 0 && !fp32_out) +
+           (ksplit > 1 ? 128 * BN * 4 : 0) +
+           (3 * stages + 4 + 2 * xstages + 2 * bstages + 2 + 4 * kYRing) * 8 + 16;
 }
 
 // Ring depths: operand slots (and, for the converting stage 1, the fp32 staging and
 // weight rings).
-int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, int *bstages) {
+int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, int *bstages, int fp32_out) {
     int s = convert ? 2 : 6, sx = convert ? 4 : 0, sb = convert ? 4 : 0;
-    while (sx > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb) > max_smem) --sx;
-    while (sb > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb) > max_smem) --sb;
-    while (s > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb) > max_smem) --s;
+    while (sx > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb, fp32_out) > max_smem) --sx;
+    while (sb > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb, fp32_out) > max_smem) --sb;
+    while (s > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb, fp32_out) > max_smem) --s;
     if (xstages) *xstages = sx;
     if (bstages) *bstages = sb;
     return s;
@@ -621,19 +688,21 @@ int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, 
 
 cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, const CUtensorMap &mapB,
                            const CUtensorMap &mapBlo, const CUtensorMap &mapY, const TcGemmArgs &g, int grid,
-                           cudaStream_t st) {
-    const int smem = bf_smem_bytes(g.BN, g.stages, g.a_convert ? g.xstages : 0, g.ksplit, g.a_convert ? g.bstages : 0);
+                           cudaStream_t st, const CUtensorMap *mapR) {
+    if (!mapR) mapR = &mapY;
+    const int smem = bf_smem_bytes(g.BN, g.stages, g.a_convert ? g.xstages : 0, g.ksplit, g.a_convert ? g.bstages : 0,
+                                   !g.out_bf16);
     cudaError_t e;
     if (g.a_convert) {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         return launch_pdl_cluster(tdc_bf_gemm_kernel<true>, grid, 192 + kConvThreads16, smem, st, g.ksplit, mapA,
-                                  mapAlo, mapB, mapBlo, mapY, g);
+                                  mapAlo, mapB, mapBlo, mapY, *mapR, g);
     } else {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         return launch_pdl_cluster(tdc_bf_gemm_kernel<false>, grid, 192, smem, st, g.ksplit, mapA, mapAlo, mapB,
-                                  mapBlo, mapY, g);
+                                  mapBlo, mapY, *mapR, g);
     }
     return cudaGetLastError();
 }
