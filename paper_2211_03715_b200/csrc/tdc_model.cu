@@ -154,6 +154,102 @@ __global__ void __launch_bounds__(128) tdc_direct_conv_kernel(const float *__res
     }
 }
 
+// The 3-channel stems (ResNet 7x7/2, VGG 3x3/1) with 64 outputs, specialised: a block
+// computes an 8 x 32 output tile from a zero-padded input patch staged in shared memory
+// (no bounds checks in the loop).  Warp w owns output channels [16w, 16w + 16) (so its
+// weight reads are broadcasts), lane l the 8 pixels of tile column l: per tap and input
+// channel, 8 scalar x loads and 4 float4 weight loads feed 128 FMAs.  The finished tile
+// is transposed through shared memory and written as contiguous 8 KB pixel rows.
+constexpr int kStemTH = 8, kStemTW = 32;
+template <int K, int S>
+__host__ __device__ constexpr int stem_smem_floats() {
+    return (K * K * 3 * 64 + ((kStemTH - 1) * S + K) * ((kStemTW - 1) * S + K) * 3) > kStemTH * kStemTW * 64
+               ? (K * K * 3 * 64 + ((kStemTH - 1) * S + K) * ((kStemTW - 1) * S + K) * 3)
+               : kStemTH * kStemTW * 64;
+}
+template <int K, int S>
+__global__ void __launch_bounds__(128) tdc_stem_kernel(const float *__restrict__ x, const float *__restrict__ w,
+                                                        const float *__restrict__ bias, float *__restrict__ y, int H,
+                                                        int W, int p, int Ho, int Wo, int relu) {
+    constexpr int C = 3, N = 64, PH = (kStemTH - 1) * S + K, PW = (kStemTW - 1) * S + K;
+    extern __shared__ float sm[];
+    float *ws = sm;                    // [K*K*C][64]
+    float *xs = sm + K * K * C * N;    // [PH][PW][C], zero outside the image
+    const int tiles_x = (Wo + kStemTW - 1) / kStemTW, tiles_y = (Ho + kStemTH - 1) / kStemTH;
+    const int tx = blockIdx.x % tiles_x, ty = (blockIdx.x / tiles_x) % tiles_y, b = blockIdx.x / (tiles_x * tiles_y);
+    for (int i = threadIdx.x; i < K * K * C * N / 4; i += blockDim.x)
+        reinterpret_cast<float4 *>(ws)[i] = __ldg(reinterpret_cast<const float4 *>(w) + i);
+    const int iy0 = ty * kStemTH * S - p, ix0 = tx * kStemTW * S - p;
+    for (int i = threadIdx.x; i < PH * PW; i += blockDim.x) {
+        const int py = i / PW, px = i % PW, iy = iy0 + py, ix = ix0 + px;
+        const bool in = iy >= 0 && iy < H && ix >= 0 && ix < W;
+        const float *src = x + (((size_t)b * H + (in ? iy : 0)) * W + (in ? ix : 0)) * C;
+#pragma unroll
+        for (int c = 0; c < C; ++c) xs[i * C + c] = in ? __ldg(src + c) : 0.f;
+    }
+    __syncthreads();
+    const int wq = threadIdx.x >> 5, col = threadIdx.x & 31;
+    float acc[kStemTH][16];
+#pragma unroll
+    for (int i = 0; i < kStemTH; ++i)
+#pragma unroll
+        for (int n = 0; n < 16; ++n) acc[i][n] = 0.f;
+#pragma unroll 1
+    for (int r = 0; r < K; ++r) {
+#pragma unroll
+        for (int t = 0; t < K; ++t)
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const float4 *wr = reinterpret_cast<const float4 *>(ws + ((r * K + t) * C + c) * N + 16 * wq);
+                const float4 w0 = wr[0], w1 = wr[1], w2 = wr[2], w3 = wr[3];
+                const float wv[16] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w,
+                                      w2.x, w2.y, w2.z, w2.w, w3.x, w3.y, w3.z, w3.w};
+#pragma unroll
+                for (int i = 0; i < kStemTH; ++i) {
+                    const float xv = xs[((i * S + r) * PW + col * S + t) * C + c];
+#pragma unroll
+                    for (int n = 0; n < 16; ++n) acc[i][n] = fmaf(xv, wv[n], acc[i][n]);
+                }
+            }
+    }
+    __syncthreads();  // done with the weights / patch: reuse shared memory for the output tile
+    float *ys = sm;   // [TH][TW][64], 16-byte chunks of a pixel rotated by the pixel index
+#pragma unroll
+    for (int i = 0; i < kStemTH; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int px = i * kStemTW + col, ch4 = (wq * 4 + j + px) & 15;
+            float4 v = make_float4(acc[i][4 * j] + bias[16 * wq + 4 * j], acc[i][4 * j + 1] + bias[16 * wq + 4 * j + 1],
+                                   acc[i][4 * j + 2] + bias[16 * wq + 4 * j + 2], acc[i][4 * j + 3] + bias[16 * wq + 4 * j + 3]);
+            if (relu) {
+                v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+            }
+            reinterpret_cast<float4 *>(ys)[px * 16 + ch4] = v;
+        }
+    __syncthreads();
+    const int ox0 = tx * kStemTW, nx = min(kStemTW, Wo - ox0);
+    for (int i = 0; i < kStemTH; ++i) {
+        const int oy = ty * kStemTH + i;
+        if (oy >= Ho) break;
+        float4 *dst = reinterpret_cast<float4 *>(y + (((size_t)b * Ho + oy) * Wo + ox0) * N);
+        for (int e = threadIdx.x; e < nx * 16; e += blockDim.x) {  // contiguous row of nx pixels
+            const int px = i * kStemTW + e / 16, ch4 = e % 16;
+            dst[e] = reinterpret_cast<const float4 *>(ys)[px * 16 + ((ch4 + px) & 15)];
+        }
+    }
+}
+
+template <int K, int S>
+cudaError_t stem_launch(const float *x, const float *w, const float *bias, float *y, int B, int H, int W, int p,
+                        int Ho, int Wo, int relu, cudaStream_t st) {
+    const int smem = stem_smem_floats<K, S>() * 4;
+    cudaError_t e = cudaFuncSetAttribute(tdc_stem_kernel<K, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    const int blocks = B * ((Ho + kStemTH - 1) / kStemTH) * ((Wo + kStemTW - 1) / kStemTW);
+    tdc_stem_kernel<K, S><<<blocks, 128, smem, st>>>(x, w, bias, y, H, W, p, Ho, Wo, relu);
+    return cudaGetLastError();
+}
+
 int ew_grid(long long n) { return (int)std::min<long long>(div_up((int)std::min<long long>(n, 1LL << 30), 256), 148 * 16); }
 
 // ------------------------------------------------------------------ dense GEMM op
@@ -302,6 +398,15 @@ tdc_status run_dense(tdc_model_s *m, ModelOp &op, const float *src, float *dst, 
     DenseOp &g = op.dense;
     const tdc_model_op &o = op.d;
     const long long M = (long long)batch * op.Ho * op.Wo;
+    if (g.direct && op.C == 3 && op.Co == 64 && !std::getenv("TDC_NO_STEM") &&
+        ((o.kernel == 7 && o.stride == 2) || (o.kernel == 3 && o.stride == 1))) {
+        const float *wd = g.d_wdirect, *bd = g.d_wdirect + (size_t)o.kernel * o.kernel * 3 * 64;
+        cudaError_t e = o.kernel == 7
+                            ? stem_launch<7, 2>(src, wd, bd, dst, batch, op.H, op.W, o.pad, op.Ho, op.Wo, o.relu, st)
+                            : stem_launch<3, 1>(src, wd, bd, dst, batch, op.H, op.W, o.pad, op.Ho, op.Wo, o.relu, st);
+        if (e != cudaSuccess) return mcuda(e, "stem conv launch");
+        return TDC_OK;
+    }
     if (g.direct) {
         const int K = o.kernel, C = op.C, N = op.Co;
         const int smem = K * K * C * kDirectCo * 4;
