@@ -61,6 +61,7 @@ struct TcGemmArgs {
     int relu;         // fp32 output only: ReLU after bias/residual
     int dbg;          // debug (TDC_GEMM_DBG): 1 skip the fp32 output stores, 2 skip residual reads
     int tma_y;        // fp32 output (remap 0, ldo == Nn): full 32x32 blocks stored by TMA (mapY)
+    int yring;        // 3xBF16 converting GEMM with fp32 output: TMA output ring depth (2 or 4)
     int gsplit;       // 3xBF16: >1 = split K into gsplit pieces, partials reduced through L2
     float *part;      // gsplit: fp32 partial tiles [tiles][gsplit-1][BN/4][128][4]
     int *flags;       // gsplit: one flag per (tile, piece > 0), zero between launches
@@ -124,7 +125,7 @@ cudaError_t fused_launch(const CUtensorMap &mapX, const FusedArgs &g, int grid, 
 
 // ---- 3xBF16 variant of the 3-launch path (tkd_bf16.cu) ----
 // fp32_out: a converting (xstages > 0) GEMM with fp32 output (model dense convs) reserves
-// its TMA output ring; stage 1 (bf16 X' output) does not.
+// its TMA output ring of fp32_out (2 or 4) buffers per warp; stage 1 (bf16 X') passes 0.
 int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages, int fp32_out = 0);
 int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, int *bstages, int fp32_out = 0);
 // mapR: fp32-output GEMMs with a residual and tma_y: TMA map of the residual (same

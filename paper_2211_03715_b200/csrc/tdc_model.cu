@@ -90,6 +90,43 @@ __global__ void tdc_maxpool_kernel(const float *__restrict__ x, float *__restric
     }
 }
 
+// float4 variants with 32-bit index arithmetic (C % 4 == 0, fewer than 2^31 vectors): the
+// scalar kernels above spend most of their time in 64-bit div/mod per element.
+__global__ void tdc_im2col4_kernel(const float4 *__restrict__ x, float4 *__restrict__ out, int B, int H, int W,
+                                   int C4, int K, int s, int p, int Ho, int Wo, int ld4) {
+    const int total = B * Ho * Wo * ld4;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int col = i % ld4, row = i / ld4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (col < K * K * C4) {
+            const int c = col % C4, rt = col / C4, t = rt % K, r = rt / K;
+            const int ox = row % Wo, t2 = row / Wo, oy = t2 % Ho, b = t2 / Ho;
+            const int y = oy * s - p + r, xx = ox * s - p + t;
+            if (y >= 0 && y < H && xx >= 0 && xx < W) v = __ldg(x + (((size_t)b * H + y) * W + xx) * C4 + c);
+        }
+        out[i] = v;
+    }
+}
+__global__ void tdc_maxpool4_kernel(const float4 *__restrict__ x, float4 *__restrict__ out, int B, int H, int W,
+                                    int C4, int K, int s, int p, int Ho, int Wo) {
+    const int total = B * Ho * Wo * C4;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int c = i % C4, pix = i / C4, ox = pix % Wo, t2 = pix / Wo, oy = t2 % Ho, b = t2 / Ho;
+        float4 m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        for (int r = 0; r < K; ++r) {
+            const int y = oy * s - p + r;
+            if (y < 0 || y >= H) continue;
+            for (int t = 0; t < K; ++t) {
+                const int xx = ox * s - p + t;
+                if (xx < 0 || xx >= W) continue;
+                const float4 v = __ldg(x + (((size_t)b * H + y) * W + xx) * C4 + c);
+                m.x = fmaxf(m.x, v.x); m.y = fmaxf(m.y, v.y); m.z = fmaxf(m.z, v.z); m.w = fmaxf(m.w, v.w);
+            }
+        }
+        out[i] = m;
+    }
+}
+
 // one block per (image, 256-channel slice): fixed-order sum over H*W (deterministic)
 __global__ void tdc_avgpool_kernel(const float *__restrict__ x, float *__restrict__ out, int HW, int C) {
     const int b = blockIdx.y;
@@ -348,7 +385,8 @@ tdc_status plan_dense(tdc_model_s *m, ModelOp &op, const tdc_model_op &o) {
     const long long Mmax = (long long)m->max_batch * op.Ho * op.Wo;
     if (Mmax > (1LL << 31) - 256) return mfail(TDC_ERR_UNSUPPORTED, "op too large (M=%lld rows)", Mmax);
     int BN = 32;
-    while (BN < N && BN < 128) BN *= 2;
+    const int bn_cap = std::getenv("TDC_DENSE_BN") ? std::atoi(std::getenv("TDC_DENSE_BN")) : 128;
+    while (BN < N && BN < bn_cap) BN *= 2;
     while (BN > 64 && div_up((int)Mmax, 128) * (long long)div_up(N, BN) < 2 * m->num_sms) BN /= 2;
     const int R = round_up(N, BN);
     std::vector<double> scale, bias;
@@ -381,7 +419,15 @@ tdc_status plan_dense(tdc_model_s *m, ModelOp &op, const tdc_model_op &o) {
     tdc::TcGemmArgs &a = g.args;
     a.Nn = N; a.kchunks = K64 / 64; a.taps = 1; a.BN = BN; a.remap = 0; a.a_convert = 1; a.out_bf16 = 0;
     a.ldo = N; a.bias = g.d_bias; a.relu = o.relu; a.ntiles = R / BN; a.ksplit = 1;
-    a.stages = tdc::bf_pick_stages(BN, m->max_smem, 1, &a.xstages, 1, &a.bstages, 1);
+    // output ring: 4 buffers per epilogue warp (residual blocks loaded two chunks ahead) when
+    // shared memory allows, else 2 (TDC_DENSE_RING=2/4 overrides)
+    a.yring = 4;
+    if (const char *ev = std::getenv("TDC_DENSE_RING")) a.yring = std::atoi(ev) > 2 ? 4 : 2;
+    a.stages = tdc::bf_pick_stages(BN, m->max_smem, 1, &a.xstages, 1, &a.bstages, a.yring);
+    if (tdc::bf_smem_bytes(BN, a.stages, a.xstages, 1, a.bstages, a.yring) > m->max_smem) {
+        a.yring = 2;
+        a.stages = tdc::bf_pick_stages(BN, m->max_smem, 1, &a.xstages, 1, &a.bstages, a.yring);
+    }
     if (const char *dbg = std::getenv("TDC_GEMM_DBG")) a.dbg = std::atoi(dbg);
     {
         const char *ev = std::getenv("TDC_NO_TMA_Y");
@@ -424,8 +470,14 @@ tdc_status run_dense(tdc_model_s *m, ModelOp &op, const float *src, float *dst, 
     if (g.im2col) {
         const int K = o.kind == TDC_OP_FC ? 1 : o.kernel;
         const long long n = M * g.Kdim;
-        tdc_im2col_kernel<<<ew_grid(n), 256, 0, st>>>(src, m->scratch, batch, op.H, op.W, op.C, K, o.stride,
-                                                       o.pad, op.Ho, op.Wo, g.Kdim);
+        if (op.C % 4 == 0 && g.Kdim % 4 == 0 && n / 4 < (1LL << 31))
+            tdc_im2col4_kernel<<<ew_grid(n / 4), 256, 0, st>>>(reinterpret_cast<const float4 *>(src),
+                                                                reinterpret_cast<float4 *>(m->scratch), batch, op.H,
+                                                                op.W, op.C / 4, K, o.stride, o.pad, op.Ho, op.Wo,
+                                                                g.Kdim / 4);
+        else
+            tdc_im2col_kernel<<<ew_grid(n), 256, 0, st>>>(src, m->scratch, batch, op.H, op.W, op.C, K, o.stride,
+                                                           o.pad, op.Ho, op.Wo, g.Kdim);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return mcuda(e, "im2col launch");
         A = m->scratch;
@@ -440,7 +492,7 @@ tdc_status run_dense(tdc_model_s *m, ModelOp &op, const float *src, float *dst, 
     a.M = (int)M;
     a.out = dst;
     a.res = res;
-    const int smem = tdc::bf_smem_bytes(a.BN, a.stages, a.xstages, 1, a.bstages, 1);
+    const int smem = tdc::bf_smem_bytes(a.BN, a.stages, a.xstages, 1, a.bstages, a.yring);
     const long long tiles = (long long)div_up((int)M, 128) * a.ntiles;
     const long long cap = (long long)m->num_sms * tdc::persistent_occupancy(smem, a.BN);
     const int grid = (int)std::max<long long>(1, std::min(tiles, cap));
@@ -625,8 +677,13 @@ tdc_status tdc_model_forward(tdc_model_t m, const float *x, int32_t batch, float
                 break;
             case TDC_OP_MAXPOOL: {
                 const long long tot = (long long)batch * op.Ho * op.Wo * op.Co;
-                tdc_maxpool_kernel<<<ew_grid(tot), 256, 0, st>>>(src, dst, batch, op.H, op.W, op.C, o.kernel,
-                                                                 o.stride, o.pad, op.Ho, op.Wo);
+                if (op.C % 4 == 0 && tot / 4 < (1LL << 31))
+                    tdc_maxpool4_kernel<<<ew_grid(tot / 4), 256, 0, st>>>(
+                        reinterpret_cast<const float4 *>(src), reinterpret_cast<float4 *>(dst), batch, op.H, op.W,
+                        op.C / 4, o.kernel, o.stride, o.pad, op.Ho, op.Wo);
+                else
+                    tdc_maxpool_kernel<<<ew_grid(tot), 256, 0, st>>>(src, dst, batch, op.H, op.W, op.C, o.kernel,
+                                                                     o.stride, o.pad, op.Ho, op.Wo);
                 e = cudaGetLastError();
                 break;
             }

@@ -110,9 +110,19 @@ constexpr int kEpiScratch16 = 4 * 4096;
 // (ring of 4 for stage 3; 2 for the converting dense convs of the model path, whose fp32
 // staging ring already takes most of shared memory)
 constexpr int kYRing = 4;
-__host__ __device__ constexpr int bf_yring(bool convert) { return convert ? 2 : kYRing; }
-__host__ __device__ inline int bf_epi_bytes(bool convert, bool out_bf16) {
-    return (convert && out_bf16) ? kEpiScratch16 : 4 * bf_yring(convert) * 4096;
+// ring depth: stage 3 (not converting) 4; converting fp32-output GEMMs g.yring (2 or 4)
+__host__ __device__ inline int bf_yring(bool convert, int yring) { return convert ? (yring > 2 ? 4 : 2) : kYRing; }
+__host__ __device__ inline int bf_epi_bytes(bool convert, bool out_bf16, int yring) {
+    return (convert && out_bf16) ? kEpiScratch16 : 4 * bf_yring(convert, yring) * 4096;
+}
+// cp.async.bulk.wait_group.read with a run-time count (0..3)
+__device__ __forceinline__ void bulk_wait_read_upto(int n) {
+    switch (n) {
+        case 0: bulk_wait_group_read<0>(); break;
+        case 1: bulk_wait_group_read<1>(); break;
+        case 2: bulk_wait_group_read<2>(); break;
+        default: bulk_wait_group_read<3>(); break;
+    }
 }
 
 // 32 rows x 64 bytes (32 bf16) per warp, row `lane` held by lane `lane` as 16
@@ -257,7 +267,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     float *epi_scratch = reinterpret_cast<float *>(bring + (size_t)SB * bslot);
     // split-K (cluster of CS CTAs over K): fp32 partial tile [128][BN], float4-swizzled
     const int CS = g.ksplit > 1 ? g.ksplit : 1;
-    float *red = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(epi_scratch) + bf_epi_bytes(CONVERT, g.out_bf16));
+    float *red = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(epi_scratch) + bf_epi_bytes(CONVERT, g.out_bf16, g.yring));
     uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(red) +
                                                   (CS > 1 ? (size_t)128 * BN * 4 : 0));
     uint64_t *conv = full + S;       // CONVERT: A hi/lo written by the converter
@@ -417,7 +427,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         }
     } else if (warp < 6) {  // --------------------------------- epilogue
         const int q = warp & 3;
-        constexpr int NR = bf_yring(CONVERT);
+        const int NR = bf_yring(CONVERT, g.yring), LA = NR / 2;  // ring depth, residual lookahead
         float *scratch = epi_scratch + q * (g.out_bf16 ? 1024 : NR * 1024);
         // fp32 output ring (tma_y): chunk counter of this warp -> buffer and residual parity
         const bool ring = !g.out_bf16 && g.tma_y && (g.ldo & 3) == 0;
@@ -427,10 +437,10 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         auto full_chunk = [&](int n) { return n + 32 <= g.Nn; };
         // TMA-load the residual block (columns n, rows r0..r0+31) into ring buffer of chunk k;
         // `pend` = TMA stores that may still be reading when the buffer's last store is done
-        auto res_load = [&](uint32_t k, int n, int r0, bool first) {
+        // `pend`: committed stores that may still be reading when this buffer's last one is done
+        auto res_load = [&](uint32_t k, int n, int r0, int pend) {
             if (lane == 0) {
-                if (first) bulk_wait_group_read<NR - 1>();
-                else bulk_wait_group_read<NR - 2>();
+                bulk_wait_read_upto(pend);
                 const uint32_t b = k % NR;
                 mbar_arrive_expect_tx(&rbar[q * kYRing + b], 4096);
                 tma_load_2d(scratch + b * 1024, &mapR, &rbar[q * kYRing + b], n, r0);
@@ -442,7 +452,9 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             const int t = u / GS, pc = u - t * GS;
             const int m0 = (t % mtiles) * kBM16, n0 = (t / mtiles) * BN;
             // the tile's first residual block is in flight while the MMAs finish
-            if (rres && (GS == 1 || pc == 0) && full_chunk(n0)) res_load(yc, n0, m0 + q * 32, true);
+            if (rres && (GS == 1 || pc == 0))
+                for (int j = 0; j < LA && j * 32 < BN && full_chunk(n0 + 32 * j); ++j)
+                    res_load(yc + j, n0 + 32 * j, m0 + q * 32, NR - 1 - j);
             mbar_wait(&tfull[acc.slot], acc.phase);
             tc_fence_after();
             if (warp == 2 && lane == 0) BFTL(seq, tit, 4);  // epilogue: accumulator ready
@@ -540,9 +552,9 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                     }
                 } else if (ring && full_chunk(n)) {  // fp32 Y through the per-warp TMA ring
                     const uint32_t b = yc % NR, buf = ring_s + b * 4096;
-                    const bool nxt = c + 32 < BN && full_chunk(n + 32);
-                    if (rres && nxt) res_load(yc + 1, n + 32, m0 + q * 32, false);
-                    else if (!rres && lane == 0) bulk_wait_group_read<NR - 1>();  // buffer b free
+                    const bool nxt = c + 32 * LA < BN && full_chunk(n + 32 * LA);
+                    if (rres && nxt) res_load(yc + LA, n + 32 * LA, m0 + q * 32, NR - LA - 1);
+                    else if (!rres && lane == 0) bulk_wait_read_upto(NR - 1);  // buffer b free
                     __syncwarp();
                     if (rres) {
                         mbar_wait(&rbar[q * kYRing + b], (yc / NR) & 1);
@@ -667,9 +679,10 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
 // xstages > 0 (converting stage 1): xstages fp32 staging slots, `stages` A slots and
 // bstages weight slots; otherwise `stages` combined A|B slots.
 int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages, int fp32_out) {
+    // fp32_out (converting GEMMs only): 0 = bf16 X' output, else the output ring depth (2 or 4)
     const int b_tile = BN * kBK16 * 2;
     const int ops = xstages ? stages * 2 * kATile16 + bstages * 2 * b_tile : stages * 2 * (kATile16 + b_tile);
-    return 1024 + xstages * kStage32 + ops + bf_epi_bytes(xstages > 0, xstages > 0 && !fp32_out) +
+    return 1024 + xstages * kStage32 + ops + bf_epi_bytes(xstages > 0, xstages > 0 && !fp32_out, fp32_out) +
            (ksplit > 1 ? 128 * BN * 4 : 0) +
            (3 * stages + 4 + 2 * xstages + 2 * bstages + 2 + 4 * kYRing) * 8 + 16;
 }
@@ -691,7 +704,7 @@ cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, c
                            cudaStream_t st, const CUtensorMap *mapR) {
     if (!mapR) mapR = &mapY;
     const int smem = bf_smem_bytes(g.BN, g.stages, g.a_convert ? g.xstages : 0, g.ksplit, g.a_convert ? g.bstages : 0,
-                                   !g.out_bf16);
+                                   g.out_bf16 ? 0 : bf_yring(true, g.yring));
     cudaError_t e;
     if (g.a_convert) {
         e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
