@@ -501,7 +501,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                             st_global_v4(dst, make_float4(v[0], v[1], v[2], v[3]));
                             st_global_v4(dst + 4, make_float4(v[4], v[5], v[6], v[7]));
                         } else {
-                            for (int j = 0; j < 8 && n + j < g.Nn; ++j) dst[j] = v[j];
+                            _Pragma("unroll") for (int j = 0; j < 8; ++j) if (n + j < g.Nn) dst[j] = v[j];
                         }
                     }
                 }
@@ -612,7 +612,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                     } else if (n + 32 <= g.Nn && (g.ldo & 3) == 0) {
                         warp_store_block32(scratch, v, valid ? dst + n : nullptr, lane);
                     } else if (valid) {
-                        for (int j = 0; j < 32 && n + j < g.Nn; ++j) dst[n + j] = v[j];
+                        _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n + j < g.Nn) dst[n + j] = v[j];
                     }
                 }
             }
@@ -1226,7 +1226,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                         warp_store_block32(scratch, v, valid ? dst + c : nullptr, lane);
                     }
                 } else if (valid) {
-                    for (int j = 0; j < 32 && c + j < g.N3; ++j) dst[c + j] = v[j];
+                    _Pragma("unroll") for (int j = 0; j < 32; ++j) if (c + j < g.N3) dst[c + j] = v[j];
                 }
             }
             tc_fence_before();

@@ -349,7 +349,7 @@ tdc_tkd_fused_tc_kernel(const __grid_constant__ CUtensorMap mapX, const FusedArg
                     if (vec && n + 32 <= g.N) {  // coalesced through shared memory
                         warp_store_block32(scratch, v, valid ? dst + n : nullptr, lane);
                     } else if (valid) {
-                        for (int j = 0; j < 32 && n + j < g.N; ++j) dst[n + j] = v[j];
+                        _Pragma("unroll") for (int j = 0; j < 32; ++j) if (n + j < g.N) dst[n + j] = v[j];
                     }
                 }
                 tc_fence_before();

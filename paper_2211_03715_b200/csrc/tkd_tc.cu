@@ -105,7 +105,9 @@ __device__ __forceinline__ void store_row32(float *dst, float *dst_lo, long long
                 *reinterpret_cast<float4 *>(dst + n + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
     } else {
-        for (int j = 0; j < 32 && n + j < Nn; ++j) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (n + j >= Nn) continue;
             if (split) {
                 const float h = rna_tf32(v[j]);
                 dst[n + j] = h;
