@@ -419,9 +419,9 @@ tdc_status plan_dense(tdc_model_s *m, ModelOp &op, const tdc_model_op &o) {
     tdc::TcGemmArgs &a = g.args;
     a.Nn = N; a.kchunks = K64 / 64; a.taps = 1; a.BN = BN; a.remap = 0; a.a_convert = 1; a.out_bf16 = 0;
     a.ldo = N; a.bias = g.d_bias; a.relu = o.relu; a.ntiles = R / BN; a.ksplit = 1;
-    // output ring: 4 buffers per epilogue warp (residual blocks loaded two chunks ahead) when
-    // shared memory allows, else 2 (TDC_DENSE_RING=2/4 overrides)
-    a.yring = 4;
+    // output ring: 2 buffers per epilogue warp (residual block loaded one chunk ahead);
+    // TDC_DENSE_RING=4 asks for 4 (two chunks ahead) if shared memory allows
+    a.yring = 2;  // shared memory goes to the fp32 staging ring first (measured)
     if (const char *ev = std::getenv("TDC_DENSE_RING")) a.yring = std::atoi(ev) > 2 ? 4 : 2;
     a.stages = tdc::bf_pick_stages(BN, m->max_smem, 1, &a.xstages, 1, &a.bstages, a.yring);
     if (tdc::bf_smem_bytes(BN, a.stages, a.xstages, 1, a.bstages, a.yring) > m->max_smem) {

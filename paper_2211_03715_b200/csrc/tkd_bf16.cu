@@ -250,20 +250,22 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int S = g.stages, BN = g.BN;
-    const int SX = CONVERT ? g.xstages : 0;  // fp32 staging ring depth (stage 1)
-    const int SB = CONVERT ? g.bstages : 0;  // stage 1: separate weight ring depth
+    const int BN = g.BN;
+    const int SX = CONVERT ? g.xstages : 0;  // fp32 staging ring depth (converting GEMMs)
+    const int S = CONVERT ? SX : g.stages;   // operand ring depth
+    const int SB = CONVERT ? g.bstages : 0;  // converting GEMMs: separate weight ring depth
     const uint32_t b_tile = (uint32_t)BN * kBK16 * 2;
     // non-CONVERT slot: A hi | B hi | A lo | B lo (one TMA ring);
-    // CONVERT: A slots (A hi | A lo, written by the converter) + a separate B ring
-    // (B hi | B lo) that the producer fills ahead of the conversion.
+    // CONVERT: the fp32 staging slot is converted IN PLACE into A hi | A lo (the 32 KB of
+    // a 128 x 64 fp32 chunk hold exactly its two 16 KB bf16 tiles), so the staging ring is
+    // the operand ring; B (hi | lo) has a separate ring the producer fills ahead.
     const uint32_t half = CONVERT ? kATile16 : kATile16 + b_tile;   // A hi -> A lo
-    const uint32_t slot_bytes = CONVERT ? 2 * kATile16 : 2 * half;
+    const uint32_t slot_bytes = CONVERT ? (uint32_t)kStage32 : 2 * half;
     const uint32_t bslot = 2 * b_tile;
-    // [SX fp32 staging slots][S operand slots][SB B slots][epilogue scratch][red][barriers]
+    // [SX fp32 staging = operand slots | S operand slots][SB B slots][epilogue scratch][red][barriers]
     uint8_t *xstage = smem;
-    uint8_t *ops = smem + (size_t)SX * kStage32;
-    uint8_t *bring = ops + (size_t)S * slot_bytes;
+    uint8_t *ops = CONVERT ? xstage : smem;
+    uint8_t *bring = smem + (size_t)(CONVERT ? SX : S) * slot_bytes;
     float *epi_scratch = reinterpret_cast<float *>(bring + (size_t)SB * bslot);
     // split-K (cluster of CS CTAs over K): fp32 partial tile [128][BN], float4-swizzled
     const int CS = g.ksplit > 1 ? g.ksplit : 1;
@@ -310,7 +312,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         }
         for (int i = 0; i < SX; ++i) {
             mbar_init(&xfull[i], 1);
-            mbar_init(&xempty[i], kConvThreads16);
+            mbar_init(&xempty[i], 1);  // arrived by the MMA commit
         }
         for (int i = 0; i < SB; ++i) {
             mbar_init(&bfull[i], 1);
@@ -415,8 +417,12 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                         mma_bf16(d, a + j * 2, b + blo + j * 2, idesc, 1);  // hi * lo
                         mma_bf16(d, a + lo + j * 2, b + j * 2, idesc, 1);   // lo * hi
                     }
-                    mma_commit(&empty[r.slot]);
-                    if (CONVERT) mma_commit(&bempty[rb.slot]);
+                    if (CONVERT) {
+                        mma_commit(&xempty[r.slot]);  // staging slot free for the next TMA load
+                        mma_commit(&bempty[rb.slot]);
+                    } else {
+                        mma_commit(&empty[r.slot]);
+                    }
                 }
                 __syncwarp();
                 if (CONVERT) rb.next();
@@ -629,39 +635,43 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         (void)res_load;
     } else if (CONVERT) {  // ----------------- converter: fp32 staging -> bf16 hi/lo A tiles
         const int tid = threadIdx.x - 192;
-        Ring r(S), rx(SX);
+        Ring rx(SX);
         int tit = 0;
         for (int u = cid; u < num_units; u += ncl, ++tit) {
             const int pc = u % GS;
             const int i0 = GS > 1 ? pc * iters / GS : ci0, i1 = GS > 1 ? (pc + 1) * iters / GS : ci1;
-            for (int i = i0; i < i1; ++i, r.next(), rx.next()) {
-                mbar_wait(&empty[r.slot], r.phase ^ 1);  // operand slot free
-                const uint32_t base = smem_u32(ops + (size_t)r.slot * slot_bytes);
+            for (int i = i0; i < i1; ++i, rx.next()) {
                 mbar_wait(&xfull[rx.slot], rx.phase);
                 if (i == i0 && tid == 0) BFTL(seq, tit, 6);  // converter: X landed
-                const uint32_t stage = smem_u32(xstage + (size_t)rx.slot * kStage32);
+                // thread = (row, 32-channel half): read the row's half from its fp32 box, then
+                // (after every converter thread has read) overwrite the slot in place with the
+                // hi tile [0, 16 KB) and lo tile [16 KB, 32 KB), 128B-swizzled K-major rows
+                const int row = tid & 127, hf = tid >> 7;
+                const uint32_t base = smem_u32(xstage + (size_t)rx.slot * kStage32);
+                const uint32_t box = base + (uint32_t)hf * (kStage32 / 2) + row * 128;
+                float v[32];
 #pragma unroll
-                for (int k = 0; k < 1024 / kConvThreads16; ++k) {
-                    const int item = k * kConvThreads16 + tid;  // row r, 8-channel chunk c8
-                    const int row = item >> 3, c8 = item & 7;
-                    const uint32_t box = stage + (uint32_t)(c8 >> 2) * (kStage32 / 2) + row * 128;
-                    const int j0 = (c8 & 3) * 2;              // fp32 16-byte chunk index in the box
-                    const float4 f0 = ld_shared_v4(box + ((j0 ^ (row & 7)) << 4));
-                    const float4 f1 = ld_shared_v4(box + (((j0 + 1) ^ (row & 7)) << 4));
-                    const float v[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-                    uint4 h, l;
-                    split_bf16x8(v, h, l);
+                for (int j = 0; j < 8; ++j) {
+                    const float4 f = ld_shared_v4(box + ((j ^ (row & 7)) << 4));
+                    v[4 * j] = f.x; v[4 * j + 1] = f.y; v[4 * j + 2] = f.z; v[4 * j + 3] = f.w;
+                }
+                uint4 h[4], l[4];
+#pragma unroll
+                for (int g8 = 0; g8 < 4; ++g8) split_bf16x8(v + 8 * g8, h[g8], l[g8]);
+                asm volatile("bar.sync 2, %0;" ::"n"(kConvThreads16) : "memory");  // all reads done
+#pragma unroll
+                for (int g8 = 0; g8 < 4; ++g8) {
+                    const int c8 = 4 * hf + g8;
                     const uint32_t dsto = row * 128 + ((c8 ^ (row & 7)) << 4);
-                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + dsto), "r"(h.x),
-                                 "r"(h.y), "r"(h.z), "r"(h.w)
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + dsto), "r"(h[g8].x),
+                                 "r"(h[g8].y), "r"(h[g8].z), "r"(h[g8].w)
                                  : "memory");
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + half + dsto),
-                                 "r"(l.x), "r"(l.y), "r"(l.z), "r"(l.w)
+                                 "r"(l[g8].x), "r"(l[g8].y), "r"(l[g8].z), "r"(l[g8].w)
                                  : "memory");
                 }
-                mbar_arrive(&xempty[rx.slot]);  // staging slot may be refilled
                 fence_proxy_async_smem();
-                mbar_arrive(&conv[r.slot]);
+                mbar_arrive(&conv[rx.slot]);
                 if (i == i1 - 1 && tid == 0) BFTL(seq, tit, 7);  // converter: done
             }
         }
@@ -681,7 +691,8 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
 int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages, int fp32_out) {
     // fp32_out (converting GEMMs only): 0 = bf16 X' output, else the output ring depth (2 or 4)
     const int b_tile = BN * kBK16 * 2;
-    const int ops = xstages ? stages * 2 * kATile16 + bstages * 2 * b_tile : stages * 2 * (kATile16 + b_tile);
+    // converting GEMMs: A is converted in place in the fp32 staging slots (stages == xstages)
+    const int ops = xstages ? bstages * 2 * b_tile : stages * 2 * (kATile16 + b_tile);
     return 1024 + xstages * kStage32 + ops + bf_epi_bytes(xstages > 0, xstages > 0 && !fp32_out, fp32_out) +
            (ksplit > 1 ? 128 * BN * 4 : 0) +
            (3 * stages + 4 + 2 * xstages + 2 * bstages + 2 + 4 * kYRing) * 8 + 16;
@@ -690,9 +701,15 @@ int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages, int 
 // Ring depths: operand slots (and, for the converting stage 1, the fp32 staging and
 // weight rings).
 int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, int *bstages, int fp32_out) {
-    int s = convert ? 2 : 6, sx = convert ? 4 : 0, sb = convert ? 4 : 0;
-    while (sx > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb, fp32_out) > max_smem) --sx;
-    while (sb > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb, fp32_out) > max_smem) --sb;
+    if (convert) {  // staging (= operand) ring first, then the weight ring
+        int sx = 6, sb = 4;
+        while (sb > 2 && bf_smem_bytes(BN, sx, sx, ksplit, sb, fp32_out) > max_smem) --sb;
+        while (sx > 2 && bf_smem_bytes(BN, sx, sx, ksplit, sb, fp32_out) > max_smem) --sx;
+        if (xstages) *xstages = sx;
+        if (bstages) *bstages = sb;
+        return sx;
+    }
+    int s = 6, sx = 0, sb = 0;
     while (s > 2 && bf_smem_bytes(BN, s, sx, ksplit, sb, fp32_out) > max_smem) --s;
     if (xstages) *xstages = sx;
     if (bstages) *bstages = sb;

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out/g11
+o=gpurun_out/g11/model_time.txt
+for cfg in "" "TDC_DENSE_BN=64" "TDC_GEMM_DBG=1" "TDC_GEMM_DBG=2" "TDC_NO_STEM=1"; do echo "cfg $cfg" >> $o; env $cfg python scripts/model_time.py >> $o 2>&1; done
