@@ -192,12 +192,12 @@ __global__ void __launch_bounds__(128) tdc_direct_conv_kernel(const float *__res
 }
 
 // The 3-channel stems (ResNet 7x7/2, VGG 3x3/1) with 64 outputs, specialised: a block
-// computes an 8 x 32 output tile from a zero-padded input patch staged in shared memory
+// computes a 16 x 16 output tile from a zero-padded input patch staged in shared memory
 // (no bounds checks in the loop).  Warp w owns output channels [16w, 16w + 16) (so its
-// weight reads are broadcasts), lane l the 8 pixels of tile column l: per tap and input
+// weight reads are broadcasts), lane l 8 pixels of tile column l % 16: per tap and input
 // channel, 8 scalar x loads and 4 float4 weight loads feed 128 FMAs.  The finished tile
 // is transposed through shared memory and written as contiguous 8 KB pixel rows.
-constexpr int kStemTH = 8, kStemTW = 32;
+constexpr int kStemTH = 16, kStemTW = 16, kStemPL = 8;  // tile rows, cols; pixels per lane
 template <int K, int S>
 __host__ __device__ constexpr int stem_smem_floats() {
     return (K * K * 3 * 64 + ((kStemTH - 1) * S + K) * ((kStemTW - 1) * S + K) * 3) > kStemTH * kStemTW * 64
@@ -205,7 +205,7 @@ __host__ __device__ constexpr int stem_smem_floats() {
                : kStemTH * kStemTW * 64;
 }
 template <int K, int S>
-__global__ void __launch_bounds__(128) tdc_stem_kernel(const float *__restrict__ x, const float *__restrict__ w,
+__global__ void __launch_bounds__(128, 3) tdc_stem_kernel(const float *__restrict__ x, const float *__restrict__ w,
                                                         const float *__restrict__ bias, float *__restrict__ y, int H,
                                                         int W, int p, int Ho, int Wo, int relu) {
     constexpr int C = 3, N = 64, PH = (kStemTH - 1) * S + K, PW = (kStemTW - 1) * S + K;
@@ -225,10 +225,10 @@ __global__ void __launch_bounds__(128) tdc_stem_kernel(const float *__restrict__
         for (int c = 0; c < C; ++c) xs[i * C + c] = in ? __ldg(src + c) : 0.f;
     }
     __syncthreads();
-    const int wq = threadIdx.x >> 5, col = threadIdx.x & 31;
-    float acc[kStemTH][16];
+    const int wq = threadIdx.x >> 5, lane = threadIdx.x & 31, col = lane & 15, rh = lane >> 4;
+    float acc[kStemPL][16];  // lane's pixels: tile rows rh*8 .. rh*8+7 of column col
 #pragma unroll
-    for (int i = 0; i < kStemTH; ++i)
+    for (int i = 0; i < kStemPL; ++i)
 #pragma unroll
         for (int n = 0; n < 16; ++n) acc[i][n] = 0.f;
 #pragma unroll 1
@@ -242,8 +242,8 @@ __global__ void __launch_bounds__(128) tdc_stem_kernel(const float *__restrict__
                 const float wv[16] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w,
                                       w2.x, w2.y, w2.z, w2.w, w3.x, w3.y, w3.z, w3.w};
 #pragma unroll
-                for (int i = 0; i < kStemTH; ++i) {
-                    const float xv = xs[((i * S + r) * PW + col * S + t) * C + c];
+                for (int i = 0; i < kStemPL; ++i) {
+                    const float xv = xs[(((rh * kStemPL + i) * S + r) * PW + col * S + t) * C + c];
 #pragma unroll
                     for (int n = 0; n < 16; ++n) acc[i][n] = fmaf(xv, wv[n], acc[i][n]);
                 }
@@ -252,10 +252,10 @@ __global__ void __launch_bounds__(128) tdc_stem_kernel(const float *__restrict__
     __syncthreads();  // done with the weights / patch: reuse shared memory for the output tile
     float *ys = sm;   // [TH][TW][64], 16-byte chunks of a pixel rotated by the pixel index
 #pragma unroll
-    for (int i = 0; i < kStemTH; ++i)
+    for (int i = 0; i < kStemPL; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int px = i * kStemTW + col, ch4 = (wq * 4 + j + px) & 15;
+            const int px = (rh * kStemPL + i) * kStemTW + col, ch4 = (wq * 4 + j + px) & 15;
             float4 v = make_float4(acc[i][4 * j] + bias[16 * wq + 4 * j], acc[i][4 * j + 1] + bias[16 * wq + 4 * j + 1],
                                    acc[i][4 * j + 2] + bias[16 * wq + 4 * j + 2], acc[i][4 * j + 3] + bias[16 * wq + 4 * j + 3]);
             if (relu) {
