@@ -10,7 +10,8 @@ from HBM; weights are a few MB and legitimately L2-resident.
 
 value  = algorithmic HBM bytes of all layers on all ranks / max-over-ranks time
          (GB/s; bytes = input once + output once + weights once per layer).
-e2e    = the same metric through tdc_conv_forward_host with pinned host buffers
+e2e    = the same metric through tdc_conv_forward_host_many (the 16 layers' host-buffer
+         forwards in one pipelined call) with pinned host buffers
          (H2D of every input and D2H of every output inside the timed region).
 roofline = the dominant layer's kernel: achieved bytes (or FLOPs) per launch /
          its mean CUDA-event duration on the launching stream.
@@ -411,21 +412,22 @@ def impl_tdc(args):
             xh = torch.from_numpy(synth.nchw_to_nhwc(L["xnp"])).pin_memory()
             yh = torch.empty((s.B, s.Ho, s.Wo, s.N)).pin_memory()
             host.append((xh, yh))
-        for L, (xh, yh) in zip(layers, host):
-            L["plan"].forward_host(xh, yh, stream=stream)
+        plans = [L["plan"] for L in layers]
+        xs, ys = [h[0] for h in host], [h[1] for h in host]
+        # one call per step: the 16 forwards' image chunks form one H2D / forward / D2H pipeline
+        tdc.forward_host_many(plans, xs, ys, stream=stream)
         e2e_steps = max(1, min(args.steps, 5))
         tdist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            for L, (xh, yh) in zip(layers, host):
-                L["plan"].forward_host(xh, yh, stream=stream)
+            tdc.forward_host_many(plans, xs, ys, stream=stream)
         torch.cuda.synchronize()
         el = tdist.max_over_ranks(time.perf_counter() - t0, "cuda")
         e2e = {"value": step_bytes * e2e_steps * world / el / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": sum(int(h[0].numel()) * 4 for h in host),
                "d2h_bytes_per_step": sum(int(h[1].numel()) * 4 for h in host),
-               "steps": e2e_steps, "api": "tdc_conv_forward_host"}
+               "steps": e2e_steps, "api": "tdc_conv_forward_host_many (16 forwards per call)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -150,6 +150,16 @@ tdc_status tdc_conv_forward(tdc_conv_plan_t plan, const float *x, float *y,
 tdc_status tdc_conv_forward_host(tdc_conv_plan_t plan, const float *x_host,
                                  float *y_host, int32_t batch, void *stream);
 
+/* n end-to-end forwards with HOST buffers in one call (plans on one device; a plan may
+ * appear more than once only if its forwards need not overlap -- they share its staging
+ * buffers, so list distinct plans).  Equivalent to n tdc_conv_forward_host calls, but the
+ * image chunks of all n forwards form one pipeline: the host->device copy of the next
+ * forward and the device->host copy of the previous one overlap the current forward.
+ * Waits for completion.  Errors as tdc_conv_forward_host, for the first failing plan. */
+tdc_status tdc_conv_forward_host_many(const tdc_conv_plan_t *plans, const float *const *x_hosts,
+                                      float *const *y_hosts, const int32_t *batches, int32_t n,
+                                      void *stream);
+
 tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t plan);
 
 /* Forward with the model-path epilogue fused into the last stage (SURVEY §8(f)

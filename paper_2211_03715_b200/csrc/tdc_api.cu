@@ -1418,67 +1418,122 @@ tdc_status tdc_conv_forward_ex(tdc_conv_plan_t p, const float *x, float *y, int3
     return forward_bf16(p, x, y, batch, (cudaStream_t)stream, residual, relu);
 }
 
-tdc_status tdc_conv_forward_host(tdc_conv_plan_t p, const float *x_host, float *y_host,
-                                 int32_t batch, void *stream) {
+namespace {
+
+// Host-buffer forward, shared by tdc_conv_forward_host and tdc_conv_forward_host_many:
+// validation, plan-owned staging buffers and the copy streams / events.
+tdc_status host_prepare(tdc_conv_plan_t p, const float *x_host, const float *y_host, int32_t batch) {
     if (!p) return fail(TDC_ERR_INVALID_ARGUMENT, "plan is NULL");
     if (!x_host || !y_host) return fail(TDC_ERR_INVALID_ARGUMENT, "x_host/y_host is NULL");
     if (batch < 1 || batch > p->desc.batch)
         return fail(TDC_ERR_INVALID_ARGUMENT, "batch %d outside [1, %d] of this plan", batch,
                     p->desc.batch);
     const tdc::LayerDims &d = p->dims;
-    const size_t in_b = (size_t)batch * d.C * d.H * d.W * sizeof(float);
-    const size_t out_b = (size_t)batch * d.N * d.Ho * d.Wo * sizeof(float);
-    DeviceGuard guard(p->device);
-    if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
     if (!p->d_stage_x) {
         const size_t max_in = (size_t)p->desc.batch * d.C * d.H * d.W * sizeof(float);
         const size_t max_out = (size_t)p->desc.batch * d.N * d.Ho * d.Wo * sizeof(float);
-        // + 256 pixel rows of slack: the last chunk of the pipeline below starts mid-buffer and
-        // the row-tiled TMA maps (extent = the plan's batch) may read a partial tile past it
+        // + 256 pixel rows of slack: a chunk of the pipeline below starts mid-buffer
         e = cudaMalloc(&p->d_stage_x, max_in + (size_t)256 * d.C * sizeof(float));
         if (e == cudaSuccess) e = cudaMalloc(&p->d_stage_y, max_out);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(host-forward staging)");
     }
-    cudaStream_t st = (cudaStream_t)stream;
-    // Pipeline over image chunks (images are independent): the H2D copy of
-    // chunk k+1 (copy stream s_in) and the D2H copy of chunk k-1 (s_out) overlap the
-    // forward of chunk k on the caller's stream, so the two link directions run
-    // concurrently instead of back to back.  Chunks of >= ~2 MB of traffic, at most 8.
-    const int nch = std::max(1, std::min<int>({batch, 8, (int)((in_b + out_b) / (2u << 20))}));
     if (!p->s_in) {
         e = cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking);
         for (int i = 0; e == cudaSuccess && i < 17; ++i) e = cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming);
         if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate/cudaEventCreate (host-forward pipeline)");
     }
+    return TDC_OK;
+}
+
+// Pipeline one forward over image chunks (images are independent): the H2D
+// copy of chunk k+1 (s_in) and the D2H copy of chunk k-1 (s_out) overlap the forward of
+// chunk k on `st`, so the two link directions run concurrently instead of back to back.
+// Chunks of >= ~2 MB of traffic, at most 8.  `ev` is a ring of 16 events (each is waited
+// on right after it is recorded, so the ring can wrap); *evi is its cursor.
+tdc_status host_enqueue(tdc_conv_plan_t p, const float *x_host, float *y_host, int32_t batch, cudaStream_t st,
+                        cudaStream_t s_in, cudaStream_t s_out, cudaEvent_t *ev, int *evi) {
+    const tdc::LayerDims &d = p->dims;
+    const size_t in_b = (size_t)batch * d.C * d.H * d.W * sizeof(float);
+    const size_t out_b = (size_t)batch * d.N * d.Ho * d.Wo * sizeof(float);
     const size_t in_img = in_b / batch, out_img = out_b / batch;
-    cudaEvent_t ev_start = p->ev[16];
-    e = cudaEventRecord(ev_start, st);  // earlier work on the caller's stream comes first
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_in, ev_start, 0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_out, ev_start, 0);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord/cudaStreamWaitEvent");
+    const int nch = std::max(1, std::min<int>({batch, 8, (int)((in_b + out_b) / (2u << 20))}));
+    cudaError_t e;
     for (int k = 0; k < nch; ++k) {
         const int b0 = (int)((long long)k * batch / nch), nb = (int)((long long)(k + 1) * batch / nch) - b0;
         float *dx = p->d_stage_x + b0 * (in_img / sizeof(float)), *dy = p->d_stage_y + b0 * (out_img / sizeof(float));
+        cudaEvent_t e_in = ev[(*evi)++ & 15], e_fw = ev[(*evi)++ & 15];
         e = cudaMemcpyAsync(dx, reinterpret_cast<const uint8_t *>(x_host) + b0 * in_img, nb * in_img,
-                            cudaMemcpyHostToDevice, p->s_in);
-        if (e == cudaSuccess) e = cudaEventRecord(p->ev[2 * k], p->s_in);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, p->ev[2 * k], 0);
+                            cudaMemcpyHostToDevice, s_in);
+        if (e == cudaSuccess) e = cudaEventRecord(e_in, s_in);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, e_in, 0);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(H2D)");
-        const tdc_status s = tdc_conv_forward(p, dx, dy, nb, stream);
+        const tdc_status s = tdc_conv_forward(p, dx, dy, nb, st);
         if (s != TDC_OK) return s;
-        e = cudaEventRecord(p->ev[2 * k + 1], st);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_out, p->ev[2 * k + 1], 0);
+        e = cudaEventRecord(e_fw, st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, e_fw, 0);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(reinterpret_cast<uint8_t *>(y_host) + b0 * out_img, dy, nb * out_img,
-                                cudaMemcpyDeviceToHost, p->s_out);
+                                cudaMemcpyDeviceToHost, s_out);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(D2H)");
     }
-    e = cudaStreamSynchronize(p->s_out);
+    return TDC_OK;
+}
+
+tdc_status host_begin(tdc_conv_plan_t p, cudaStream_t st) {  // earlier work on `st` comes first
+    cudaError_t e = cudaEventRecord(p->ev[16], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_in, p->ev[16], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_out, p->ev[16], 0);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord/cudaStreamWaitEvent");
+    return TDC_OK;
+}
+
+tdc_status host_finish(tdc_conv_plan_t p, cudaStream_t st) {
+    cudaError_t e = cudaStreamSynchronize(p->s_out);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
     return TDC_OK;
+}
+
+}  // namespace
+
+tdc_status tdc_conv_forward_host(tdc_conv_plan_t p, const float *x_host, float *y_host,
+                                 int32_t batch, void *stream) {
+    tdc_status s = host_prepare(p, x_host, y_host, batch);
+    if (s != TDC_OK) return s;
+    DeviceGuard guard(p->device);
+    if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((s = host_begin(p, st)) != TDC_OK) return s;
+    int evi = 0;
+    if ((s = host_enqueue(p, x_host, y_host, batch, st, p->s_in, p->s_out, p->ev, &evi)) != TDC_OK) return s;
+    return host_finish(p, st);
+}
+
+tdc_status tdc_conv_forward_host_many(const tdc_conv_plan_t *plans, const float *const *x_hosts,
+                                      float *const *y_hosts, const int32_t *batches, int32_t n, void *stream) {
+    if (!plans || !x_hosts || !y_hosts || !batches || n < 1)
+        return fail(TDC_ERR_INVALID_ARGUMENT, "plans/x_hosts/y_hosts/batches NULL or n < 1");
+    for (int i = 0; i < n; ++i) {
+        const tdc_status s = host_prepare(plans[i], x_hosts[i], y_hosts[i], batches[i]);
+        if (s != TDC_OK) return s;
+        if (plans[i]->device != plans[0]->device)
+            return fail(TDC_ERR_INVALID_ARGUMENT, "plan %d is on device %d, plan 0 on %d", i, plans[i]->device,
+                        plans[0]->device);
+    }
+    tdc_conv_plan_t p0 = plans[0];
+    DeviceGuard guard(p0->device);
+    if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    tdc_status s = host_begin(p0, st);
+    if (s != TDC_OK) return s;
+    int evi = 0;  // one chunk stream across all n forwards: copies of one overlap the next's
+    for (int i = 0; i < n; ++i)
+        if ((s = host_enqueue(plans[i], x_hosts[i], y_hosts[i], batches[i], st, p0->s_in, p0->s_out, p0->ev,
+                              &evi)) != TDC_OK)
+            return s;
+    return host_finish(p0, st);
 }
 
 tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t p) {

@@ -26,7 +26,7 @@ EXPORTED = [
     "tdc_version", "tdc_status_string", "tdc_last_error", "tdc_conv_output_shape",
     "tdc_conv_plan", "tdc_conv_plan_query", "tdc_conv_forward", "tdc_conv_forward_host",
     "tdc_conv_plan_destroy", "tdc_conv_forward_ex", "tdc_model_create", "tdc_model_forward",
-    "tdc_model_output_shape", "tdc_model_destroy", "tdc_conv_plan_ex",
+    "tdc_model_output_shape", "tdc_model_destroy", "tdc_conv_plan_ex", "tdc_conv_forward_host_many",
 ]
 TDC_OP_CONV, TDC_OP_TKD, TDC_OP_MAXPOOL, TDC_OP_AVGPOOL, TDC_OP_FC = range(5)
 
@@ -87,6 +87,8 @@ def _load():
     lib.tdc_conv_plan_query.argtypes = [vp, ctypes.POINTER(tdc_plan_info)]
     lib.tdc_conv_forward.argtypes = [vp, vp, vp, i32, vp]
     lib.tdc_conv_forward_host.argtypes = [vp, vp, vp, i32, vp]
+    lib.tdc_conv_forward_host_many.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                               ctypes.POINTER(i32), i32, vp]
     lib.tdc_conv_plan_destroy.argtypes = [vp]
     lib.tdc_conv_forward_ex.argtypes = [vp, vp, vp, i32, vp, i32, vp]
     lib.tdc_conv_plan_ex.argtypes = [desc_p, fp, fp, fp, fp, ctypes.POINTER(tdc_plan_hints), i32,
@@ -183,6 +185,20 @@ def tdc_conv_forward_host(plan, x_host_ptr: int, y_host_ptr: int, batch: int,
     _check(_lib.tdc_conv_forward_host(plan, ctypes.c_void_p(x_host_ptr),
                                       ctypes.c_void_p(y_host_ptr), batch,
                                       ctypes.c_void_p(stream)))
+
+
+def tdc_conv_forward_host_many(plans, x_host_ptrs, y_host_ptrs, batches, stream: int = 0) -> None:
+    n = len(plans)
+    vp = ctypes.c_void_p
+    _check(_lib.tdc_conv_forward_host_many((vp * n)(*plans), (vp * n)(*x_host_ptrs), (vp * n)(*y_host_ptrs),
+                                           (ctypes.c_int32 * n)(*batches), n, vp(stream)))
+
+
+def forward_host_many(plans, xs, ys, stream=None) -> None:
+    """n end-to-end forwards (ConvPlan objects, pinned host tensors) as one pipeline."""
+    sh = ConvPlan._stream_handle(stream)
+    tdc_conv_forward_host_many([p._h for p in plans], [x.data_ptr() for x in xs], [y.data_ptr() for y in ys],
+                               [int(x.shape[0]) for x in xs], sh)
 
 
 def tdc_conv_plan_destroy(plan) -> None:

@@ -332,3 +332,29 @@ def test_forward_host_pipelined_chunks(env, math, layout):
     ref = ref_of(s, d)
     got = synth.nhwc_to_nchw(yh.numpy()) if layout == "nhwc" else yh.numpy()
     assert err(got, ref) <= TOL[math]
+
+
+def test_forward_host_many_matches_device(env):
+    """tdc_conv_forward_host_many pipelines several layers' host-buffer forwards in one
+    call; each result equals that layer's device-buffer forward bit for bit."""
+    torch, tdc = env
+    shapes = [synth.R18_SHAPES[i][0].with_batch(b) for i, b in ((0, 4), (4, 8), (6, 3), (1, 2))]
+    plans, xs, ys, refs = [], [], [], []
+    for k, s in enumerate(shapes):
+        d = synth.make_layer(s, seed=40 + k, bias=True)
+        p = tdc.ConvPlan(s, d, math=tdc.TDC_MATH_3XBF16)
+        xn = synth.nchw_to_nhwc(d["x"])
+        xd = torch.from_numpy(xn).cuda()
+        yd = torch.full((s.B, s.Ho, s.Wo, s.N), float("nan"), device="cuda")
+        p.forward(xd, yd)
+        refs.append(yd)
+        plans.append(p)
+        xs.append(torch.from_numpy(xn).pin_memory())
+        ys.append(torch.full((s.B, s.Ho, s.Wo, s.N), float("nan")).pin_memory())
+    tdc.forward_host_many(plans, xs, ys)
+    tdc.forward_host_many(plans, xs, ys)
+    torch.cuda.synchronize()
+    for y, r in zip(ys, refs):
+        assert np.array_equal(y.numpy(), r.cpu().numpy())
+    for p in plans:
+        p.close()
