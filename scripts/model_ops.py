@@ -1,6 +1,6 @@
 """Map the last Tucker ResNet-50 forward of an ncu launch list (scripts/model_profile.py)
 to its ops and print each op's kernel time next to its HBM-ideal time (fp32 activations
-in/out + residual, at the measured HBM peak).  Usage: python scripts/model_ops.py r50.csv"""
+in/out + residual, at the measured HBM peak).  Usage: python scripts/model_ops.py launches.csv [r50|vgg16]"""
 import csv
 import io
 import json
@@ -25,8 +25,9 @@ try:
                                        "MEASURED_PEAKS.json")))["hbm_gbs"]
 except Exception:
     peak = 6553.0
-B = 32
-ops = sm.tucker_resnet(50)
+arch = sys.argv[2] if len(sys.argv) > 2 else "r50"
+B = 32 if arch == "r50" else 64
+ops = sm.tucker_resnet(50) if arch == "r50" else sm.tucker_vgg16()
 i = 0
 tot = tot_ideal = 0.0
 agg = {}
