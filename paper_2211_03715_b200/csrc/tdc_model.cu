@@ -296,6 +296,7 @@ struct DenseOp {
     bool direct = false;     // thin input (C <= 4, N % 4 == 0): tdc_direct_conv_kernel
     float *d_wdirect = nullptr;  // [K][K][C][N] fp32, BN folded, then the bias
     uint16_t *d_w = nullptr;  // [hi | lo] bf16 panels [R][K64], then fp32 bias
+    float *d_gs = nullptr;    // split-K through L2: partial tiles | flags (few-tile long-K GEMMs)
     float *d_bias = nullptr;
     tdc::TcGemmArgs args;
     CUtensorMap mapA, mapB, mapBlo;
@@ -387,7 +388,10 @@ tdc_status plan_dense(tdc_model_s *m, ModelOp &op, const tdc_model_op &o) {
     int BN = 32;
     const int bn_cap = std::getenv("TDC_DENSE_BN") ? std::atoi(std::getenv("TDC_DENSE_BN")) : 128;
     while (BN < N && BN < bn_cap) BN *= 2;
-    while (BN > 64 && div_up((int)Mmax, 128) * (long long)div_up(N, BN) < 2 * m->num_sms) BN /= 2;
+    // few M tiles and a long K (classifiers, VGG FC1): keep the widest N tile -- A is
+    // re-read once per N tile -- and fill the SMs with split-K pieces instead (below)
+    const bool wide = div_up((int)Mmax, 128) <= 4 && K64 / 64 >= 8;
+    while (!wide && BN > 64 && div_up((int)Mmax, 128) * (long long)div_up(N, BN) < 2 * m->num_sms) BN /= 2;
     const int R = round_up(N, BN);
     std::vector<double> scale, bias;
     bn_fold(o, N, scale, bias);
@@ -432,6 +436,25 @@ tdc_status plan_dense(tdc_model_s *m, ModelOp &op, const tdc_model_op &o) {
     {
         const char *ev = std::getenv("TDC_NO_TMA_Y");
         a.tma_y = N % 4 == 0 && !(ev && ev[0] && ev[0] != '0');
+    }
+    // Split-K through L2 (gsplit) for the few-tile, long-K GEMMs (classifiers, the VGG FC1
+    // 7x7 conv): the K loop is cut into fixed pieces spread over the idle SMs; the piece-0
+    // CTA adds the partials in piece order (deterministic) and runs the epilogue.
+    {
+        const long long tiles = (long long)div_up((int)Mmax, 128) * (R / BN);
+        const int kch = K64 / 64;
+        int gsp = 1;
+        if (tiles < m->num_sms && kch >= 8 && !std::getenv("TDC_DENSE_NO_GSPLIT"))
+            gsp = (int)std::max<long long>(1, std::min<long long>({8, kch / 4, m->num_sms / tiles}));
+        if (gsp > 1) {
+            const size_t parts = (size_t)tiles * (gsp - 1) * 128 * BN, flags = (size_t)tiles * (gsp - 1);
+            e = cudaMalloc(&g.d_gs, parts * sizeof(float) + flags * sizeof(int));
+            if (e == cudaSuccess) e = cudaMemset(g.d_gs, 0, parts * sizeof(float) + flags * sizeof(int));
+            if (e != cudaSuccess) return mcuda(e, "cudaMalloc(dense split-K workspace)");
+            a.gsplit = gsp;
+            a.part = g.d_gs;
+            a.flags = reinterpret_cast<int *>(g.d_gs + parts);
+        }
     }
     if (!tdc::make_tma_2d_bf16(&g.mapB, g.d_w, R, K64, K64, BN) ||
         !tdc::make_tma_2d_bf16(&g.mapBlo, g.d_w + nw, R, K64, K64, BN))
@@ -493,8 +516,10 @@ tdc_status run_dense(tdc_model_s *m, ModelOp &op, const float *src, float *dst, 
     a.out = dst;
     a.res = res;
     const int smem = tdc::bf_smem_bytes(a.BN, a.stages, a.xstages, 1, a.bstages, a.yring);
-    const long long tiles = (long long)div_up((int)M, 128) * a.ntiles;
-    const long long cap = (long long)m->num_sms * tdc::persistent_occupancy(smem, a.BN);
+    const long long tiles = (long long)div_up((int)M, 128) * a.ntiles * std::max(1, a.gsplit);
+    // split-K: at most one CTA per SM, so every CTA is co-resident (piece-0 CTAs wait on others)
+    const long long cap = a.gsplit > 1 ? (long long)m->num_sms
+                                       : (long long)m->num_sms * tdc::persistent_occupancy(smem, a.BN);
     const int grid = (int)std::max<long long>(1, std::min(tiles, cap));
     if (a.tma_y && (dst != g.mapY_dst || M != g.mapY_rows)) {
         // extent = this call's rows: the last tile's 32-row blocks past M are clipped, not
@@ -520,6 +545,7 @@ void destroy(tdc_model_s *m) {
     for (auto &op : m->ops) {
         if (op.tkd) tdc_conv_plan_destroy(op.tkd);
         if (op.dense.d_w) cudaFree(op.dense.d_w);
+        if (op.dense.d_gs) cudaFree(op.dense.d_gs);
         if (op.dense.d_wdirect) cudaFree(op.dense.d_wdirect);
     }
     for (size_t i = 1; i < m->act.size(); ++i)
