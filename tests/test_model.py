@@ -160,3 +160,15 @@ def test_model_rejects_bad_graphs(gpu):
     bad[2]["c_in"] += 4          # geometry mismatch with its source
     with pytest.raises(tdc.TdcError):
         tdc.Model(bad, 2)
+
+
+@pytest.mark.gpu
+def test_vgg16_classifier_split_k_partial_batch_and_determinism(gpu):
+    """The VGG-16 classifier GEMMs (one M tile, K up to 25,088) run split-K through L2
+    (fixed pieces per plan): a partial batch equals the slice of the full batch bit for
+    bit and repeated forwards are identical."""
+    ops = sm.tucker_vgg16()
+    x = sm.model_input(3, 224, seed=11)
+    full = run_model(gpu, ops, x)
+    assert np.array_equal(full[:2], run_model(gpu, ops, x, batch=2))
+    assert np.array_equal(full, run_model(gpu, ops, x))
