@@ -388,10 +388,32 @@ tdc_status plan_dense(tdc_model_s *m, ModelOp &op, const tdc_model_op &o) {
     int BN = 32;
     const int bn_cap = std::getenv("TDC_DENSE_BN") ? std::atoi(std::getenv("TDC_DENSE_BN")) : 128;
     while (BN < N && BN < bn_cap) BN *= 2;
-    // few M tiles and a long K (classifiers, VGG FC1): keep the widest N tile -- A is
-    // re-read once per N tile -- and fill the SMs with split-K pieces instead (below)
-    const bool wide = div_up((int)Mmax, 128) <= 4 && K64 / 64 >= 8;
-    while (!wide && BN > 64 && div_up((int)Mmax, 128) * (long long)div_up(N, BN) < 2 * m->num_sms) BN /= 2;
+    // (N tile, split-K pieces) from a streaming model: every K chunk of a
+    // work unit moves 32 KB of fp32 A and 256*BN B bytes into the SM; A is re-read once per
+    // N tile and B once per M tile.  A CTA streams at ~40 GB/s and the chip at ~5 TB/s
+    // (measured on these kernels), so time ~ max(per-CTA bytes / 40 GB/s, all bytes /
+    // 5 TB/s) + the split-K fix-up traffic.  Pieces > 1 only when K is long (>= 8 chunks).
+    int gsp = 1;
+    {
+        const int mt = div_up((int)Mmax, 128), kch = K64 / 64, top = BN;
+        const bool gs_ok = kch >= 8 && !std::getenv("TDC_DENSE_NO_GSPLIT");
+        double best = 1e30;
+        int bbn = BN;
+        for (int b = top; b >= 32 && b >= top / 4; b /= 2)
+            for (int gq = 1; gq <= (gs_ok ? std::min(8, kch / 4) : 1); ++gq) {
+                const long long units = (long long)mt * div_up(N, b) * gq;
+                const double unit_bytes = (double)div_up(kch, gq) * (32768.0 + 256.0 * b);
+                const double waves = (double)div_up((int)units, m->num_sms);
+                const double t = std::max(waves * unit_bytes / 40e3, units * unit_bytes / 5e6) +
+                                 (gq > 1 ? 2.0 + (gq - 1) * (double)mt * div_up(N, b) * 128 * b * 8 / 5e6 : 0.0);
+                if (t < best * 0.97) {
+                    best = t;
+                    bbn = b;
+                    gsp = gq;
+                }
+            }
+        BN = bbn;
+    }
     const int R = round_up(N, BN);
     std::vector<double> scale, bias;
     bn_fold(o, N, scale, bias);
@@ -442,10 +464,6 @@ tdc_status plan_dense(tdc_model_s *m, ModelOp &op, const tdc_model_op &o) {
     // CTA adds the partials in piece order (deterministic) and runs the epilogue.
     {
         const long long tiles = (long long)div_up((int)Mmax, 128) * (R / BN);
-        const int kch = K64 / 64;
-        int gsp = 1;
-        if (tiles < m->num_sms && kch >= 8 && !std::getenv("TDC_DENSE_NO_GSPLIT"))
-            gsp = (int)std::max<long long>(1, std::min<long long>({8, kch / 4, m->num_sms / tiles}));
         if (gsp > 1) {
             const size_t parts = (size_t)tiles * (gsp - 1) * 128 * BN, flags = (size_t)tiles * (gsp - 1);
             e = cudaMalloc(&g.d_gs, parts * sizeof(float) + flags * sizeof(int));
