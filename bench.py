@@ -56,6 +56,7 @@ def parse():
                          "tf32: 1e-2 mode; fp32: CUDA-core FFMA")
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-model-sweep", action="store_true", help="skip the ResNet-50 batch 1..256 sweep")
     ap.add_argument("--no-model", action="store_true",
                     help="skip the Tucker ResNet-50 whole-model images/s measurement")
     ap.add_argument("--model-batch", type=int, default=32)
@@ -350,7 +351,8 @@ def impl_tdc(args):
     # sharded over the ranks, strong scaling).  Each rank runs the whole model on its own
     # shard (no collective beyond the timing barrier); images/s = all ranks' images /
     # max-over-ranks time.
-    def time_model(ops, mb):
+    def time_model(ops, mb, steps=None):
+        steps = steps or args.steps
         net = tdc.Model(ops, max_batch=mb, device=local)
         mh, mw, mc = net.output_shape()
         import synth.models as sm
@@ -371,7 +373,7 @@ def impl_tdc(args):
         torch.cuda.synchronize()
         m0.record(stream)
         with torch.cuda.stream(stream):
-            for _ in range(args.steps):
+            for _ in range(steps):
                 if mgraph is not None:
                     mgraph.replay()
                 else:
@@ -379,7 +381,7 @@ def impl_tdc(args):
         m1.record(stream)
         torch.cuda.synchronize()
         tdist.barrier()
-        mms = tdist.max_over_ranks(m0.elapsed_time(m1), "cuda") / args.steps
+        mms = tdist.max_over_ranks(m0.elapsed_time(m1), "cuda") / steps
         how = "cuda_graph_replay" if mgraph is not None else "stream_launches"
         mgraph = None
         net.close()
@@ -402,6 +404,13 @@ def impl_tdc(args):
             "math": "3xbf16 (fp32-grade)", "batch_per_gpu": vb, "global_batch": vb * world, "n_gpus": world,
             "scaling": "strong (global batch 64 sharded)", "ms_per_batch": round(vms, 4),
             "images_per_s": round(vb * world / (vms * 1e-3), 1), "launch": how}
+        if not args.no_model_sweep:  # BASELINE config 3: ResNet-50 at batch 1..256 per GPU
+            sweep = {}
+            for sb in (1, 8, 64, 128, 256):
+                sms, _ = time_model(sm.tucker_resnet(50, seed=synth.BASE_SEED + 1000 * rank), sb,
+                                    steps=max(3, min(args.steps, 10)))
+                sweep[str(sb)] = {"ms_per_batch": round(sms, 4), "images_per_s": round(sb * world / (sms * 1e-3), 1)}
+            model["tucker_resnet50"]["batch_sweep_per_gpu"] = sweep
 
     # ---- end to end through the host-buffer C-ABI call ----
     e2e = None
