@@ -1206,7 +1206,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             const bool valid = out_row(m0 + q * 32 + lane, &dst_row);
             const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + 2 * ncols + a3.slot * ncols3;
             float *dst = g.y + dst_row * g.N3;
-            for (int c = 0; c < g.N3p; c += 32) {
+            for (int c = 0; c < ((g.dbg & 64) ? 0 : g.N3p); c += 32) {  // dbg 64: no E3 TMEM loads
                 uint32_t rr[32];
                 float v[32];
                 tmem_ld_32x32b_x32(src + c, rr);
