@@ -20,6 +20,7 @@
 //   stage 3  A = Z hi/lo by TMA (bf16 boxes {64, 128}), B = U_out bf16,
 //            epilogue writes fp32 Y (+bias).
 #include <cuda.h>
+#include <type_traits>
 #include <cuda_bf16.h>
 
 #include "internal.h"
@@ -964,33 +965,37 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                         tc_fence_after();
                         if (tit == 0 && lane == 0) BFCTAP(kc * g.ngroups + grp, 1);
                         if (TG == 9 && g.ngroups == 1) {  // 3x3 core: fully unrolled taps
-                            if (elect_one()) {
-                                const uint64_t aslot = da + ((ra.slot * a_bytes) >> 4);
-                                const uint64_t bslot = db + ((ws * w_slot) >> 4);
+                            // Descriptor bases and per-tap offsets computed in converged code from
+                            // warp-uniform values (kernel parameters, ring cursors), so they live in
+                            // uniform registers and each MMA costs a uniform add; the hi|lo
+                            // concatenation branch is hoisted out of the unrolled stream.
+                            const uint64_t aslot = da + ((ra.slot * a_bytes) >> 4);
+                            const uint64_t bslot = db + ((ws * w_slot) >> 4);
+                            auto stream = [&](auto ncat) {
+                                if (elect_one()) {
 #pragma unroll
-                                for (int tt = 0; tt < 9; ++tt) {
-                                    // tap offsets straight from the kernel parameters (constant
-                                    // index -> uniform loads), so the descriptors stay in uniform
-                                    // registers without per-MMA register->uniform moves
-                                    const uint64_t a = aslot + (((uint32_t)g.tap_phase[tt] * 4 * band_bytes +
-                                                                 (uint32_t)g.tap_off[tt] * 16) >> 4);
-                                    const uint64_t b = bslot + tt * wtap16;
+                                    for (int tt = 0; tt < 9; ++tt) {
+                                        const uint64_t a = aslot + (((uint32_t)g.tap_phase[tt] * 4 * band_bytes +
+                                                                     (uint32_t)g.tap_off[tt] * 16) >> 4);
+                                        const uint64_t b = bslot + tt * wtap16;
 #pragma unroll
-                                    for (int j = 0; j < 2; ++j) {
-                                        const uint64_t aj = a + j * plane2a, bj = b + j * plane2b;
-                                        if (g.ncat) {
+                                        for (int j = 0; j < 2; ++j) {
+                                            const uint64_t aj = a + j * plane2a, bj = b + j * plane2b;
                                             mma_bf16(d, aj, bj, idesc, accum);
-                                            mma_bf16(d, aj + a_lo, bj, idesc, 1);
-                                        } else {
-                                            mma_bf16(d, aj, bj, idesc, accum);
-                                            mma_bf16(d, aj, bj + b_lo, idesc, 1);
-                                            mma_bf16(d, aj + a_lo, bj, idesc, 1);
+                                            if (decltype(ncat)::value) {
+                                                mma_bf16(d, aj + a_lo, bj, idesc, 1);
+                                            } else {
+                                                mma_bf16(d, aj, bj + b_lo, idesc, 1);
+                                                mma_bf16(d, aj + a_lo, bj, idesc, 1);
+                                            }
+                                            accum = 1;
                                         }
-                                        accum = 1;
                                     }
+                                    if (!resident) mma_commit(&w_empty[ws]);
                                 }
-                                if (!resident) mma_commit(&w_empty[ws]);
-                            }
+                            };
+                            if (g.ncat) stream(std::integral_constant<bool, true>());
+                            else stream(std::integral_constant<bool, false>());
                         } else if (elect_one()) {
                             for (int tt = 0; tt < TG; ++tt) {
                                 const int tap = grp * TG + tt;
