@@ -159,7 +159,10 @@ struct BfCoreArgs {
     int relu;                 // fused stage 3: ReLU after bias/residual
     int dbg;                  // debug (TDC_CORE_DBG): 1 skip Y stores, 2 skip Z smem writes,
                               // 4 skip band reloads after the first tile, 8 skip S3 MMAs,
-                              // 16 no acc2-free wait, 32 no E2 TMEM loads, 64 no E3 TMEM loads
+                              // 16 no acc2-free wait, 32 no E2 TMEM loads, 64 no E3 TMEM loads,
+                              // 256 no stage 3 at all (no S3 waits/commits, E3 idle), 512 MMA warp
+                              // does not wait for bands after the first tile, 1024 (with 512) no
+                              // per-tile weight wait or band-slot commit
     int gsplit;               // stage 2 alone: >1 = split the D1 chunks into gsplit pieces (L2 partials)
     float *part;              // gsplit: fp32 partial tiles [tiles][gsplit-1][BN/4][128][4]
     int *flags;               // gsplit: one flag per (tile, piece > 0)

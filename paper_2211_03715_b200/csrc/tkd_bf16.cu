@@ -896,7 +896,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             const int k0 = GS > 1 ? pc * g.kchunks / GS : ck0, k1 = GS > 1 ? (pc + 1) * g.kchunks / GS : ck1;
             const int m0 = (t % mtiles) * kBM16, nt = t / mtiles;
             for (int kc = k0; kc < k1; ++kc, ra.next()) {
-                mbar_wait_sleep(&a_empty[ra.slot], ra.phase ^ 1);
+                if (!(g.dbg & 1024) || tit < 2) mbar_wait_sleep(&a_empty[ra.slot], ra.phase ^ 1);
                 if (kc == k0 && lane == 0) BFCTL(tit, 0);  // producer: band issue
                 const bool stale = (g.dbg & 4) && tit >= 2;  // debug: keep the stale band
                 if (lane == 0) mbar_arrive_expect_tx(&a_full[ra.slot], stale ? 0u : a_bytes);
@@ -951,13 +951,13 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                 const uint32_t d = tmem + acc.slot * ncols;
                 uint32_t accum = 0;
                 for (int kc = k0; kc < k1; ++kc, ra.next()) {
-                    mbar_wait(&a_full[ra.slot], ra.phase);
+                    if (!(g.dbg & 512) || tit == 0) mbar_wait(&a_full[ra.slot], ra.phase);  // dbg 512: stale bands
                     if (kc == k0 && lane == 0) BFCTL(tit, 2);  // MMA: band landed
                     for (int grp = 0; grp < g.ngroups; ++grp) {
                         int ws;
                         if (resident) {
                             ws = kc * g.ngroups + grp;
-                            mbar_wait(&w_full[ws], 0);
+                            if (!(g.dbg & 1024) || tit == 0) mbar_wait(&w_full[ws], 0);
                         } else {
                             ws = rw.slot;
                             mbar_wait(&w_full[ws], rw.phase);
@@ -1024,7 +1024,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                         accum = 1;
                         if (!resident) rw.next();
                     }
-                    if (elect_one()) mma_commit(&a_empty[ra.slot]);
+                    if (!(g.dbg & 1024) && elect_one()) mma_commit(&a_empty[ra.slot]);  // dbg 1024: none
                     __syncwarp();
                 }
                 if (elect_one()) mma_commit(&tfull[acc.slot]);
@@ -1032,7 +1032,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                 acc.next();
                 if (lane == 0) BFCTL(tit, 3);  // MMA: all issued
             }
-            if (F3 && pending) {  // ---- stage 3 of the previous tile
+            if (F3 && pending && !(g.dbg & 256)) {  // ---- stage 3 of the previous tile (dbg 256: none)
                 mbar_wait(&t3empty[a3.slot], a3.phase ^ 1);
                 if (lane == 0) BFCTL(tit - 1, 6);  // S3: acc3 buffer free
                 mbar_wait(&z_full[zr.slot], zr.phase);
@@ -1126,7 +1126,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             }
             long long dst_row = 0;
             const bool valid = out_row(m0 + r, &dst_row);
-            if (F3) mbar_wait_sleep(&z_empty[zr.slot], zr.phase ^ 1);
+            if (F3 && !(g.dbg & 256)) mbar_wait_sleep(&z_empty[zr.slot], zr.phase ^ 1);
             const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
             const uint32_t zb = smem_u32(zs) + zr.slot * zbuf;
             const bool gpart = GS > 1 && pc > 0;  // split-K piece: fp32 partial -> L2 workspace
@@ -1202,7 +1202,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         float *scratch = epi_scratch + q * 1024;
         Ring a3(2);
         int tit = 0;
-        for (int t = cid; t < num_tiles; t += ncl, a3.next(), ++tit) {
+        for (int t = (g.dbg & 256) ? num_tiles : cid; t < num_tiles; t += ncl, a3.next(), ++tit) {
             const int m0 = (t % mtiles) * kBM16;
             mbar_wait_sleep(&t3full[a3.slot], a3.phase);
             tc_fence_after();

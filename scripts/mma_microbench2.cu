@@ -4,6 +4,7 @@
 // issue-loop overheads.  Debug tool, not product.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2211_03715_b200/csrc
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "sm100.cuh"
@@ -390,7 +391,7 @@ template <int VAR>
 void run_core(long long *d) {
     auto k = bench_core<VAR>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 201 * 1024);
-    const int tiles = 64, grid = 148;
+    const int tiles = getenv("MB_TILES") ? atoi(getenv("MB_TILES")) : 64, grid = 148;
     k<<<grid, 128, 201 * 1024>>>(tiles, d);
     cudaError_t e = cudaDeviceSynchronize();
     long long h[512];
@@ -425,6 +426,10 @@ void run(long long *d, int ctas_per_sm) {
 int main() {
     long long *d;
     cudaMalloc(&d, 8 * 512);
+    if (getenv("MB_CORE_ONLY")) {  // the core kernel's MMA pattern only (MB_TILES tiles per CTA)
+        run_core<0>(d); run_core<6>(d);
+        return 0;
+    }
 #define ALLN(BF, M, TS, E) run<BF, M, 32, TS, E>(d, 1); run<BF, M, 64, TS, E>(d, 1); \
     run<BF, M, 128, TS, E>(d, 1); run<BF, M, 256, TS, E>(d, 1);
     run_core<0>(d); run_core<1>(d); run_core<2>(d); run_core<3>(d); run_core<4>(d); run_core<5>(d); run_core<6>(d);
