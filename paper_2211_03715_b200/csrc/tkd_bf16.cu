@@ -965,15 +965,16 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                         tc_fence_after();
                         if (tit == 0 && lane == 0) BFCTAP(kc * g.ngroups + grp, 1);
                         if (TG == 9 && g.ngroups == 1) {  // 3x3 core: fully unrolled taps
-                            // Descriptor bases and per-tap offsets computed in converged code from
-                            // warp-uniform values (kernel parameters, ring cursors), so they live in
-                            // uniform registers and each MMA costs a uniform add; the hi|lo
-                            // concatenation branch is hoisted out of the unrolled stream.
+                            // Descriptor bases computed in converged code from warp-uniform values
+                            // (kernel parameters, ring cursors) so they live in uniform registers;
+                            // the hi|lo concatenation branch is hoisted out of the stream.  The tap
+                            // loop stays rolled: the fully unrolled stream measured slower (code
+                            // size).
                             const uint64_t aslot = da + ((ra.slot * a_bytes) >> 4);
                             const uint64_t bslot = db + ((ws * w_slot) >> 4);
                             auto stream = [&](auto ncat) {
                                 if (elect_one()) {
-#pragma unroll
+#pragma unroll 1
                                     for (int tt = 0; tt < 9; ++tt) {
                                         const uint64_t a = aslot + (((uint32_t)g.tap_phase[tt] * 4 * band_bytes +
                                                                      (uint32_t)g.tap_off[tt] * 16) >> 4);
