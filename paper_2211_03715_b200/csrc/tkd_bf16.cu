@@ -31,6 +31,17 @@ namespace tdc {
 
 using namespace sm100;
 
+// Debug knobs (TDC_CORE_DBG / TDC_GEMM_DBG bits, TDC_Y_DIRECT) exist only in debug builds
+// (-DTDC_DEBUG_KNOBS, implied by the timeline build): the production kernels carry no
+// knob branches in their hot loops (smaller code).
+#if defined(TDC_DEBUG_KNOBS) || defined(TDC_TIMELINE)
+#define TDC_DBG(g, bit) ((g).dbg & (bit))
+#define TDC_YDIRECT(g) ((g).y_direct)
+#else
+#define TDC_DBG(g, bit) 0
+#define TDC_YDIRECT(g) 0
+#endif
+
 #ifdef TDC_TIMELINE
 __device__ unsigned long long g_tdc_bf_tl[4 * 64 * 8];
 __device__ unsigned int g_tdc_bf_seq;
@@ -438,7 +449,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         float *scratch = epi_scratch + q * (g.out_bf16 ? 1024 : NR * 1024);
         // fp32 output ring (tma_y): chunk counter of this warp -> buffer and residual parity
         const bool ring = !g.out_bf16 && g.tma_y && (g.ldo & 3) == 0;
-        const bool rres = ring && g.res && !(g.dbg & 2);
+        const bool rres = ring && g.res && !TDC_DBG(g, 2);
         const uint32_t ring_s = smem_u32(scratch);
         uint32_t yc = 0;
         auto full_chunk = [&](int n) { return n + 32 <= g.Nn; };
@@ -572,7 +583,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                         }
                     }
                     epi_bias_res_relu<32>(v, n, g.Nn, g.bias, nullptr, g.relu);
-                    if (!(g.dbg & 1)) {
+                    if (!TDC_DBG(g, 1)) {
 #pragma unroll
                         for (int j4 = 0; j4 < 8; ++j4)
                             st_shared_v4(buf + (uint32_t)(lane * 128 + ((j4 ^ (lane & 7)) << 4)), v[4 * j4],
@@ -590,8 +601,8 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                     ++yc;
                 } else {  // fp32 Y (+bias, +residual, ReLU), row-major, coalesced through shared memory
                     const bool full = n + 32 <= g.Nn && (g.ldo & 3) == 0;
-                    if (g.dbg & 1) continue;
-                    if (g.res && full && !(g.dbg & 2)) {  // residual block read coalesced, then per-lane rows
+                    if (TDC_DBG(g, 1)) continue;
+                    if (g.res && full && !TDC_DBG(g, 2)) {  // residual block read coalesced, then per-lane rows
                         float rv[32];
                         warp_load_block32(scratch, rv, valid ? g.res + dst_row * g.ldo + n : nullptr, lane);
 #pragma unroll
@@ -896,9 +907,9 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             const int k0 = GS > 1 ? pc * g.kchunks / GS : ck0, k1 = GS > 1 ? (pc + 1) * g.kchunks / GS : ck1;
             const int m0 = (t % mtiles) * kBM16, nt = t / mtiles;
             for (int kc = k0; kc < k1; ++kc, ra.next()) {
-                if (!(g.dbg & 1024) || tit < 2) mbar_wait_sleep(&a_empty[ra.slot], ra.phase ^ 1);
+                if (!TDC_DBG(g, 1024) || tit < 2) mbar_wait_sleep(&a_empty[ra.slot], ra.phase ^ 1);
                 if (kc == k0 && lane == 0) BFCTL(tit, 0);  // producer: band issue
-                const bool stale = (g.dbg & 4) && tit >= 2;  // debug: keep the stale band
+                const bool stale = TDC_DBG(g, 4) && tit >= 2;  // debug: keep the stale band
                 if (lane == 0) mbar_arrive_expect_tx(&a_full[ra.slot], stale ? 0u : a_bytes);
                 __syncwarp();
                 uint8_t *dst = a_slots + (size_t)ra.slot * a_bytes;
@@ -945,19 +956,19 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             const int pc = u % GS;
             const int k0 = GS > 1 ? pc * g.kchunks / GS : ck0, k1 = GS > 1 ? (pc + 1) * g.kchunks / GS : ck1;
             if (have) {
-                if (!(g.dbg & 16)) mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
+                if (!TDC_DBG(g, 16)) mbar_wait(&tempty[acc.slot], acc.phase ^ 1);
                 tc_fence_after();
                 if (lane == 0) BFCTL(tit, 1);  // MMA: accumulator free
                 const uint32_t d = tmem + acc.slot * ncols;
                 uint32_t accum = 0;
                 for (int kc = k0; kc < k1; ++kc, ra.next()) {
-                    if (!(g.dbg & 512) || tit == 0) mbar_wait(&a_full[ra.slot], ra.phase);  // dbg 512: stale bands
+                    if (!TDC_DBG(g, 512) || tit == 0) mbar_wait(&a_full[ra.slot], ra.phase);  // dbg 512: stale bands
                     if (kc == k0 && lane == 0) BFCTL(tit, 2);  // MMA: band landed
                     for (int grp = 0; grp < g.ngroups; ++grp) {
                         int ws;
                         if (resident) {
                             ws = kc * g.ngroups + grp;
-                            if (!(g.dbg & 1024) || tit == 0) mbar_wait(&w_full[ws], 0);
+                            if (!TDC_DBG(g, 1024) || tit == 0) mbar_wait(&w_full[ws], 0);
                         } else {
                             ws = rw.slot;
                             mbar_wait(&w_full[ws], rw.phase);
@@ -1025,7 +1036,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                         accum = 1;
                         if (!resident) rw.next();
                     }
-                    if (!(g.dbg & 1024) && elect_one()) mma_commit(&a_empty[ra.slot]);  // dbg 1024: none
+                    if (!TDC_DBG(g, 1024) && elect_one()) mma_commit(&a_empty[ra.slot]);  // dbg 1024: none
                     __syncwarp();
                 }
                 if (elect_one()) mma_commit(&tfull[acc.slot]);
@@ -1033,7 +1044,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                 acc.next();
                 if (lane == 0) BFCTL(tit, 3);  // MMA: all issued
             }
-            if (F3 && pending && !(g.dbg & 256)) {  // ---- stage 3 of the previous tile (dbg 256: none)
+            if (F3 && pending && !TDC_DBG(g, 256)) {  // ---- stage 3 of the previous tile (dbg 256: none)
                 mbar_wait(&t3empty[a3.slot], a3.phase ^ 1);
                 if (lane == 0) BFCTL(tit - 1, 6);  // S3: acc3 buffer free
                 mbar_wait(&z_full[zr.slot], zr.phase);
@@ -1041,7 +1052,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                 if (lane == 0) BFCTL(tit - 1, 7);  // S3: Z ready, issuing
                 if (elect_one()) {
                     const uint32_t d3 = tmem + 2 * ncols + a3.slot * ncols3;
-                    if (g.dbg & 8) {  // debug: no stage-3 MMAs
+                    if (TDC_DBG(g, 8)) {  // debug: no stage-3 MMAs
                         mma_commit(&z_empty[zr.slot]);
                         mma_commit(&t3full[a3.slot]);
                     } else {
@@ -1127,13 +1138,13 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             }
             long long dst_row = 0;
             const bool valid = out_row(m0 + r, &dst_row);
-            if (F3 && !(g.dbg & 256)) mbar_wait_sleep(&z_empty[zr.slot], zr.phase ^ 1);
+            if (F3 && !TDC_DBG(g, 256)) mbar_wait_sleep(&z_empty[zr.slot], zr.phase ^ 1);
             const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
             const uint32_t zb = smem_u32(zs) + zr.slot * zbuf;
             const bool gpart = GS > 1 && pc > 0;  // split-K piece: fp32 partial -> L2 workspace
             if (GS > 1 && pc == 0)
                 for (int pp = 1; pp < GS; ++pp) gs_wait(g.flags + t * (GS - 1) + pp - 1);
-            for (int c = 0; c < ((g.dbg & 32) ? 0 : BN); c += 32) {
+            for (int c = 0; c < (TDC_DBG(g, 32) ? 0 : BN); c += 32) {
                 uint32_t rr[32];
                 float v[32];
                 tmem_ld_32x32b_x32(src + c, rr);
@@ -1154,7 +1165,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                 }
                 for (int pp = 1; pp < GS; ++pp)  // partials in piece order (deterministic)
                     gs_add32(g.part + (size_t)(t * (GS - 1) + pp - 1) * 128 * BN, c, r, v);
-                if (F3 && (g.dbg & 2)) {
+                if (F3 && TDC_DBG(g, 2)) {
                 } else if (F3) {  // Z hi/lo planes [c/8 + pl][row r][16 B] (conflict-free: lanes = rows)
 #pragma unroll
                     for (int pl = 0; pl < 4; ++pl) {
@@ -1203,7 +1214,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         float *scratch = epi_scratch + q * 1024;
         Ring a3(2);
         int tit = 0;
-        for (int t = (g.dbg & 256) ? num_tiles : cid; t < num_tiles; t += ncl, a3.next(), ++tit) {
+        for (int t = TDC_DBG(g, 256) ? num_tiles : cid; t < num_tiles; t += ncl, a3.next(), ++tit) {
             const int m0 = (t % mtiles) * kBM16;
             mbar_wait_sleep(&t3full[a3.slot], a3.phase);
             tc_fence_after();
@@ -1212,7 +1223,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             const bool valid = out_row(m0 + q * 32 + lane, &dst_row);
             const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + 2 * ncols + a3.slot * ncols3;
             float *dst = g.y + dst_row * g.N3;
-            for (int c = 0; c < ((g.dbg & 64) ? 0 : g.N3p); c += 32) {  // dbg 64: no E3 TMEM loads
+            for (int c = 0; c < (TDC_DBG(g, 64) ? 0 : g.N3p); c += 32) {  // dbg 64: no E3 TMEM loads
                 uint32_t rr[32];
                 float v[32];
                 tmem_ld_32x32b_x32(src + c, rr);
@@ -1227,7 +1238,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
                 }
-                if (c >= g.N3 || (g.dbg & 1)) continue;  // warp-uniform
+                if (c >= g.N3 || TDC_DBG(g, 1)) continue;  // warp-uniform
                 if (g.res && c + 32 <= g.N3 && (g.N3 & 3) == 0) {  // coalesced residual block
                     float rv[32];
                     warp_load_block32(scratch, rv, valid ? g.res + dst_row * g.N3 + c : nullptr, lane);
@@ -1239,7 +1250,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                                           g.relu);
                 }
                 if (c + 32 <= g.N3 && (g.N3 & 3) == 0) {
-                    if (g.y_direct) {  // each lane stores its own row: no shared-memory traffic
+                    if (TDC_YDIRECT(g)) {  // each lane stores its own row: no shared-memory traffic
                         if (valid)
 #pragma unroll
                             for (int j = 0; j < 8; ++j)

@@ -1,4 +1,6 @@
 # A/B of core3 epilogue knobs on the two core3 layers (56x56 s1, 28x28 s1)
+# debug knobs (TDC_*_DBG, TDC_Y_DIRECT) exist only in the debug/timeline build
+export TDC_LIB=paper_2211_03715_b200/libtdc_tl.so  # python paper_2211_03715_b200/build.py --timeline
 mkdir -p gpurun_out/g3
 o=gpurun_out/g3/knobs.txt
 echo base >> $o; python scripts/layer_bench.py 3xbf16 0 2 >> $o 2>&1
