@@ -253,7 +253,7 @@ __device__ __forceinline__ void gs_publish(int *flag, bool leader) {
 // ============================================================ GEMM (stages 1, 3)
 constexpr int kConvThreads16 = 256;  // 8 converter warps (stage 1 is converter-paced otherwise)
 
-template <bool CONVERT>
+template <bool CONVERT, bool CLUSTER>  // CLUSTER: cluster split-K code compiled in (opt-in)
 __global__ void __launch_bounds__(CONVERT ? 192 + kConvThreads16 : 192, 1)
 tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo,
@@ -280,7 +280,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     uint8_t *bring = smem + (size_t)(CONVERT ? SX : S) * slot_bytes;
     float *epi_scratch = reinterpret_cast<float *>(bring + (size_t)SB * bslot);
     // split-K (cluster of CS CTAs over K): fp32 partial tile [128][BN], float4-swizzled
-    const int CS = g.ksplit > 1 ? g.ksplit : 1;
+    const int CS = (CLUSTER && g.ksplit > 1) ? g.ksplit : 1;
     float *red = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(epi_scratch) + bf_epi_bytes(CONVERT, g.out_bf16, g.yring));
     uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(red) +
                                                   (CS > 1 ? (size_t)128 * BN * 4 : 0));
@@ -734,19 +734,19 @@ cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, c
     if (!mapR) mapR = &mapY;
     const int smem = bf_smem_bytes(g.BN, g.stages, g.a_convert ? g.xstages : 0, g.ksplit, g.a_convert ? g.bstages : 0,
                                    g.out_bf16 ? 0 : bf_yring(true, g.yring));
-    cudaError_t e;
-    if (g.a_convert) {
-        e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    // the cluster split-K variant is a separate instantiation, so the default kernels carry
+    // none of its code (smaller hot loops)
+    auto go = [&](auto kernel, int threads) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        return launch_pdl_cluster(tdc_bf_gemm_kernel<true>, grid, 192 + kConvThreads16, smem, st, g.ksplit, mapA,
-                                  mapAlo, mapB, mapBlo, mapY, *mapR, g);
-    } else {
-        e = cudaFuncSetAttribute(tdc_bf_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        return launch_pdl_cluster(tdc_bf_gemm_kernel<false>, grid, 192, smem, st, g.ksplit, mapA, mapAlo, mapB,
-                                  mapBlo, mapY, *mapR, g);
-    }
-    return cudaGetLastError();
+        return launch_pdl_cluster(kernel, grid, threads, smem, st, g.ksplit, mapA, mapAlo, mapB, mapBlo, mapY, *mapR,
+                                  g);
+    };
+    const bool cl = g.ksplit > 1;
+    if (g.a_convert)
+        return cl ? go(tdc_bf_gemm_kernel<true, true>, 192 + kConvThreads16)
+                  : go(tdc_bf_gemm_kernel<true, false>, 192 + kConvThreads16);
+    return cl ? go(tdc_bf_gemm_kernel<false, true>, 192) : go(tdc_bf_gemm_kernel<false, false>, 192);
 }
 
 // ============================================================ core conv (stage 2)
