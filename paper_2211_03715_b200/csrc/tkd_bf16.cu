@@ -789,7 +789,7 @@ int bf_core3_tmem_cols(const BfCoreArgs &g) { return bf_core3_tmem(g); }
 // bf16 hi/lo by the epilogue-2 warps straight into shared memory, stage 3 multiplies
 // it with the resident U_out panel, epilogue-3 warps write Y (+bias).  Z never
 // touches HBM.  MMA issue is software-pipelined: S2(tile i) then S3(tile i-1).
-template <bool F3>
+template <bool F3, bool CLUSTER>  // CLUSTER: cluster split-K code compiled in (opt-in, stage 2 alone)
 __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const BfCoreArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
@@ -806,7 +806,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
     uint8_t *w_slots = smem + 2 * (size_t)a_bytes;
     float *epi_scratch = reinterpret_cast<float *>(w_slots + (size_t)WS * w_slot);
     uint8_t *zs = reinterpret_cast<uint8_t *>(epi_scratch) + kEpiScratch16;  // F3: 2 Z buffers
-    const int CS = (!F3 && g.ksplit > 1) ? g.ksplit : 1;                      // split-K cluster size
+    const int CS = (!F3 && CLUSTER && g.ksplit > 1) ? g.ksplit : 1;           // split-K cluster size
     float *red = reinterpret_cast<float *>(zs);                              // split-K partial [128][BN]
     const uint32_t red_bytes = CS > 1 ? (uint32_t)128 * BN * 4 : 0u;
     uint8_t *w3s = zs + 2 * (size_t)zbuf + red_bytes;                        // F3: U_out panel
@@ -1277,18 +1277,20 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
 
 cudaError_t bf_core_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
     const int smem = bf_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.tg, g.w_slots, g.ksplit);
-    cudaError_t e =
-        cudaFuncSetAttribute(tdc_bf_core_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    return launch_pdl_cluster(tdc_bf_core_kernel<false>, grid, 192, smem, st, g.ksplit, g);
+    auto go = [&](auto kernel) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        return launch_pdl_cluster(kernel, grid, 192, smem, st, g.ksplit, g);
+    };
+    return g.ksplit > 1 ? go(tdc_bf_core_kernel<false, true>) : go(tdc_bf_core_kernel<false, false>);
 }
 
 cudaError_t bf_core3_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
     const int smem = bf_core3_smem_bytes(g);
     cudaError_t e =
-        cudaFuncSetAttribute(tdc_bf_core_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(tdc_bf_core_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(tdc_bf_core_kernel<true>, grid, 320, smem, st, g);
+    return launch_pdl(tdc_bf_core_kernel<true, false>, grid, 320, smem, st, g);
 }
 
 }  // namespace tdc

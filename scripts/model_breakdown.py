@@ -1,4 +1,5 @@
 """Map an ncu launch list of one Tucker ResNet-50 forward (scripts/model_profile.py) to ops."""
+import re
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from scripts.parse_launches import load
@@ -22,7 +23,7 @@ def count(start):
     i = start; n = 0
     for o, nl in zip(ops, nl_of):
         if nl is None:
-            nl = 2 if "core_kernel<1>" in ks[i + 1]["name"] else 3
+            nl = 2 if re.search(r"core_kernel<(\(bool\))?(1|true)[,>]", ks[i + 1]["name"]) else 3
         i += nl; n += nl
     return n
 n = count(len(ks) - 200 if len(ks) > 200 else 0)
@@ -30,7 +31,7 @@ last = ks[-n:]
 i = 0; rows = []
 for oi, (o, nl) in enumerate(zip(ops, nl_of)):
     if nl is None:
-        nl = 2 if "core_kernel<1>" in last[i + 1]["name"] else 3
+        nl = 2 if re.search(r"core_kernel<(\(bool\))?(1|true)[,>]", last[i + 1]["name"]) else 3
     t = sum(x.get("gpu__time_duration.sum", 0) for x in last[i:i + nl]) / 1e3
     rows.append((t, oi, o["kind"], o["c_in"], o["c_out"], o["kernel"], o["stride"], o["height"], nl))
     i += nl

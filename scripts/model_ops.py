@@ -5,6 +5,7 @@ import csv
 import io
 import json
 import os
+import re
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -39,7 +40,7 @@ for oi, o in enumerate(ops):
     if kind == 0:
         n = 1 if (C <= 4 or (K == 1 and s == 1 and o["pad"] == 0)) else 2
     elif kind == 1:
-        n = 2 if "core_kernel<true>" in ks[i + 1]["name"] or "core_kernel<1>" in ks[i + 1]["name"] else 3
+        n = 2 if re.search(r"core_kernel<(\(bool\))?(1|true)[,>]", ks[i + 1]["name"]) else 3
     else:
         n = 1
     t = sum(k["t"] for k in ks[i:i + n])

@@ -4,6 +4,7 @@ Usage: python scripts/ncu_traffic.py <math> <launches.csv>"""
 import json
 import os
 import statistics
+import re
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -18,9 +19,9 @@ ks = load(path)
 groups, i = [], 0
 while i < len(ks):
     n = ks[i]["name"]
-    if "tdc_bf_gemm_kernel<1>" in n:
+    if re.search(r"tdc_bf_gemm_kernel<(\(bool\))?(1|true)[,>]", n):
         j = i + 1
-        while j < len(ks) and "tdc_bf_gemm_kernel<1>" not in ks[j]["name"] and j - i < 3:
+        while j < len(ks) and not re.search(r"tdc_bf_gemm_kernel<(\(bool\))?(1|true)[,>]", ks[j]["name"]) and j - i < 3:
             j += 1
         groups.append(ks[i:j])
         i = j
