@@ -253,7 +253,7 @@ __device__ __forceinline__ void gs_publish(int *flag, bool leader) {
 // ============================================================ GEMM (stages 1, 3)
 constexpr int kConvThreads16 = 256;  // 8 converter warps (stage 1 is converter-paced otherwise)
 
-template <bool CONVERT, bool CLUSTER>  // CLUSTER: cluster split-K code compiled in (opt-in)
+template <bool CONVERT, int KS>  // KS: 0 plain, 1 cluster split-K, 2 split-K through L2 (code compiled in)
 __global__ void __launch_bounds__(CONVERT ? 192 + kConvThreads16 : 192, 1)
 tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo,
@@ -280,7 +280,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     uint8_t *bring = smem + (size_t)(CONVERT ? SX : S) * slot_bytes;
     float *epi_scratch = reinterpret_cast<float *>(bring + (size_t)SB * bslot);
     // split-K (cluster of CS CTAs over K): fp32 partial tile [128][BN], float4-swizzled
-    const int CS = (CLUSTER && g.ksplit > 1) ? g.ksplit : 1;
+    const int CS = (KS == 1 && g.ksplit > 1) ? g.ksplit : 1;
     float *red = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(epi_scratch) + bf_epi_bytes(CONVERT, g.out_bf16, g.yring));
     uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(red) +
                                                   (CS > 1 ? (size_t)128 * BN * 4 : 0));
@@ -306,7 +306,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     const int crank = CS > 1 ? (int)cluster_ctarank() : 0;
     const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;  // cluster id / count
     const int ci0 = crank * iters / CS, ci1 = (crank + 1) * iters / CS;  // cluster split: this CTA's K range
-    const int GS = (CS == 1 && g.gsplit > 1) ? g.gsplit : 1;              // split-K through L2
+    const int GS = (KS == 2 && g.gsplit > 1) ? g.gsplit : 1;              // split-K through L2
     const int num_units = num_tiles * GS;
 #ifdef TDC_TIMELINE
     const int seq = (int)*(volatile unsigned int *)&g_tdc_bf_seq;
@@ -742,11 +742,14 @@ cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, c
         return launch_pdl_cluster(kernel, grid, threads, smem, st, g.ksplit, mapA, mapAlo, mapB, mapBlo, mapY, *mapR,
                                   g);
     };
-    const bool cl = g.ksplit > 1;
-    if (g.a_convert)
-        return cl ? go(tdc_bf_gemm_kernel<true, true>, 192 + kConvThreads16)
-                  : go(tdc_bf_gemm_kernel<true, false>, 192 + kConvThreads16);
-    return cl ? go(tdc_bf_gemm_kernel<false, true>, 192) : go(tdc_bf_gemm_kernel<false, false>, 192);
+    const int ks = g.ksplit > 1 ? 1 : (g.gsplit > 1 ? 2 : 0);
+    if (g.a_convert) {
+        const int th = 192 + kConvThreads16;
+        return ks == 1 ? go(tdc_bf_gemm_kernel<true, 1>, th)
+                       : (ks == 2 ? go(tdc_bf_gemm_kernel<true, 2>, th) : go(tdc_bf_gemm_kernel<true, 0>, th));
+    }
+    return ks == 1 ? go(tdc_bf_gemm_kernel<false, 1>, 192)
+                   : (ks == 2 ? go(tdc_bf_gemm_kernel<false, 2>, 192) : go(tdc_bf_gemm_kernel<false, 0>, 192));
 }
 
 // ============================================================ core conv (stage 2)
@@ -789,7 +792,7 @@ int bf_core3_tmem_cols(const BfCoreArgs &g) { return bf_core3_tmem(g); }
 // bf16 hi/lo by the epilogue-2 warps straight into shared memory, stage 3 multiplies
 // it with the resident U_out panel, epilogue-3 warps write Y (+bias).  Z never
 // touches HBM.  MMA issue is software-pipelined: S2(tile i) then S3(tile i-1).
-template <bool F3, bool CLUSTER>  // CLUSTER: cluster split-K code compiled in (opt-in, stage 2 alone)
+template <bool F3, int KS>  // KS: 0 plain, 1 cluster split-K, 2 split-K through L2 (stage 2 alone)
 __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const BfCoreArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
@@ -806,7 +809,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
     uint8_t *w_slots = smem + 2 * (size_t)a_bytes;
     float *epi_scratch = reinterpret_cast<float *>(w_slots + (size_t)WS * w_slot);
     uint8_t *zs = reinterpret_cast<uint8_t *>(epi_scratch) + kEpiScratch16;  // F3: 2 Z buffers
-    const int CS = (!F3 && CLUSTER && g.ksplit > 1) ? g.ksplit : 1;           // split-K cluster size
+    const int CS = (!F3 && KS == 1 && g.ksplit > 1) ? g.ksplit : 1;           // split-K cluster size
     float *red = reinterpret_cast<float *>(zs);                              // split-K partial [128][BN]
     const uint32_t red_bytes = CS > 1 ? (uint32_t)128 * BN * 4 : 0u;
     uint8_t *w3s = zs + 2 * (size_t)zbuf + red_bytes;                        // F3: U_out panel
@@ -836,7 +839,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
     const int crank = CS > 1 ? (int)cluster_ctarank() : 0;
     const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;                 // cluster id / count
     const int ck0 = crank * g.kchunks / CS, ck1 = (crank + 1) * g.kchunks / CS;  // cluster split: chunks
-    const int GS = (!F3 && CS == 1 && g.gsplit > 1) ? g.gsplit : 1;                // split-K through L2
+    const int GS = (!F3 && KS == 2 && g.gsplit > 1) ? g.gsplit : 1;                // split-K through L2
     const int num_units = num_tiles * GS;
 
     if (threadIdx.x == 0) {
@@ -1282,15 +1285,16 @@ cudaError_t bf_core_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         return launch_pdl_cluster(kernel, grid, 192, smem, st, g.ksplit, g);
     };
-    return g.ksplit > 1 ? go(tdc_bf_core_kernel<false, true>) : go(tdc_bf_core_kernel<false, false>);
+    return g.ksplit > 1 ? go(tdc_bf_core_kernel<false, 1>)
+                        : (g.gsplit > 1 ? go(tdc_bf_core_kernel<false, 2>) : go(tdc_bf_core_kernel<false, 0>));
 }
 
 cudaError_t bf_core3_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
     const int smem = bf_core3_smem_bytes(g);
     cudaError_t e =
-        cudaFuncSetAttribute(tdc_bf_core_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(tdc_bf_core_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return launch_pdl(tdc_bf_core_kernel<true, false>, grid, 320, smem, st, g);
+    return launch_pdl(tdc_bf_core_kernel<true, 0>, grid, 320, smem, st, g);
 }
 
 }  // namespace tdc
