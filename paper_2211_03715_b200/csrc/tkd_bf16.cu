@@ -253,7 +253,9 @@ __device__ __forceinline__ void gs_publish(int *flag, bool leader) {
 // ============================================================ GEMM (stages 1, 3)
 constexpr int kConvThreads16 = 256;  // 8 converter warps (stage 1 is converter-paced otherwise)
 
-template <bool CONVERT, int KS>  // KS: 0 plain, 1 cluster split-K, 2 split-K through L2 (code compiled in)
+// KS: 0 plain, 1 cluster split-K, 2 split-K through L2; OB: bf16 planar X' output (stage 1)
+// rather than fp32 -- each instantiation carries only the epilogue code it runs.
+template <bool CONVERT, int KS, bool OB>
 __global__ void __launch_bounds__(CONVERT ? 192 + kConvThreads16 : 192, 1)
 tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
                    const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo,
@@ -281,7 +283,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     float *epi_scratch = reinterpret_cast<float *>(bring + (size_t)SB * bslot);
     // split-K (cluster of CS CTAs over K): fp32 partial tile [128][BN], float4-swizzled
     const int CS = (KS == 1 && g.ksplit > 1) ? g.ksplit : 1;
-    float *red = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(epi_scratch) + bf_epi_bytes(CONVERT, g.out_bf16, g.yring));
+    float *red = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(epi_scratch) + bf_epi_bytes(CONVERT, OB, g.yring));
     uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(red) +
                                                   (CS > 1 ? (size_t)128 * BN * 4 : 0));
     uint64_t *conv = full + S;       // CONVERT: A hi/lo written by the converter
@@ -446,9 +448,9 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     } else if (warp < 6) {  // --------------------------------- epilogue
         const int q = warp & 3;
         const int NR = bf_yring(CONVERT, g.yring), LA = NR / 2;  // ring depth, residual lookahead
-        float *scratch = epi_scratch + q * (g.out_bf16 ? 1024 : NR * 1024);
+        float *scratch = epi_scratch + q * (OB ? 1024 : NR * 1024);
         // fp32 output ring (tma_y): chunk counter of this warp -> buffer and residual parity
-        const bool ring = !g.out_bf16 && g.tma_y && (g.ldo & 3) == 0;
+        const bool ring = !OB && g.tma_y && (g.ldo & 3) == 0;
         const bool rres = ring && g.res && !TDC_DBG(g, 2);
         const uint32_t ring_s = smem_u32(scratch);
         uint32_t yc = 0;
@@ -498,7 +500,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                 for (int u = tid; u < nr * g8; u += 128) {
                     // bf16 planar output: consecutive threads take consecutive rows of one plane;
                     // fp32 row-major output: consecutive threads take consecutive columns of a row
-                    const int rl = g.out_bf16 ? u % nr : u / g8, c8 = g.out_bf16 ? u / nr : u % g8;
+                    const int rl = OB ? u % nr : u / g8, c8 = OB ? u / nr : u % g8;
                     const int rw = r0 + rl;
                     float v[8];
                     red_sum8(red_a, BN, CS, rw, c8, v);
@@ -506,7 +508,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                     const bool valid = remap_row(g, m0 + rw, &dst_row);
                     const int n = n0 + 8 * c8;
                     if (!valid || n >= g.Nn) continue;
-                    if (g.out_bf16) {
+                    if (OB) {
                         uint4 h, l;
                         split_bf16x8(v, h, l);
                         const long long off = ((long long)(n >> 3) * g.planar_stride + dst_row) * 8;
@@ -555,7 +557,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
                 for (int pp = 1; pp < GS; ++pp)  // partials in piece order (deterministic)
                     gs_add32(g.part + (size_t)(t * (GS - 1) + pp - 1) * 128 * BN, c, q * 32 + lane, v);
-                if (g.out_bf16) {  // X' hi/lo planar bf16: plane n/8 at (plane * stride + row) * 8
+                if (OB) {  // X' hi/lo planar bf16: plane n/8 at (plane * stride + row) * 8
                     if (valid) {
                         __nv_bfloat16 *hi = reinterpret_cast<__nv_bfloat16 *>(g.out);
                         __nv_bfloat16 *lo = reinterpret_cast<__nv_bfloat16 *>(g.out_lo);
@@ -743,13 +745,17 @@ cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, c
                                   g);
     };
     const int ks = g.ksplit > 1 ? 1 : (g.gsplit > 1 ? 2 : 0);
-    if (g.a_convert) {
-        const int th = 192 + kConvThreads16;
-        return ks == 1 ? go(tdc_bf_gemm_kernel<true, 1>, th)
-                       : (ks == 2 ? go(tdc_bf_gemm_kernel<true, 2>, th) : go(tdc_bf_gemm_kernel<true, 0>, th));
-    }
-    return ks == 1 ? go(tdc_bf_gemm_kernel<false, 1>, 192)
-                   : (ks == 2 ? go(tdc_bf_gemm_kernel<false, 2>, 192) : go(tdc_bf_gemm_kernel<false, 0>, 192));
+    const int th = 192 + kConvThreads16;
+    if (g.a_convert && g.out_bf16)  // stage 1
+        return ks == 1 ? go(tdc_bf_gemm_kernel<true, 1, true>, th)
+                       : (ks == 2 ? go(tdc_bf_gemm_kernel<true, 2, true>, th) : go(tdc_bf_gemm_kernel<true, 0, true>, th));
+    if (g.a_convert)  // model dense convolutions (fp32 out)
+        return ks == 1 ? go(tdc_bf_gemm_kernel<true, 1, false>, th)
+                       : (ks == 2 ? go(tdc_bf_gemm_kernel<true, 2, false>, th)
+                                  : go(tdc_bf_gemm_kernel<true, 0, false>, th));
+    return ks == 1 ? go(tdc_bf_gemm_kernel<false, 1, false>, 192)
+                   : (ks == 2 ? go(tdc_bf_gemm_kernel<false, 2, false>, 192)
+                              : go(tdc_bf_gemm_kernel<false, 0, false>, 192));
 }
 
 // ============================================================ core conv (stage 2)
