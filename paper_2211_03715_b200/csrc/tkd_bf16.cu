@@ -798,7 +798,9 @@ int bf_core3_tmem_cols(const BfCoreArgs &g) { return bf_core3_tmem(g); }
 // bf16 hi/lo by the epilogue-2 warps straight into shared memory, stage 3 multiplies
 // it with the resident U_out panel, epilogue-3 warps write Y (+bias).  Z never
 // touches HBM.  MMA issue is software-pipelined: S2(tile i) then S3(tile i-1).
-template <bool F3, int KS>  // KS: 0 plain, 1 cluster split-K, 2 split-K through L2 (stage 2 alone)
+// KS: 0 plain, 1 cluster split-K, 2 split-K through L2 (stage 2 alone); RES: the fused
+// stage-3 epilogue adds a residual (model path) -- compiled only where used.
+template <bool F3, int KS, bool RES>
 __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const BfCoreArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
@@ -1248,14 +1250,14 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
                 }
                 if (c >= g.N3 || TDC_DBG(g, 1)) continue;  // warp-uniform
-                if (g.res && c + 32 <= g.N3 && (g.N3 & 3) == 0) {  // coalesced residual block
+                if (RES && g.res && c + 32 <= g.N3 && (g.N3 & 3) == 0) {  // coalesced residual block
                     float rv[32];
                     warp_load_block32(scratch, rv, valid ? g.res + dst_row * g.N3 + c : nullptr, lane);
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] += rv[j];
                     epi_bias_res_relu<32>(v, c, g.N3, g.bias, nullptr, g.relu);
                 } else {
-                    epi_bias_res_relu<32>(v, c, g.N3, g.bias, (g.res && valid) ? g.res + dst_row * g.N3 : nullptr,
+                    epi_bias_res_relu<32>(v, c, g.N3, g.bias, (RES && g.res && valid) ? g.res + dst_row * g.N3 : nullptr,
                                           g.relu);
                 }
                 if (c + 32 <= g.N3 && (g.N3 & 3) == 0) {
@@ -1291,16 +1293,18 @@ cudaError_t bf_core_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         return launch_pdl_cluster(kernel, grid, 192, smem, st, g.ksplit, g);
     };
-    return g.ksplit > 1 ? go(tdc_bf_core_kernel<false, 1>)
-                        : (g.gsplit > 1 ? go(tdc_bf_core_kernel<false, 2>) : go(tdc_bf_core_kernel<false, 0>));
+    return g.ksplit > 1 ? go(tdc_bf_core_kernel<false, 1, false>)
+                        : (g.gsplit > 1 ? go(tdc_bf_core_kernel<false, 2, false>) : go(tdc_bf_core_kernel<false, 0, false>));
 }
 
 cudaError_t bf_core3_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
     const int smem = bf_core3_smem_bytes(g);
-    cudaError_t e =
-        cudaFuncSetAttribute(tdc_bf_core_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    return launch_pdl(tdc_bf_core_kernel<true, 0>, grid, 320, smem, st, g);
+    auto go = [&](auto kernel) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        return launch_pdl(kernel, grid, 320, smem, st, g);
+    };
+    return g.res ? go(tdc_bf_core_kernel<true, 0, true>) : go(tdc_bf_core_kernel<true, 0, false>);
 }
 
 }  // namespace tdc
