@@ -33,7 +33,9 @@ while i < len(ks):
         i += 1
 names = [s.name for s, c in synth.R18_SHAPES for _ in range(c)]
 steps = len(groups) // len(names)
-last = groups[-len(names):]  # the last (timed) step
+# the first bench step: bench.py times each layer alone after the steps, so the tail of
+# the list is the last layer repeated; ncu flushes caches per launch, so any step is as cold
+last = groups[:len(names)]
 per = {}
 for nm, g in zip(names, last):
     b = sum(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0) for k in g)
