@@ -48,7 +48,7 @@ WORKLOAD = "tucker_resnet18_3x3_tkd_layers"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["tdc", "reference"], default="tdc")
     ap.add_argument("--math", choices=["fp32", "tf32", "3xtf32", "3xbf16"], default="3xbf16",
