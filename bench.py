@@ -63,7 +63,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="issue the timed steps as individual launches instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=10.0)
+    ap.add_argument("--no-b1", action="store_true", help="skip the batch-1 latency section")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     return ap.parse_args()
 
 
@@ -208,7 +209,10 @@ def impl_tdc(args):
     stream = torch.cuda.Stream()
     layers = []
     for lid, s in insts:
-        d = synth.make_layer(s, seed=synth.BASE_SEED + 1000 * rank, layer_id=lid)
+        # identical weights on every rank (seed independent of the rank); the input is this
+        # rank's shard [rank*B, rank*B + B) of the layer's global batch (weak scaling)
+        d = synth.make_layer(s.with_batch(1), seed=synth.BASE_SEED, layer_id=lid)
+        d["x"] = synth.make_images(s, rank * s.B, s.B, seed=synth.BASE_SEED, layer_id=lid)
         plan = tdc.ConvPlan(s, d, layout=tdc.TDC_LAYOUT_NHWC, math=math, device=local)
         x = torch.from_numpy(synth.nchw_to_nhwc(d["x"])).cuda()
         y = torch.empty((s.B, s.Ho, s.Wo, s.N), device="cuda")
@@ -346,27 +350,90 @@ def impl_tdc(args):
                  "timing": "layer alone, back-to-back forwards between CUDA events on the launching stream, "
                            "inputs rotated over > 2x L2"})
 
+    # ---- batch-1 latency, the paper's regime (batch 1, averaged over 1000
+    # inferences): BASELINE config 1 and the 7 R18 shapes at B = 1.  Per forward: CUDA-graph
+    # replay and plain stream launches (device time between events, `reps` forwards back to
+    # back), and the host-observed latency of one call + stream synchronize (median).
+    def b1_latency(shape, mname, reps=50):
+        d1 = synth.make_layer(shape, seed=synth.BASE_SEED)
+        pl = tdc.ConvPlan(shape, d1, layout=tdc.TDC_LAYOUT_NHWC, math=tdc.MATH_NAMES[mname], device=local)
+        bx = torch.from_numpy(synth.nchw_to_nhwc(d1["x"])).cuda()
+        by = torch.empty((shape.B, shape.Ho, shape.Wo, shape.N), device="cuda")
+        with torch.cuda.stream(stream):
+            for _ in range(5):
+                pl.forward(bx, by, stream=stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            pl.forward(bx, by, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        plain = e0.elapsed_time(e1) * 1e3 / reps
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1, stream=stream):
+            for _ in range(reps):
+                pl.forward(bx, by, stream=stream)
+        with torch.cuda.stream(stream):
+            g1.replay()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(4):
+                g1.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        graph_us = e0.elapsed_time(e1) * 1e3 / (4 * reps)
+        lat = []
+        for _ in range(reps):
+            h0 = time.perf_counter()
+            pl.forward(bx, by, stream=stream)
+            stream.synchronize()
+            lat.append((time.perf_counter() - h0) * 1e6)
+        info = pl.info()
+        del g1
+        pl.close()
+        return {"layer": shape.name, "math": mname, "variant": info.variant_name,
+                "launches": info.launches_per_forward, "graph_us": round(graph_us, 2),
+                "launch_us": round(plain, 2), "host_sync_us": round(statistics.median(lat), 2),
+                "bytes": rl.tkd_bytes(shape), "flops": rl.tkd_flops(shape)}
+
+    batch1 = None
+    if not args.no_b1:
+        batch1 = [b1_latency(synth.CONFIG1, "fp32"), b1_latency(synth.CONFIG1, args.math)]
+        batch1 += [b1_latency(sh.with_batch(1), args.math) for sh, _ in synth.R18_SHAPES]
+
     # ---- whole-model inference (BASELINE metric part 2): Tucker ResNet-50 (config 3,
     # batch 32 per GPU, weak scaling) and Tucker VGG-16 (config 4, global batch 64
     # sharded over the ranks, strong scaling).  Each rank runs the whole model on its own
     # shard (no collective beyond the timing barrier); images/s = all ranks' images /
     # max-over-ranks time.
-    def time_model(ops, mb, steps=None):
+    def time_model(ops, global_batch, steps=None):
+        """Batch-sharded inference: identical weights on every rank, rank r
+        runs images [start, start + count) of the global batch, and the logits are
+        all-gathered (NCCL) into global-batch order on every rank -- the gather is inside
+        the timed region.  Returns (ms per global batch, launch mode)."""
         steps = steps or args.steps
+        sh = tdist.BatchShard(global_batch)
+        mb = max(1, sh.count)
         net = tdc.Model(ops, max_batch=mb, device=local)
         mh, mw, mc = net.output_shape()
         import synth.models as sm
-        mx = torch.from_numpy(sm.model_input(mb, 224, seed=synth.BASE_SEED + rank)).cuda()
+        mx = torch.from_numpy(sm.model_input(mb, 224, seed=synth.BASE_SEED, first=sh.start)).cuda()
         mo = torch.empty((mb, mh, mw, mc), device="cuda")
+
+        def fwd():
+            net.forward(mx, mo, stream=stream)
+
         with torch.cuda.stream(stream):
             for _ in range(max(args.warmup, 3)):
-                net.forward(mx, mo, stream=stream)
+                fwd()
         torch.cuda.synchronize()
         mgraph = None
         if not args.no_graph:
             mgraph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(mgraph, stream=stream):
-                net.forward(mx, mo, stream=stream)
+                fwd()
             torch.cuda.synchronize()
         m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tdist.barrier()
@@ -377,12 +444,17 @@ def impl_tdc(args):
                 if mgraph is not None:
                     mgraph.replay()
                 else:
-                    net.forward(mx, mo, stream=stream)
+                    fwd()
+                if world > 1:
+                    logits = sh.gather(mo.view(mb, -1))
         m1.record(stream)
         torch.cuda.synchronize()
         tdist.barrier()
         mms = tdist.max_over_ranks(m0.elapsed_time(m1), "cuda") / steps
         how = "cuda_graph_replay" if mgraph is not None else "stream_launches"
+        if world > 1:
+            how += " + all_gather(logits)"
+            assert logits.shape[0] == global_batch
         mgraph = None
         net.close()
         return mms, how
@@ -391,23 +463,22 @@ def impl_tdc(args):
     if not args.no_model:
         import synth.models as sm
         mb = args.model_batch
-        mms, how = time_model(sm.tucker_resnet(50, seed=synth.BASE_SEED + 1000 * rank), mb)
+        mms, how = time_model(sm.tucker_resnet(50, seed=synth.BASE_SEED), mb * world)
         model = {"tucker_resnet50": {
             "ranks": "paper-style r = 1/4 (D = C/4) on every 3x3 conv", "input": "224x224x3 synthetic, NHWC fp32",
             "math": "3xbf16 (fp32-grade)", "batch_per_gpu": mb, "global_batch": mb * world, "n_gpus": world,
             "scaling": "weak", "ms_per_batch": round(mms, 4), "images_per_s": round(mb * world / (mms * 1e-3), 1),
             "launch": how}}
-        vb = max(1, 64 // world)
-        vms, how = time_model(sm.tucker_vgg16(seed=synth.BASE_SEED + 1000 * rank), vb)
+        vms, how = time_model(sm.tucker_vgg16(seed=synth.BASE_SEED), 64)
         model["tucker_vgg16"] = {
             "ranks": "paper-style r = 3/8 on the 12 3x3 convs after the first", "input": "224x224x3 synthetic",
-            "math": "3xbf16 (fp32-grade)", "batch_per_gpu": vb, "global_batch": vb * world, "n_gpus": world,
-            "scaling": "strong (global batch 64 sharded)", "ms_per_batch": round(vms, 4),
-            "images_per_s": round(vb * world / (vms * 1e-3), 1), "launch": how}
+            "math": "3xbf16 (fp32-grade)", "batch_per_gpu": tdist.shard(64, world, rank)[1], "global_batch": 64,
+            "n_gpus": world, "scaling": "strong (global batch 64 sharded)", "ms_per_batch": round(vms, 4),
+            "images_per_s": round(64 / (vms * 1e-3), 1), "launch": how}
         if not args.no_model_sweep:  # BASELINE config 3: ResNet-50 at batch 1..256 per GPU
             sweep = {}
             for sb in (1, 8, 64, 128, 256):
-                sms, _ = time_model(sm.tucker_resnet(50, seed=synth.BASE_SEED + 1000 * rank), sb,
+                sms, _ = time_model(sm.tucker_resnet(50, seed=synth.BASE_SEED), sb * world,
                                     steps=max(3, min(args.steps, 10)))
                 sweep[str(sb)] = {"ms_per_batch": round(sms, 4), "images_per_s": round(sb * world / (sms * 1e-3), 1)}
             model["tucker_resnet50"]["batch_sweep_per_gpu"] = sweep
@@ -461,7 +532,7 @@ def impl_tdc(args):
                              "3xbf16": "hi*hi+hi*lo+lo*hi bf16 split, fp32 accumulate; fp32-grade, "
                                        "tolerance 1e-4"}[args.math],
                 "data": "synthetic", "config": config_dict(args, world),
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "model": model,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "model": model, "batch1": batch1,
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": sampler.summary(), "layers": layer_rows,
                 "step_bytes": step_bytes, "step_flops": sum(rl.tkd_flops(L["shape"]) for L in layers)}
@@ -471,8 +542,27 @@ def impl_tdc(args):
     tdist.finalize()
 
 
+def self_launch(args) -> bool:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-launch this script as N
+    ranks (one process per GPU) with torch.distributed.run on 127.0.0.1."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    self_launch(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     if args.impl == "reference":
         impl_reference(args)
     else:

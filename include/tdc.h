@@ -55,7 +55,10 @@ typedef enum {
     TDC_MATH_FP32 = 0,   /* fp32 FFMA on CUDA cores (the paper's precision); tol 1e-4 */
     TDC_MATH_3XTF32 = 1, /* tcgen05 TF32 with hi/lo split (3 products); tol 1e-4            */
     TDC_MATH_TF32 = 2,   /* tcgen05 TF32, one product; tol 1e-2 (north_star)                */
-    TDC_MATH_3XBF16 = 3  /* tcgen05 bf16 with hi/lo split (3 products); tol 1e-4            */
+    TDC_MATH_3XBF16 = 3  /* tcgen05 bf16 with hi/lo split (3 products, lo*lo dropped):
+                          * ~2^-16 relative per product -- NOT IEEE fp32 (about 40x the fp32
+                          * kernel's error on the same layer) but within the 1e-4
+                          * max-normalized tolerance; integer layers bit-exact             */
 } tdc_math;
 
 /* Layer descriptor.  All sizes > 0; 1 <= rank_in <= c_in and
@@ -107,7 +110,14 @@ typedef struct {
     int32_t bn_stage1, bn_core, bn_stage3; /* 0 auto                               */
     int32_t ksplit_stage1, ksplit_core, ksplit_stage3; /* 0 auto, 1 off, 2..4     */
     int32_t gsplit_stage1, gsplit_core, gsplit_stage3; /* split-K through L2:
-                                              0 auto, 1 off, 2..8 pieces (clamped to K chunks) */
+                                              0 auto, 1 off, 2..8 pieces (clamped to K chunks).
+                                              The piece-0 CTA of a tile spins until the other
+                                              pieces publish: the grid is capped at one CTA per
+                                              SM and REQUIRES every CTA to be co-resident, so do
+                                              not combine with MPS SM limits, green contexts or
+                                              a concurrent persistent kernel on the same GPU.
+                                              The model path enables it for long-K classifier
+                                              GEMMs; set TDC_DENSE_NO_GSPLIT=1 to disable it there. */
 } tdc_plan_hints;
 
 const char *tdc_version(void);

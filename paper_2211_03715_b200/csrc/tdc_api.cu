@@ -211,8 +211,8 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
     const int band_rows = round_up(128 + maxoff, 8);
     int phase_of[tdc::kMaxTaps], nphase = 0, phase_src[tdc::kMaxTaps];
     {
-        int idx_of[tdc::kMaxTaps];
-        for (int i = 0; i < tdc::kMaxTaps; ++i) idx_of[i] = -1;
+        // phase id (r % s) * s + (t % s) ranges over s*s values, not K*K
+        std::vector<int> idx_of((size_t)s * s, -1);
         for (int r = 0; r < K; ++r)
             for (int t = 0; t < K; ++t) {
                 const int ph = (r % s) * s + (t % s);
@@ -521,8 +521,8 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
     const int band_rows = round_up(128 + maxoff, 8);
     int phase_of[tdc::kMaxTaps], nphase = 0, phase_src[tdc::kMaxTaps];
     {
-        int idx_of[tdc::kMaxTaps];
-        for (int i = 0; i < tdc::kMaxTaps; ++i) idx_of[i] = -1;
+        // phase id (r % s) * s + (t % s) ranges over s*s values, not K*K
+        std::vector<int> idx_of((size_t)s * s, -1);
         for (int r = 0; r < K; ++r)
             for (int t = 0; t < K; ++t) {
                 const int ph = (r % s) * s + (t % s);
@@ -1412,7 +1412,16 @@ tdc_status tdc_conv_forward_ex(tdc_conv_plan_t p, const float *x, float *y, int3
         return fail(TDC_ERR_UNSUPPORTED,
                     "residual/relu epilogue needs an NHWC plan in TDC_MATH_3XBF16 (this plan: variant %d)",
                     p->variant);
-    if (residual == y) return fail(TDC_ERR_INVALID_ARGUMENT, "residual must not alias y");
+    {   // x / residual must not overlap y (ranges, not just equal pointers)
+        const tdc::LayerDims &d = p->dims;
+        const char *y0 = (const char *)y, *y1 = (const char *)(y + (size_t)batch * d.N * d.Ho * d.Wo);
+        const char *x0 = (const char *)x, *x1 = (const char *)(x + (size_t)batch * d.C * d.H * d.W);
+        if (x0 < y1 && y0 < x1) return fail(TDC_ERR_INVALID_ARGUMENT, "x and y must not alias");
+        if (residual) {
+            const char *r0 = (const char *)residual, *r1 = (const char *)(residual + (size_t)batch * d.N * d.Ho * d.Wo);
+            if (r0 < y1 && y0 < r1) return fail(TDC_ERR_INVALID_ARGUMENT, "residual must not overlap y");
+        }
+    }
     DeviceGuard guard(p->device);
     if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
     return forward_bf16(p, x, y, batch, (cudaStream_t)stream, residual, relu);
@@ -1500,10 +1509,12 @@ tdc_status host_finish(tdc_conv_plan_t p, cudaStream_t st) {
 
 tdc_status tdc_conv_forward_host(tdc_conv_plan_t p, const float *x_host, float *y_host,
                                  int32_t batch, void *stream) {
-    tdc_status s = host_prepare(p, x_host, y_host, batch);
-    if (s != TDC_OK) return s;
+    if (!p) return fail(TDC_ERR_INVALID_ARGUMENT, "plan is NULL");
+    // staging buffers, copy streams and events are created on the plan's device
     DeviceGuard guard(p->device);
     if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+    tdc_status s = host_prepare(p, x_host, y_host, batch);
+    if (s != TDC_OK) return s;
     cudaStream_t st = (cudaStream_t)stream;
     if ((s = host_begin(p, st)) != TDC_OK) return s;
     int evi = 0;
@@ -1515,9 +1526,8 @@ tdc_status tdc_conv_forward_host_many(const tdc_conv_plan_t *plans, const float 
                                       float *const *y_hosts, const int32_t *batches, int32_t n, void *stream) {
     if (!plans || !x_hosts || !y_hosts || !batches || n < 1)
         return fail(TDC_ERR_INVALID_ARGUMENT, "plans/x_hosts/y_hosts/batches NULL or n < 1");
-    for (int i = 0; i < n; ++i) {
-        const tdc_status s = host_prepare(plans[i], x_hosts[i], y_hosts[i], batches[i]);
-        if (s != TDC_OK) return s;
+    for (int i = 0; i < n; ++i) {  // one device for all plans, checked before any allocation
+        if (!plans[i]) return fail(TDC_ERR_INVALID_ARGUMENT, "plan %d is NULL", i);
         if (plans[i]->device != plans[0]->device)
             return fail(TDC_ERR_INVALID_ARGUMENT, "plan %d is on device %d, plan 0 on %d", i, plans[i]->device,
                         plans[0]->device);
@@ -1525,6 +1535,10 @@ tdc_status tdc_conv_forward_host_many(const tdc_conv_plan_t *plans, const float 
     tdc_conv_plan_t p0 = plans[0];
     DeviceGuard guard(p0->device);
     if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+    for (int i = 0; i < n; ++i) {
+        const tdc_status s = host_prepare(plans[i], x_hosts[i], y_hosts[i], batches[i]);
+        if (s != TDC_OK) return s;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     tdc_status s = host_begin(p0, st);
     if (s != TDC_OK) return s;

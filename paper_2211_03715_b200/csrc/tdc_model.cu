@@ -301,7 +301,7 @@ struct DenseOp {
     tdc::TcGemmArgs args;
     CUtensorMap mapA, mapB, mapBlo;
     const float *mapA_src = nullptr;
-    long long mapA_rows = 0;
+    long long mapA_rows = 0;  // the A map's row extent = this call's rows (loads past it zero-fill)
     CUtensorMap mapY;        // TMA map of the output (tma_y), re-encoded when dst changes
     const float *mapY_dst = nullptr;
     long long mapY_rows = 0;  // the map's row extent = this call's rows (TMA stores clip there)
@@ -523,11 +523,13 @@ tdc_status run_dense(tdc_model_s *m, ModelOp &op, const float *src, float *dst, 
         if (e != cudaSuccess) return mcuda(e, "im2col launch");
         A = m->scratch;
     }
-    const long long rows = (long long)m->max_batch * op.Ho * op.Wo;
-    if (A != g.mapA_src) {
-        if (!tdc::make_tma_2d(&g.mapA, A, rows, g.Kdim, g.Kdim, 128))
+    // extent = this call's rows, so the last M tile of a partial batch is zero-filled instead
+    // of reading past a caller's input sized for `batch`
+    if (A != g.mapA_src || M != g.mapA_rows) {
+        if (!tdc::make_tma_2d(&g.mapA, A, M, g.Kdim, g.Kdim, 128))
             return mfail(TDC_ERR_INVALID_ARGUMENT, "cuTensorMapEncodeTiled rejected a dense-op input (16-byte aligned?)");
         g.mapA_src = A;
+        g.mapA_rows = M;
     }
     tdc::TcGemmArgs a = g.args;
     a.M = (int)M;

@@ -115,6 +115,20 @@ def make_layer(shape: LayerShape, seed: int = BASE_SEED, layer_id: int = 0,
             "bias": b}
 
 
+def make_images(shape: LayerShape, first: int, count: int, seed: int = BASE_SEED,
+                layer_id: int = 0) -> np.ndarray:
+    """Images [first, first + count) of a layer's global input batch, NCHW fp32
+    ~ U[-1, 1): every image has its own counter-based stream (seed, layer, image), so a
+    rank's shard of the global batch is the same data whatever the number of ranks
+    (multi-GPU runs shard the batch)."""
+    s = shape
+    out = np.empty((count, s.C, s.H, s.W), np.float32)
+    for i in range(count):
+        g = np.random.Generator(np.random.PCG64([seed, layer_id, 0x1A6E, first + i]))
+        out[i] = g.uniform(-1.0, 1.0, (s.C, s.H, s.W)).astype(np.float32)
+    return out
+
+
 def nchw_to_nhwc(a: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(np.transpose(a, (0, 2, 3, 1)))
 

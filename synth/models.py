@@ -142,7 +142,12 @@ def tucker_vgg16(image: int = 224, num_classes: int = 1000, ratio: float = 3 / 8
     return b.ops
 
 
-def model_input(batch: int, image: int = 224, seed: int = 42) -> np.ndarray:
-    """Synthetic ImageNet-shaped input, NHWC fp32 ~ N(0, 1) (normalised pixels)."""
-    return np.random.Generator(np.random.PCG64(seed + 999_999)).standard_normal(
-        (batch, image, image, 3)).astype(np.float32)
+def model_input(batch: int, image: int = 224, seed: int = 42, first: int = 0) -> np.ndarray:
+    """Synthetic ImageNet-shaped input, NHWC fp32 ~ N(0, 1) (normalised pixels):
+    images [first, first + batch) of the global batch, one seeded stream per image so
+    a rank's shard equals the same slice of the unsharded batch."""
+    out = np.empty((batch, image, image, 3), np.float32)
+    for i in range(batch):
+        g = np.random.Generator(np.random.PCG64([seed, 999_999, first + i]))
+        out[i] = g.standard_normal((image, image, 3)).astype(np.float32)
+    return out

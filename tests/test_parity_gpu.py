@@ -90,11 +90,21 @@ def test_integer_layer_is_bit_exact(env, layout, math):
     LayerShape(1, 5, 3, 3, 3, 2, 2, 3, 1, 1),         # smaller than a tile
     LayerShape(1, 64, 64, 1, 1, 16, 16, 3, 1, 1),     # 1x1 image, all padding
     LayerShape(2, 64, 96, 20, 17, 64, 96, 3, 1, 1),   # full ranks
+    LayerShape(1, 8, 8, 30, 30, 4, 4, 3, 24, 1),      # stride 24 > K*K phases
+    LayerShape(1, 8, 8, 20, 20, 4, 4, 7, 8, 3),       # 7x7 core, stride 8
 ])
 @pytest.mark.parametrize("math", MATHS)
 def test_ragged_and_edge_shapes(env, shape, math):
     d = synth.make_layer(shape, seed=7, bias=True)
-    got, _ = run_layer(env, shape, d, "nhwc", math)
+    got, info = run_layer(env, shape, d, "nhwc", math)
+    # the variant that ran is asserted, so no case silently exercises another kernel:
+    # TMA needs 16-byte pixel rows (C % 4 == 0); otherwise every mode uses the FP32 kernel
+    if math == "fp32" or shape.C % 4:
+        assert info.variant_name == "fused_simt_fp32", info.variant_name
+    elif math == "3xbf16":
+        assert "3xbf16" in info.variant_name, info.variant_name
+    else:
+        assert info.variant_name != "fused_simt_fp32", info.variant_name
     assert err(got, ref_of(shape, d)) <= TOL[math]
 
 
@@ -209,6 +219,7 @@ def test_3xbf16_core3_and_three_launch(env, shape, fuse3, monkeypatch):
     s = shape.with_batch(2)
     d = synth.make_layer(s, seed=21, bias=True)
     got, info = run_layer(env, s, d, "nhwc", "3xbf16")
+    assert "3xbf16" in info.variant_name, info.variant_name
     if not fuse3:
         assert info.variant_name == "tc3_3xbf16_band"
     assert err(got, ref_of(s, d)) <= TOL["3xbf16"]
@@ -251,7 +262,8 @@ def test_3xbf16_wide_rank_large_m(env, shape):
     shared memory (a Tucker VGG-16 28x28x512 layer at batch 64 hit this).  Sampled
     outputs against the oracle evaluated point by point."""
     d = synth.make_layer(shape, seed=9)
-    got, _ = run_layer(env, shape, d, "nhwc", "3xbf16")
+    got, info = run_layer(env, shape, d, "nhwc", "3xbf16")
+    assert "3xbf16" in info.variant_name, info.variant_name
     pts = synth.sample_points(shape, 200, seed=1)
     ref = oracle.tkd_points(d["x"], d["core"], d["u_in"], d["u_out"], pts, None, shape.stride, shape.pad)
     vals = np.array([got[p] for p in pts], dtype=np.float64)
