@@ -118,6 +118,11 @@ typedef struct {
                                               a concurrent persistent kernel on the same GPU.
                                               The model path enables it for long-K classifier
                                               GEMMs; set TDC_DENSE_NO_GSPLIT=1 to disable it there. */
+    int32_t fused_layer;                   /* TDC_MATH_3XBF16: the single-launch layer kernel
+                                              (stage 1 + core + stage 3, X' and Z on chip):
+                                              -1 auto (when it fits and no other field asks
+                                              for the three-launch kernels), 0 never, 1 when
+                                              it fits                                      */
 } tdc_plan_hints;
 
 const char *tdc_version(void);

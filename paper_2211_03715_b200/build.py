@@ -31,17 +31,21 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, timeline: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, timeline: bool = False, knobs: bool = False) -> str:
     """timeline=True builds the debug variant libtdc_tl.so (-DTDC_TIMELINE: per-tile
-    %globaltimer events of CTA 0, read by scripts/*timeline.py via TDC_LIB)."""
-    lib = LIB.replace("libtdc.so", "libtdc_tl.so") if timeline else LIB
-    if not force and not timeline and up_to_date():
+    %globaltimer events of CTA 0, read by scripts/*timeline.py via TDC_LIB); knobs=True
+    builds libtdc_kn.so (-DTDC_DEBUG_KNOBS: the TDC_*_DBG attribution switches, no stamps)."""
+    lib = LIB.replace("libtdc.so", "libtdc_tl.so") if timeline else (LIB.replace("libtdc.so", "libtdc_kn.so")
+                                                                    if knobs else LIB)
+    if not force and not timeline and not knobs and up_to_date():
         return LIB
     tmp = lib + f".{os.getpid()}.tmp"
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
            "-shared", "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources()]
     if timeline:
         cmd.insert(1, "-DTDC_TIMELINE")
+    if knobs:
+        cmd.insert(1, "-DTDC_DEBUG_KNOBS")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
@@ -51,4 +55,5 @@ def build(force: bool = False, verbose: bool = False, timeline: bool = False) ->
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, timeline="--timeline" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, timeline="--timeline" in sys.argv,
+                knobs="--knobs" in sys.argv))

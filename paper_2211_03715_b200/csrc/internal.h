@@ -175,6 +175,35 @@ cudaError_t bf_core_launch(const BfCoreArgs &g, int grid, cudaStream_t st);
 bool make_tma_2d_bf16(CUtensorMap *map, const void *base, long long rows, int k_extent, int pitch,
                       int box_rows);
 
+// Single-launch 3xBF16 TKD layer (tkd_layer.cu): stage 1 -> X' band ring in shared
+// memory -> core -> Z in shared memory -> stage 3, one persistent kernel.  Stride 1.
+struct BfLayerArgs {
+    int B, H, W, C, N, K, KK, s, p, Ho, Wo, Wp, Wq, Hq;
+    int R, e, T;              // output rows per tile (R*Wq <= 128), (K-1)/s, tiles per image
+    int rpb;                  // padded input rows per stage-1 block (rpb*Wp <= 128)
+    int NR, NRB;              // band ring rows (2R+e) and buffer rows incl. the mirror rows
+    int XR, ZR;               // rows of an X staging tile / a Z plane (multiples of 8, <= 128)
+    int cchunks;              // 64-channel chunks of C (TMA zero-fills channels >= C)
+    int D1s, D2s, N3p;        // ranks / output channels padded to multiples of 32
+    int XS;                   // X staging ring depth (<= 4)
+    int pf_blocks;            // stage-1 blocks the producer's L2 prefetch runs ahead of its loads
+    int num_tiles;            // batch * T for this call
+    int tmem_cols;
+    int tap_off[kMaxTaps];    // r*Wq + t
+    const uint16_t *w1;       // U_in per 64-channel chunk: [2*D1s rows: hi | lo][64] bf16, 128B-swizzled image
+    const uint16_t *w2;       // core [D1s/32][tap][plane 4][2*D2s rows: hi | lo][8]
+    const uint16_t *w3;       // U_out [D2s/8][2*N3p rows: hi | lo][8]
+    const float *bias;        // [N] or null
+    const float *res;         // residual [B*Ho*Wo][N] or null (model path)
+    int relu;
+    float *y;                 // [B*Ho*Wo][N]
+    uint8_t *dbg;             // debug: CTA 0 copies its shared memory here at exit (null = off)
+    int knobs;                // debug builds only (TDC_LAYER_DBG): 1 no Y stores, 2 no X conversion,
+                              // 4 no band writes, 8 no Z writes, 16/32/64 no S2/S1/S3 MMAs,
+                              // 128 no X loads after the first tiles (results wrong by design)
+};
+int bf_layer_smem_bytes(const BfLayerArgs &g);
+cudaError_t bf_layer_launch(const CUtensorMap &mapX, const BfLayerArgs &g, int grid, cudaStream_t st);
 // NCHW <-> NHWC for the NCHW API layout.
 cudaError_t nchw_to_nhwc(const float *src, float *dst, int B, int C, int H, int W,
                          cudaStream_t st);

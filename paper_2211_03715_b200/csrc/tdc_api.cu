@@ -128,7 +128,7 @@ struct tdc_conv_plan_s {
     tdc::TcCoreArgs core_args;
     tdc::BfCoreArgs bf_core;
     bool fuse3 = false;            // 3xBF16: core + stage 3 in one kernel (Z on chip)
-    tdc_plan_hints hints = {-1, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // planner overrides (tdc_conv_plan_ex)
+    tdc_plan_hints hints = {-1, 0, 0, 0, 0, 0, 0, 0, 0, 0, -1};  // planner overrides (tdc_conv_plan_ex)
     CUtensorMap mapY3;             // 3xBF16 stage 3: TMA map of the output (per y pointer)
     const float *last_y3 = nullptr;
     long long last_y3_rows = 0;
@@ -143,6 +143,11 @@ struct tdc_conv_plan_s {
     const float *tc_last_x = nullptr;
     int tc_last_x_batch = 0;
     int max_smem = 0;
+    // single-launch 3xBF16 layer (variant 5, tkd_layer.cu)
+    tdc::BfLayerArgs bl;
+    CUtensorMap lmapX;
+    const float *l_last_x = nullptr;
+    int l_last_batch = 0;
 };
 
 namespace {
@@ -849,6 +854,162 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
     return TDC_OK;
 }
 
+// Plan the single-launch 3xBF16 layer kernel (variant 5): stage 1, the core and stage 3
+// in one persistent kernel with X' and Z on chip.  Used when the
+// layer has stride 1, its ranks / output channels fit one tile (<= 128, hi|lo
+// concatenated in one MMA), all weights stay resident in shared memory next to the
+// band ring and X staging, and the accumulators fit TMEM; *used = false otherwise.
+tdc_status plan_layer(tdc_conv_plan_s *p, const float *core, const float *u_in, const float *u_out,
+                      const float *bias, bool *used) {
+    *used = false;
+    const tdc_conv_desc &d = p->desc;
+    const int C = d.c_in, N = d.c_out, D1 = d.rank_in, D2 = d.rank_out, K = d.kernel;
+    const int s = d.stride, pad = d.pad, H = d.height, W = d.width;
+    {
+        const char *ev = std::getenv("TDC_NO_LAYER"), *ev3 = std::getenv("TDC_NO_FUSE3");
+        const tdc_plan_hints &h = p->hints;
+        if ((ev && ev[0] && ev[0] != '0') || (ev3 && ev3[0] && ev3[0] != '0') || h.fused_layer == 0) return TDC_OK;
+        // auto: an explicit choice for the three-launch kernels (tile, split or fusion
+        // override) asks for those kernels
+        const bool other = h.core3 == 0 || h.bn_stage1 > 0 || h.bn_core > 0 || h.bn_stage3 > 0 ||
+                           h.ksplit_stage1 > 0 || h.ksplit_core > 0 || h.ksplit_stage3 > 0 || h.gsplit_stage1 > 0 ||
+                           h.gsplit_core > 0 || h.gsplit_stage3 > 0;
+        if (h.fused_layer < 0 && other) return TDC_OK;
+    }
+    if (s != 1 || C % 4 || K * K > tdc::kMaxTaps) return TDC_OK;
+    const int Wp = W + 2 * pad, Hp = H + 2 * pad;
+    const int D1s = round_up(D1, 32), D2s = round_up(D2, 32), N3p = round_up(N, 32);
+    if (D1s > 128 || D2s > 128 || N3p > 128 || Wp > 128 || Wp > 256) return TDC_OK;
+    tdc::BfLayerArgs g;
+    std::memset(&g, 0, sizeof g);
+    g.B = d.batch; g.H = H; g.W = W; g.C = C; g.N = N; g.K = K; g.KK = K * K; g.s = s; g.p = pad;
+    g.Ho = p->dims.Ho; g.Wo = p->dims.Wo; g.Wp = Wp; g.Wq = Wp; g.Hq = Hp;
+    g.R = std::min(128 / Wp, g.Ho);
+    g.e = K - 1;
+    if (g.R < 1) return TDC_OK;
+    g.T = div_up(g.Ho, g.R);
+    g.rpb = g.R;
+    g.NR = 2 * g.R + g.e;
+    {   // windows start at multiples of gcd(R, NR) below NR; the last one (+ its guard row)
+        // must be contiguous: NRB = max start + R + e + 1, mirror rows = NRB - NR
+        int a = g.R, b = g.NR;
+        while (b) { const int t = a % b; a = b; b = t; }
+        g.NRB = g.NR - a + g.R + g.e + 1;
+    }
+    g.XR = round_up(g.R * Wp, 8);   // rpb = R: one block = R padded rows
+    g.ZR = round_up(g.R * g.Wq, 8);
+    if (g.XR > 128 || g.ZR > 128) return TDC_OK;
+    g.cchunks = div_up(C, 64);
+    g.D1s = D1s; g.D2s = D2s; g.N3p = N3p;
+    const int tcols = 4 * D1s + 4 * D2s + 4 * N3p;
+    if (tcols > 512) return TDC_OK;
+    g.tmem_cols = 32;
+    while (g.tmem_cols < tcols) g.tmem_cols *= 2;
+    g.XS = 0;
+    const char *xs_env = std::getenv("TDC_LAYER_XS");  // A/B knob: maximum X staging depth
+    for (int xs = xs_env ? std::max(2, std::min(4, std::atoi(xs_env))) : 4; xs >= 2 && !g.XS; --xs) {
+        g.XS = xs;
+        if (tdc::bf_layer_smem_bytes(g) > p->max_smem) g.XS = 0;
+    }
+    if (!g.XS) return TDC_OK;
+    for (int r = 0; r < K; ++r)
+        for (int t = 0; t < K; ++t) g.tap_off[r * K + t] = r * g.Wq + t;
+
+    // ---- a0: bf16 hi/lo operand images (CRSN idea) ----
+    const int KK = K * K, C64 = g.cchunks * 64;
+    const size_t n1 = (size_t)g.cchunks * 2 * D1s * 64;           // U_in, swizzled per chunk
+    const size_t n2 = (size_t)(D1s / 32) * KK * 4 * 2 * D2s * 8;   // core
+    const size_t n3 = (size_t)(D2s / 8) * 2 * N3p * 8;             // U_out
+    std::vector<uint16_t> hb(n1 + n2 + n3, 0);
+    auto split = [](float v, uint16_t *hi, uint16_t *lo) {
+        *hi = bf16_bits_host(v);
+        *lo = bf16_bits_host(v - bf16_to_float_host(*hi));
+    };
+    uint16_t *w1 = hb.data(), *w2 = w1 + n1, *w3 = w2 + n2;
+    for (int cc = 0; cc < g.cchunks; ++cc)      // [cc][row: hi a | lo D1s + a][64 ch], 128B swizzle
+        for (int a = 0; a < D1; ++a)
+            for (int k = 0; k < 64; ++k) {
+                const int c = cc * 64 + k;
+                if (c >= C) continue;
+                uint16_t hi, lo;
+                split(u_in[(size_t)c * D1 + a], &hi, &lo);
+                for (int hl = 0; hl < 2; ++hl) {
+                    const int row = hl * D1s + a;
+                    const size_t at = ((size_t)cc * 2 * D1s + row) * 64 + (size_t)(((k / 8) ^ (row & 7)) * 8 + k % 8);
+                    w1[at] = hl ? lo : hi;
+                }
+            }
+    for (int r = 0; r < K; ++r)                 // [kc][tap][plane][row: hi q | lo D2s + q][8]
+        for (int t = 0; t < K; ++t)
+            for (int q = 0; q < D2; ++q)
+                for (int a = 0; a < D1; ++a) {
+                    uint16_t hi, lo;
+                    split(core[(((size_t)q * D1 + a) * K + r) * K + t], &hi, &lo);
+                    const int tap = r * K + t, kc = a / 32, pl = (a % 32) / 8, e8 = a % 8;
+                    const size_t base = (((size_t)kc * KK + tap) * 4 + pl) * 2 * D2s;
+                    w2[(base + q) * 8 + e8] = hi;
+                    w2[(base + D2s + q) * 8 + e8] = lo;
+                }
+    for (int n = 0; n < N; ++n)                 // [plane q/8][row: hi n | lo N3p + n][8]
+        for (int q = 0; q < D2; ++q) {
+            uint16_t hi, lo;
+            split(u_out[(size_t)n * D2 + q], &hi, &lo);
+            const size_t row = (size_t)(q / 8) * 2 * N3p;
+            w3[(row + n) * 8 + q % 8] = hi;
+            w3[(row + N3p + n) * 8 + q % 8] = lo;
+        }
+    (void)C64;
+    const size_t wbytes = hb.size() * sizeof(uint16_t), nbias = round_up(N, 4);
+    cudaError_t e = cudaMalloc(&p->d_tc_w, wbytes + nbias * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(layer weights)");
+    e = cudaMemcpy(p->d_tc_w, hb.data(), wbytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && bias) {
+        std::vector<float> bb(nbias, 0.f);
+        for (int n = 0; n < N; ++n) bb[n] = bias[n];
+        e = cudaMemcpy(reinterpret_cast<uint8_t *>(p->d_tc_w) + wbytes, bb.data(), nbias * sizeof(float),
+                       cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(layer weights)");
+    p->weight_bytes += wbytes + nbias * sizeof(float);
+    const uint16_t *wb = reinterpret_cast<const uint16_t *>(p->d_tc_w);
+    g.w1 = wb;
+    g.w2 = wb + n1;
+    g.w3 = wb + n1 + n2;
+    g.bias = bias ? reinterpret_cast<const float *>(reinterpret_cast<uint8_t *>(p->d_tc_w) + wbytes) : nullptr;
+    {
+        const char *kn = std::getenv("TDC_LAYER_DBG");  // honoured by the debug builds only
+        g.knobs = kn ? std::atoi(kn) : 0;
+        const char *pf = std::getenv("TDC_LAYER_PF");   // L2 prefetch distance (blocks), A/B knob
+        g.pf_blocks = pf ? std::atoi(pf) : 4;
+    }
+    p->bl = g;
+    p->l_last_x = nullptr;
+    p->variant = 5;
+    *used = true;
+    return TDC_OK;
+}
+
+tdc_status forward_layer(tdc_conv_plan_s *p, const float *x, float *y, int batch, cudaStream_t st,
+                         const float *res = nullptr, int relu = 0) {
+    tdc::BfLayerArgs g = p->bl;
+    if (x != p->l_last_x || batch != p->l_last_batch) {
+        // box {32 ch, Wp, rpb rows}: the padding columns/rows are out of bounds -> zeros
+        if (!tdc::make_tma_4d_nhwc(&p->lmapX, x, g.C, g.W, g.H, batch, g.Wp, g.rpb))
+            return fail(TDC_ERR_INVALID_ARGUMENT, "cuTensorMapEncodeTiled rejected x (needs 16-byte aligned pointer)");
+        p->l_last_x = x;
+        p->l_last_batch = batch;
+    }
+    g.B = batch;
+    g.num_tiles = batch * g.T;
+    g.y = y;
+    g.res = res;
+    g.relu = relu;
+    const int grid = std::max(1, std::min(g.num_tiles, p->num_sms));
+    cudaError_t e = tdc::bf_layer_launch(p->lmapX, g, grid, st);
+    if (e != cudaSuccess) return cuda_fail(e, "3xBF16 single-launch layer kernel");
+    return TDC_OK;
+}
+
 tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch, cudaStream_t st,
                         const float *res = nullptr, int relu = 0) {
     const tdc::LayerDims &d = p->dims;
@@ -1269,6 +1430,13 @@ tdc_status tdc_conv_plan_ex(const tdc_conv_desc *desc, const float *core, const 
     }
     bool bf = false;
     if (d.math == TDC_MATH_3XBF16) {
+        s = plan_layer(p, core, u_in, u_out, bias, &bf);
+        if (s != TDC_OK) {
+            tdc_conv_plan_destroy(p);
+            return s;
+        }
+    }
+    if (d.math == TDC_MATH_3XBF16 && !bf) {
         s = plan_bf16(p, core, u_in, u_out, bias, &bf);
         if (s != TDC_OK) {
             tdc_conv_plan_destroy(p);
@@ -1306,6 +1474,7 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
     info->variant = p->variant;
     const bool tc = p->variant == 2 || p->variant == 4, fz = p->variant == 3;
     std::snprintf(info->variant_name, sizeof info->variant_name, "%s",
+                  p->variant == 5 ? "layer_3xbf16_fused" :
                   p->variant == 4 ? (p->fuse3 ? "tc2_3xbf16_core3" : "tc3_3xbf16_band") : fz ? "fused_tc_tf32"
                      : tc ? (p->split ? (p->tc_core ? "tc3_3xtf32_band" : "tc3_3xtf32")
                                       : (p->tc_core ? "tc3_tf32_band" : "tc3_tf32"))
@@ -1352,6 +1521,21 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
         info->ctas_per_image = p->fargs.tiles_per_img;  // tiles per image (persistent grid)
         info->concurrent_forward = p->desc.layout == TDC_LAYOUT_NHWC ? 1 : 0;
     }
+    if (p->variant == 5) {
+        const tdc::BfLayerArgs &g = p->bl;
+        info->launches_per_forward = 1 + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
+        info->tile_h = g.R;
+        info->tile_w = g.Wo;
+        info->threads_per_cta = 608;
+        info->smem_bytes_per_cta = tdc::bf_layer_smem_bytes(g);
+        info->ctas_per_image = g.T;  // tiles per image (persistent grid)
+        info->bn_stage1 = g.D1s;
+        info->bn_core = g.D2s;
+        info->bn_stage3 = g.N3p;
+        info->ksplit_stage1 = info->ksplit_core = info->ksplit_stage3 = 1;
+        info->gsplit_stage1 = info->gsplit_core = info->gsplit_stage3 = 1;
+        info->core3 = 1;
+    }
     info->weight_bytes = (int64_t)p->weight_bytes;
     return TDC_OK;
 }
@@ -1374,6 +1558,7 @@ tdc_status tdc_conv_forward(tdc_conv_plan_t p, const float *x, float *y, int32_t
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
     if (p->desc.layout == TDC_LAYOUT_NHWC) {
+        if (p->variant == 5) return forward_layer(p, x, y, batch, st);
         if (p->variant == 4) return forward_bf16(p, x, y, batch, st);
         if (p->variant == 3) return forward_fused(p, x, y, batch, st);
         if (p->variant == 2) return forward_tc(p, x, y, batch, st);
@@ -1383,7 +1568,10 @@ tdc_status tdc_conv_forward(tdc_conv_plan_t p, const float *x, float *y, int32_t
     }
     e = tdc::nchw_to_nhwc(x, p->d_ws_in, batch, d.C, d.H, d.W, st);
     if (e != cudaSuccess) return cuda_fail(e, "NCHW->NHWC launch");
-    if (p->variant == 4) {
+    if (p->variant == 5) {
+        tdc_status s = forward_layer(p, p->d_ws_in, p->d_ws_out, batch, st);
+        if (s != TDC_OK) return s;
+    } else if (p->variant == 4) {
         tdc_status s = forward_bf16(p, p->d_ws_in, p->d_ws_out, batch, st);
         if (s != TDC_OK) return s;
     } else if (p->variant == 3) {
@@ -1408,7 +1596,7 @@ tdc_status tdc_conv_forward_ex(tdc_conv_plan_t p, const float *x, float *y, int3
     if (!x || !y) return fail(TDC_ERR_INVALID_ARGUMENT, "x/y is NULL");
     if (batch < 1 || batch > p->desc.batch)
         return fail(TDC_ERR_INVALID_ARGUMENT, "batch %d outside [1, %d] of this plan", batch, p->desc.batch);
-    if (p->variant != 4 || p->desc.layout != TDC_LAYOUT_NHWC)
+    if ((p->variant != 4 && p->variant != 5) || p->desc.layout != TDC_LAYOUT_NHWC)
         return fail(TDC_ERR_UNSUPPORTED,
                     "residual/relu epilogue needs an NHWC plan in TDC_MATH_3XBF16 (this plan: variant %d)",
                     p->variant);
@@ -1424,6 +1612,7 @@ tdc_status tdc_conv_forward_ex(tdc_conv_plan_t p, const float *x, float *y, int3
     }
     DeviceGuard guard(p->device);
     if (guard.err != cudaSuccess) return cuda_fail(guard.err, "cudaSetDevice");
+    if (p->variant == 5) return forward_layer(p, x, y, batch, (cudaStream_t)stream, residual, relu);
     return forward_bf16(p, x, y, batch, (cudaStream_t)stream, residual, relu);
 }
 
@@ -1548,6 +1737,27 @@ tdc_status tdc_conv_forward_host_many(const tdc_conv_plan_t *plans, const float 
                               &evi)) != TDC_OK)
             return s;
     return host_finish(p0, st);
+}
+
+// Debug only (not in tdc.h): run the single-launch layer kernel with CTA 0's shared
+// memory copied to dbg_dev (device, >= smem bytes) at exit.  Returns the layout offsets
+// (xs, w1, w2, w3, band, z) in off[6].
+tdc_status tdc_debug_layer_forward(tdc_conv_plan_t p, const float *x, float *y, int32_t batch, void *dbg_dev,
+                                   int32_t *off) {
+    if (!p || p->variant != 5) return fail(TDC_ERR_INVALID_ARGUMENT, "not a single-launch layer plan");
+    DeviceGuard guard(p->device);
+    p->bl.dbg = reinterpret_cast<uint8_t *>(dbg_dev);
+    const tdc_status s = forward_layer(p, x, y, batch, nullptr);
+    p->bl.dbg = nullptr;
+    const tdc::BfLayerArgs &g = p->bl;
+    const int XS = g.XS;
+    off[0] = 0;
+    off[1] = XS * 2 * g.XR * 128;
+    off[2] = off[1] + g.cchunks * 2 * g.D1s * 128;
+    off[3] = off[2] + (g.D1s / 32) * g.KK * 4 * 2 * g.D2s * 16;
+    off[4] = off[3] + (g.D2s / 8) * 2 * g.N3p * 16;
+    off[5] = off[4] + 2 * (g.D1s / 8) * g.NRB * g.Wq * 16;  // Z buffer 0
+    return s;
 }
 
 tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t p) {

@@ -667,7 +667,7 @@ tdc_status tdc_model_create(const tdc_model_op *ops, int32_t n_ops, int32_t max_
             if (s == TDC_OK) {
                 tdc_plan_info info;
                 tdc_conv_plan_query(op.tkd, &info);
-                if (info.variant != 4)
+                if (info.variant != 4 && info.variant != 5)  // 3-launch or single-launch 3xBF16
                     s = mfail(TDC_ERR_UNSUPPORTED, "op %d: TKD layer did not get the 3xBF16 tensor-core plan", i);
             }
         } else if (o.kind == TDC_OP_CONV || o.kind == TDC_OP_FC) {

@@ -50,7 +50,7 @@ class tdc_plan_info(ctypes.Structure):
 
 
 HINT_FIELDS = ("core3", "bn_stage1", "bn_core", "bn_stage3", "ksplit_stage1", "ksplit_core", "ksplit_stage3",
-               "gsplit_stage1", "gsplit_core", "gsplit_stage3")
+               "gsplit_stage1", "gsplit_core", "gsplit_stage3", "fused_layer")
 
 
 class tdc_plan_hints(ctypes.Structure):
@@ -154,7 +154,7 @@ def tdc_conv_plan(desc: tdc_conv_desc, core, u_in, u_out, bias=None, device: int
 
 def make_hints(**kw) -> tdc_plan_hints:
     """Planner overrides; unspecified fields = the planner's own choice."""
-    h = tdc_plan_hints(core3=-1)
+    h = tdc_plan_hints(core3=-1, fused_layer=-1)
     for k, v in kw.items():
         if k not in HINT_FIELDS:
             raise KeyError(k)

@@ -1,0 +1,138 @@
+"""The single-launch 3xBF16 layer kernel (variant 5, tkd_layer.cu: stage 1 -> X' band
+ring in shared memory -> core -> Z in shared memory -> stage 3) against the fp64
+oracle (reading R13: max-normalized error <= 1e-4), on shapes that exercise the band
+ring: tiles that start an image or a CTA's range (halo rows recomputed), ring
+wrap-around with mirrored rows, ragged channel counts and ranks (zero padding to
+32), 1x1 and 5x5 cores, batch 1 .. 32, partial batches, bias and the model-path
+residual/ReLU epilogue."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import LayerShape
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2211_03715_b200 import tdc
+    return torch, tdc
+
+
+def run(env, s, d, batch=None, hints=None, res=None, relu=0):
+    torch, tdc = env
+    plan = tdc.ConvPlan(s, d, layout=tdc.TDC_LAYOUT_NHWC, math=tdc.TDC_MATH_3XBF16, hints=hints)
+    b = s.B if batch is None else batch
+    x = torch.from_numpy(synth.nchw_to_nhwc(d["x"][:b])).cuda()
+    y = torch.full((b, s.Ho, s.Wo, s.N), float("nan"), device="cuda")
+    if res is None and not relu:
+        plan.forward(x, y, batch=b)
+    else:
+        r = torch.from_numpy(synth.nchw_to_nhwc(res[:b])).cuda() if res is not None else None
+        tdc.tdc_conv_forward_ex(plan._h, x.data_ptr(), y.data_ptr(), b, r.data_ptr() if r is not None else 0, relu)
+    torch.cuda.synchronize()
+    info = plan.info()
+    plan.close()
+    return synth.nhwc_to_nchw(y.cpu().numpy()), info
+
+
+def err(got, ref):
+    return float(np.max(np.abs(got.astype(np.float64) - ref)) / np.max(np.abs(ref)))
+
+
+SHAPES = [
+    LayerShape(2, 64, 64, 56, 56, 32, 32, 3, 1, 1, "r18_56"),       # the bench's dominant layer
+    LayerShape(3, 16, 16, 8, 8, 4, 4, 3, 1, 1, "config1_b3"),       # BASELINE config 1 shape
+    LayerShape(2, 37, 29, 13, 11, 7, 5, 3, 1, 1, "ragged"),          # C % 4 != 0 -> not this kernel
+    LayerShape(2, 40, 36, 13, 11, 7, 5, 3, 1, 1, "ragged4"),
+    LayerShape(2, 128, 32, 20, 14, 16, 16, 3, 1, 1, "c128_2chunks"),
+    LayerShape(1, 64, 64, 30, 30, 32, 32, 5, 1, 2, "k5_fallback"),          # 25 taps: weights too big
+    LayerShape(1, 16, 16, 12, 12, 8, 8, 5, 1, 2, "k5_fallback2"),          # 25 taps x 32-padded ranks
+    LayerShape(2, 32, 64, 9, 9, 16, 16, 1, 1, 0, "k1"),
+    LayerShape(2, 64, 32, 17, 100, 32, 32, 3, 1, 1, "wide_r1_fallback"),  # Wp = 102: band too big
+    LayerShape(2, 16, 16, 9, 70, 16, 16, 3, 1, 1, "wide_r1"),                # Wp = 72 -> R = 1 < e = 2
+    LayerShape(2, 64, 64, 12, 12, 32, 32, 3, 1, 0, "nopad"),
+    LayerShape(1, 64, 64, 1, 1, 16, 16, 3, 1, 1, "1x1_image"),
+]
+
+
+@pytest.mark.parametrize("s", SHAPES, ids=lambda s: s.name)
+def test_layer_kernel_matches_oracle(env, s):
+    d = synth.make_layer(s, seed=11, bias=True)
+    got, info = run(env, s, d)
+    if s.C % 4 == 0 and "fallback" not in s.name:
+        assert info.variant_name == "layer_3xbf16_fused", info.variant_name
+        assert info.launches_per_forward == 1
+    ref = oracle.tkd_stages(d["x"], d["core"], d["u_in"], d["u_out"], d["bias"], s.stride, s.pad)
+    assert np.all(np.isfinite(got))
+    assert err(got, ref) <= TOL, (s.name, err(got, ref))
+
+
+def test_integer_layer_is_bit_exact(env):
+    s = LayerShape(3, 16, 16, 10, 9, 8, 4, 3, 1, 1)
+    d = synth.make_layer(s, integer=True, bias=True)
+    got, info = run(env, s, d)
+    assert info.variant_name == "layer_3xbf16_fused"
+    ref = oracle.tkd_stages(d["x"], d["core"], d["u_in"], d["u_out"], d["bias"], s.stride, s.pad)
+    assert np.array_equal(got.astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("B", [1, 5, 32])
+def test_r18_56_full_batch_against_oracle_images(env, B):
+    """Batch 32 = the bench's launch (896 tiles over 148 CTAs: every CTA range starts
+    mid-image and crosses image boundaries); images 0, B/2 and B-1 element by element."""
+    s = LayerShape(B, 64, 64, 56, 56, 32, 32, 3, 1, 1)
+    d = synth.make_layer(s, seed=synth.BASE_SEED)
+    got, info = run(env, s, d)
+    assert info.variant_name == "layer_3xbf16_fused"
+    imgs = sorted({0, B // 2, B - 1})
+    ref = oracle.tkd_stages(d["x"][imgs], d["core"], d["u_in"], d["u_out"], None, s.stride, s.pad)
+    assert err(got[imgs], ref) <= TOL
+
+
+def test_partial_batch_is_slice_of_full_batch(env):
+    s = LayerShape(9, 64, 64, 20, 20, 32, 32, 3, 1, 1)
+    d = synth.make_layer(s, seed=3)
+    full, _ = run(env, s, d)
+    part, _ = run(env, s, d, batch=4)
+    one, _ = run(env, s.with_batch(1), {**d, "x": d["x"][:1]})
+    # a different batch gives a different CTA partition (other halo recomputation), but
+    # every output is computed by the same arithmetic: bit-identical
+    assert np.array_equal(part, full[:4])
+    assert np.array_equal(one[0], full[0])
+
+
+def test_deterministic(env):
+    s = LayerShape(8, 64, 64, 28, 28, 32, 32, 3, 1, 1)
+    d = synth.make_layer(s, seed=5)
+    a, _ = run(env, s, d)
+    b, _ = run(env, s, d)
+    assert np.array_equal(a, b)
+
+
+def test_residual_relu_epilogue(env):
+    s = LayerShape(2, 64, 64, 14, 14, 16, 32, 3, 1, 1)
+    d = synth.make_layer(s, seed=8, bias=True)
+    res = np.random.default_rng(1).standard_normal((s.B, s.N, s.Ho, s.Wo)).astype(np.float32)
+    got, info = run(env, s, d, res=res, relu=1)
+    assert info.variant_name == "layer_3xbf16_fused"
+    ref = oracle.tkd_stages(d["x"], d["core"], d["u_in"], d["u_out"], d["bias"], s.stride, s.pad)
+    ref = np.maximum(ref + res.astype(np.float64), 0.0)
+    assert err(got, ref) <= TOL
+
+
+def test_hint_zero_selects_three_launch_kernels(env):
+    s = LayerShape(2, 64, 64, 16, 16, 32, 32, 3, 1, 1)
+    d = synth.make_layer(s, seed=4)
+    a, ia = run(env, s, d)
+    b, ib = run(env, s, d, hints={"fused_layer": 0})
+    assert ia.variant_name == "layer_3xbf16_fused" and ib.variant_name != "layer_3xbf16_fused"
+    ref = oracle.tkd_stages(d["x"], d["core"], d["u_in"], d["u_out"], None, s.stride, s.pad)
+    assert err(a, ref) <= TOL and err(b, ref) <= TOL
