@@ -901,7 +901,14 @@ tdc_status plan_layer(tdc_conv_plan_s *p, const float *core, const float *u_in, 
     if (g.XR > 128 || g.ZR > 128) return TDC_OK;
     g.cchunks = div_up(C, 64);
     g.D1s = D1s; g.D2s = D2s; g.N3p = N3p;
-    const int tcols = 4 * D1s + 4 * D2s + 4 * N3p;
+    {   // taps along N (K = 3, D2s = 32): 1 acc1 + 1 acc2 of 6*D2s columns + 2 acc3
+        const char *ev = std::getenv("TDC_LAYER_TN");  // A/B knob: 0 disables
+        // opt-in (TDC_LAYER_TN=1): measured 2x slower on the 56x56 layer
+        g.tn = K == 3 && D2s == 32 && 4 * D1s + 6 * D2s + 2 * N3p <= 512 && ev && ev[0] == '1';
+        const char *e3 = std::getenv("TDC_LAYER_NCAT3");  // A/B knob
+        g.ncat3 = e3 ? (e3[0] == '1') : 1;
+    }
+    const int tcols = g.tn ? 4 * D1s + 6 * D2s + 2 * N3p : 4 * D1s + 4 * D2s + (g.ncat3 ? 4 : 2) * N3p;
     if (tcols > 512) return TDC_OK;
     g.tmem_cols = 32;
     while (g.tmem_cols < tcols) g.tmem_cols *= 2;
@@ -939,16 +946,22 @@ tdc_status plan_layer(tdc_conv_plan_s *p, const float *core, const float *u_in, 
                     w1[at] = hl ? lo : hi;
                 }
             }
-    for (int r = 0; r < K; ++r)                 // [kc][tap][plane][row: hi q | lo D2s + q][8]
+    for (int r = 0; r < K; ++r)
         for (int t = 0; t < K; ++t)
             for (int q = 0; q < D2; ++q)
                 for (int a = 0; a < D1; ++a) {
                     uint16_t hi, lo;
                     split(core[(((size_t)q * D1 + a) * K + r) * K + t], &hi, &lo);
                     const int tap = r * K + t, kc = a / 32, pl = (a % 32) / 8, e8 = a % 8;
-                    const size_t base = (((size_t)kc * KK + tap) * 4 + pl) * 2 * D2s;
-                    w2[(base + q) * 8 + e8] = hi;
-                    w2[(base + D2s + q) * 8 + e8] = lo;
+                    if (g.tn) {  // [kc][r][plane][rows: hi (t, q) = t*D2s + q | lo 3*D2s + t*D2s + q][8]
+                        const size_t base = (((size_t)kc * K + r) * 4 + pl) * 6 * D2s;
+                        w2[(base + t * D2s + q) * 8 + e8] = hi;
+                        w2[(base + 3 * D2s + t * D2s + q) * 8 + e8] = lo;
+                    } else {     // [kc][tap][plane][row: hi q | lo D2s + q][8]
+                        const size_t base = (((size_t)kc * KK + tap) * 4 + pl) * 2 * D2s;
+                        w2[(base + q) * 8 + e8] = hi;
+                        w2[(base + D2s + q) * 8 + e8] = lo;
+                    }
                 }
     for (int n = 0; n < N; ++n)                 // [plane q/8][row: hi n | lo N3p + n][8]
         for (int q = 0; q < D2; ++q) {

@@ -92,7 +92,7 @@ constexpr int kS13Warp = 18;        // stage-1 / stage-3 MMA issue
 constexpr uint32_t kEpiScr = 4 * 4096;
 
 struct LayerSmem {
-    uint32_t xs, w1, w2, w3, band, z, scr, bars, total;
+    uint32_t xs, w1, w2, w3, band, z, scr, xch, bars, total;
 };
 
 __host__ __device__ inline LayerSmem layer_smem(const BfLayerArgs &g) {
@@ -105,6 +105,7 @@ __host__ __device__ inline LayerSmem layer_smem(const BfLayerArgs &g) {
     s.band = o; o += 2u * (g.D1s / 8) * g.NRB * g.Wq * 16;
     s.z = o;    o += 2u * 2u * (g.D2s / 8) * g.ZR * 16;  // two Z buffers (hi | lo each)
     s.scr = o;  o += kEpiScr;
+    s.xch = o;  o += g.tn ? 2 * 4 * 48 * 4 : 0;  // TN: epilogue-2 row exchange
     s.bars = o; o += 64 * 8 + 16;
     s.total = o + 1024;  // + alignment slack of the dynamic shared memory base
     return s;
@@ -128,7 +129,13 @@ __device__ __forceinline__ TileGeo tile_geo(const BfLayerArgs &g, int k, int k0)
     return t;
 }
 
-template <int KT>  // core size K at compile time (3), or 0 = any K
+// KT: core size K at compile time (3), or 0 = any K.  TN ("taps along N", K = 3, D2 = 32):
+// the three taps of a core row share one A operand -- B = [taps (r,0),(r,1),(r,2) hi | lo],
+// N = 6*D2 -- so stage 2 issues 12 MMAs of N = 192/96 per tile instead of 36 of N = 64/32
+// (a third of the band re-reads); the horizontal shift t of tap (r,t) is applied by
+// epilogue 2 (Z[m] = sum_t acc[m + t][tap t], lane shuffles + a 2-row exchange between
+// the epilogue warps).  Its 192-column accumulator and one acc1 buffer fit TMEM.
+template <int KT, bool TN>
 __global__ void __launch_bounds__(kLayerThreads, 1)
 tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -181,8 +188,12 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
     const int k0 = (int)((long long)blockIdx.x * g.num_tiles / gridDim.x);
     const int k1 = (int)((long long)(blockIdx.x + 1) * g.num_tiles / gridDim.x);
     const int nt = k1 - k0;
-    const uint32_t acc1_cols = 2 * g.D1s, acc2_cols = 2 * g.D2s, acc3_cols = 2 * g.N3p;
-    const uint32_t acc2_base = 2 * acc1_cols, acc3_base = acc2_base + 2 * acc2_cols;
+    // TN: acc2 is 6*D2s wide and single-buffered; stage 3 then skips the hi|lo concatenation
+    // (3 MMAs into N3p columns instead of 2 into 2*N3p) so both acc1 and acc3 stay double-buffered
+    constexpr int NA1 = 2, NA2 = TN ? 1 : 2;  // acc1 / acc2 buffers
+    const bool s3cat = !TN && g.ncat3;  // stage 3 with [hi | lo] U_out along N (2 MMAs, 2*N3p columns)
+    const uint32_t acc1_cols = 2 * g.D1s, acc2_cols = (TN ? 6 : 2) * g.D2s, acc3_cols = (s3cat ? 2 : 1) * g.N3p;
+    const uint32_t acc2_base = NA1 * acc1_cols, acc3_base = acc2_base + NA2 * acc2_cols;
     const uint32_t plane_stride = (uint32_t)g.NRB * g.Wq * 16;   // bytes between band planes
     const uint32_t band_half = (uint32_t)(g.D1s / 8) * plane_stride;  // hi -> lo
     const uint32_t zhalf = (uint32_t)(g.D2s / 8) * g.ZR * 16;      // Z hi -> lo
@@ -253,6 +264,8 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
         const uint64_t dw1 = sdesc_kmajor_sw128(smem_u32(smem + L.w1));
         const uint64_t dband = sdesc_kmajor_none(smem_u32(smem + L.band), plane_stride, 128);
         const uint64_t dw2 = sdesc_kmajor_none(smem_u32(smem + L.w2), 2 * g.D2s * 16, 128);
+        const uint64_t dw2tn = sdesc_kmajor_none(smem_u32(smem + L.w2), 6 * g.D2s * 16, 128);
+        const uint32_t id2tn = idesc_bf16(128, 6 * g.D2s), id2tnh = idesc_bf16(128, 3 * g.D2s);
         const uint64_t dz = sdesc_kmajor_none(smem_u32(smem + L.z), g.ZR * 16, 128);
         const uint64_t dw3 = sdesc_kmajor_none(smem_u32(smem + L.w3), 2 * g.N3p * 16, 128);
         const uint32_t w1_chunk = (uint32_t)2 * g.D1s * 128;
@@ -264,7 +277,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
         mbar_wait(w_full, 0);
         int s1_tile = 0;  // (timeline) local tile of the next stage-1 block
         auto s1_block = [&]() {
-            const uint32_t ab = ublk & 1, aph = (ublk >> 1) & 1;
+            const uint32_t ab = NA1 == 1 ? 0u : (ublk & 1), aph = NA1 == 1 ? (ublk & 1) : ((ublk >> 1) & 1);
             if (lane == 0) LTL(s1_tile, 13);  // MMA: S1 block start
             mbar_wait(&a1_empty[ab], aph ^ 1);
             tc_fence_after();
@@ -292,13 +305,36 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
             if (lane == 0) LTL(s1_tile, 2);  // MMA: S1 block issued
         };
         auto s2 = [&](int t, uint32_t start) {
-            const uint32_t sb = t & 1, sph = (t >> 1) & 1;
+            const uint32_t sb = t & 1, sph = (t >> 1) & 1;                       // band ring
+            const uint32_t ab2 = NA2 == 1 ? 0u : sb, aph2 = NA2 == 1 ? (t & 1) : sph;  // acc2
             mbar_wait(&band_ready[sb], sph);
-            mbar_wait(&a2_empty[sb], sph ^ 1);
+            mbar_wait(&a2_empty[ab2], aph2 ^ 1);
             tc_fence_after();
-            const uint32_t d = tmem + acc2_base + sb * acc2_cols;
+            const uint32_t d = tmem + acc2_base + ab2 * acc2_cols;
             const uint64_t arow = dband + start * (uint32_t)g.Wq;  // 16-byte units
-            if (KT > 0) {
+            if (TN) {
+                const uint32_t wq = (uint32_t)g.Wq, p2a = (2 * plane_stride) >> 4, lo_a = band_half >> 4;
+                const uint32_t wr = (4 * 6 * g.D2s * 16) >> 4, p2b = (2 * 6 * g.D2s * 16) >> 4;  // per row r / K16
+                for (int kc = 0; kc < (LKNOB(16) ? 0 : kc2); ++kc) {
+                    const uint64_t ak = arow + (uint32_t)kc * ((4 * plane_stride) >> 4);
+                    const uint64_t bk = dw2tn + (uint32_t)kc * 3 * wr;
+                    if (elect_one()) {
+#pragma unroll
+                        for (int r = 0; r < 3; ++r)
+#pragma unroll
+                            for (int j = 0; j < 2; ++j) {
+                                const uint64_t aj = ak + r * wq + j * p2a, bj = bk + r * wr + j * p2b;
+                                mma_bf16(d, aj, bj, id2tn, (kc > 0) || r || j);  // hi * [3 taps hi | 3 taps lo]
+                                mma_bf16(d, aj + lo_a, bj, id2tnh, 1);           // lo * [3 taps hi]
+                            }
+                    }
+                    __syncwarp();
+                }
+                if (elect_one()) {
+                    mma_commit(&band_free[sb]);
+                    mma_commit(&a2_full[ab2]);
+                }
+            } else if (KT > 0) {
                 // compile-time taps: every descriptor is the converged, warp-uniform row base
                 // plus r*Wq + t (16-byte rows), so the MMAs issue back to back from uniform
                 // registers instead of each waiting on a parameter load + R2UR chain
@@ -324,7 +360,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
                 }
                 if (elect_one()) {
                     mma_commit(&band_free[sb]);
-                    mma_commit(&a2_full[sb]);
+                    mma_commit(&a2_full[ab2]);
                 }
             } else if (elect_one()) {
                 uint32_t acc = 0;
@@ -342,7 +378,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
                         }
                     }
                 mma_commit(&band_free[sb]);
-                mma_commit(&a2_full[sb]);
+                mma_commit(&a2_full[ab2]);
             }
             __syncwarp();
         };
@@ -356,8 +392,14 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
                 const uint64_t zs = dz + ((sb * 2 * zhalf) >> 4);
                 for (int j = 0; j < (LKNOB(64) ? 0 : k3); ++j) {
                     const uint64_t a = zs + ((j * 2 * g.ZR * 16) >> 4), b = dw3 + ((j * w3_plane2) >> 4);
-                    mma_bf16(d, a, b, id3, j > 0);
-                    mma_bf16(d, a + (zhalf >> 4), b, id3h, 1);
+                    if (!s3cat) {  // hi*hi, hi*lo, lo*hi into the same N3p columns (half the TMEM reads)
+                        mma_bf16(d, a, b, id3h, j > 0);
+                        mma_bf16(d, a, b + ((g.N3p * 16) >> 4), id3h, 1);
+                        mma_bf16(d, a + (zhalf >> 4), b, id3h, 1);
+                    } else {
+                        mma_bf16(d, a, b, id3, j > 0);
+                        mma_bf16(d, a + (zhalf >> 4), b, id3h, 1);
+                    }
                 }
                 mma_commit(&z_empty[sb]);
                 mma_commit(&a3_full[sb]);
@@ -407,7 +449,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
         for (int t = 0; t < nt; ++t) {
             const TileGeo tg = tile_geo(g, k0 + t, k0);
             for (int blk = 0; blk < tg.nb; ++blk, ++ublk) {
-                const uint32_t ab = ublk & 1, aph = (ublk >> 1) & 1;
+                const uint32_t ab = NA1 == 1 ? 0u : (ublk & 1), aph = NA1 == 1 ? (ublk & 1) : ((ublk >> 1) & 1);
                 if (blk == 0 && t > 0) {  // ring rows about to be overwritten are no longer read
                     const int tw = tg.fresh ? t - 1 : t - 2;
                     if (tw >= 0) ewait(&band_free[tw & 1], (tw >> 1) & 1);
@@ -462,20 +504,85 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         const int r = q * 32 + lane;
         const bool zrow = r < g.ZR;  // Z planes hold ZR rows (rows beyond: junk MMA rows)
+        float *xbuf = reinterpret_cast<float *>(smem + L.xch);  // TN: [chunk 2][quarter 4][3][16]
         for (int t = 0; t < nt; ++t) {
             const uint32_t sb = t & 1, sph = (t >> 1) & 1;
+            const uint32_t ab2 = NA2 == 1 ? 0u : sb, aph2 = NA2 == 1 ? (t & 1) : sph;
             const uint32_t zb = smem_u32(smem + L.z) + sb * 2 * zhalf;
-            ewait(&a2_full[sb], sph);
+            ewait(&a2_full[ab2], aph2);
             tc_fence_after();
             if (threadIdx.x == 192) LTL(t, 7);  // E2: acc2 full seen
+            if (TN) {  // Z[m] = sum_t (hi + lo part of tap t)[m + t]  (D2s = 32: two 16-column chunks)
+                const uint32_t a2 = tmem + lane_base + acc2_base;
+                const uint32_t lo3 = 3 * g.D2s;
+                uint4 h0[4], l0[4];
+#pragma unroll
+                for (int ch = 0; ch < 2; ++ch) {
+                    const int c = ch * 16;
+                    float p[3][16];
+#pragma unroll
+                    for (int tp = 0; tp < 3; ++tp) {
+                        uint32_t r0[16], r1[16];
+                        tmem_ld_32x32b_x16(a2 + tp * g.D2s + c, r0);
+                        tmem_ld_32x32b_x16(a2 + lo3 + tp * g.D2s + c, r1);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) p[tp][jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
+                    }
+                    if (threadIdx.x == 192) LTL(t, 16 + ch);  // E2 (TN): chunk ch loaded
+                    if (ch == 1) {  // every TMEM read of this tile done: S2(t+1) may overwrite acc2
+                        tc_fence_before();
+                        mbar_arrive_relaxed(&a2_empty[0]);
+                    }
+                    // rows m+1, m+2 of the last lanes live in the next lane quarter: publish ours
+                    float *mine = xbuf + (ch * 4 + q) * 48, *next = xbuf + (ch * 4 + ((q + 1) & 3)) * 48;
+                    if (lane == 0)
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) {
+                            mine[jj] = p[1][jj];
+                            mine[16 + jj] = p[2][jj];
+                        }
+                    if (lane == 1)
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) mine[32 + jj] = p[2][jj];
+                    asm volatile("bar.sync 3, 128;" ::: "memory");
+                    if (threadIdx.x == 192) LTL(t, 18 + ch);  // E2 (TN): exchange done
+                    float v[16];
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        float s1 = __shfl_down_sync(0xffffffffu, p[1][jj], 1);
+                        float s2 = __shfl_down_sync(0xffffffffu, p[2][jj], 2);
+                        if (lane == 31) s1 = next[jj];
+                        if (lane >= 30) s2 = next[16 + (lane - 30) * 16 + jj];
+                        v[jj] = p[0][jj] + s1 + s2;
+                    }
+                    split_bf16x8(v, h0[2 * ch], l0[2 * ch]);
+                    split_bf16x8(v + 8, h0[2 * ch + 1], l0[2 * ch + 1]);
+                }
+                ewait(&z_empty[sb], sph ^ 1);  // S3 two tiles back has read this Z buffer
+                if (threadIdx.x == 192) LTL(t, 12);
+                if (!LKNOB(8) && zrow)
+#pragma unroll
+                    for (int pl = 0; pl < 4; ++pl) {
+                        const uint32_t o = ((uint32_t)pl * g.ZR + r) * 16;
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(zb + o), "r"(h0[pl].x),
+                                     "r"(h0[pl].y), "r"(h0[pl].z), "r"(h0[pl].w) : "memory");
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(zb + zhalf + o), "r"(l0[pl].x),
+                                     "r"(l0[pl].y), "r"(l0[pl].z), "r"(l0[pl].w) : "memory");
+                    }
+                fence_proxy_async_smem();
+                mbar_arrive(&z_full[sb]);
+                if (threadIdx.x == 192) LTL(t, 8);
+                continue;
+            }
             // the first 32 columns are read and split before waiting for the Z buffer, so the
             // S3(t-1) -> E2(t) -> S3(t) hand-off carries only the shared-memory stores
             uint4 h0[4], l0[4];
 #pragma unroll
             for (int c = 0; c < 32; c += 16) {
                 uint32_t r0[16], r1[16];
-                tmem_ld_32x32b_x16(tmem + lane_base + acc2_base + sb * acc2_cols + c, r0);
-                tmem_ld_32x32b_x16(tmem + lane_base + acc2_base + sb * acc2_cols + g.D2s + c, r1);
+                tmem_ld_32x32b_x16(tmem + lane_base + acc2_base + ab2 * acc2_cols + c, r0);
+                tmem_ld_32x32b_x16(tmem + lane_base + acc2_base + ab2 * acc2_cols + g.D2s + c, r1);
                 tmem_ld_wait();
                 float v[16];
 #pragma unroll
@@ -496,8 +603,8 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
                 }
             for (int c = 32; c < g.D2s; c += 16) {
                 uint32_t r0[16], r1[16];
-                tmem_ld_32x32b_x16(tmem + lane_base + acc2_base + sb * acc2_cols + c, r0);
-                tmem_ld_32x32b_x16(tmem + lane_base + acc2_base + sb * acc2_cols + g.D2s + c, r1);
+                tmem_ld_32x32b_x16(tmem + lane_base + acc2_base + ab2 * acc2_cols + c, r0);
+                tmem_ld_32x32b_x16(tmem + lane_base + acc2_base + ab2 * acc2_cols + g.D2s + c, r1);
                 tmem_ld_wait();
                 float v[16];
 #pragma unroll
@@ -515,7 +622,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
                 }
             }
             tc_fence_before();
-            mbar_arrive_relaxed(&a2_empty[sb]);
+            mbar_arrive_relaxed(&a2_empty[ab2]);
             fence_proxy_async_smem();
             mbar_arrive(&z_full[sb]);
             if (threadIdx.x == 192) LTL(t, 8);  // E2: Z written
@@ -543,10 +650,11 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
                 for (int hh = 0; hh < 2; ++hh) {
                     uint32_t r0[16], r1[16];
                     tmem_ld_32x32b_x16(tmem + lane_base + acc3_base + sb * acc3_cols + c + 16 * hh, r0);
-                    tmem_ld_32x32b_x16(tmem + lane_base + acc3_base + sb * acc3_cols + g.N3p + c + 16 * hh, r1);
+                    if (s3cat) tmem_ld_32x32b_x16(tmem + lane_base + acc3_base + sb * acc3_cols + g.N3p + c + 16 * hh, r1);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) v[16 * hh + jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
+                    for (int jj = 0; jj < 16; ++jj)
+                        v[16 * hh + jj] = s3cat ? __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]) : __uint_as_float(r0[jj]);
                 }
                 if (c >= g.N) continue;  // warp-uniform
                 epi_bias_res_relu<32>(v, c, g.N, g.bias, (g.res && valid) ? g.res + orow * g.N : nullptr, g.relu);
@@ -635,7 +743,8 @@ cudaError_t bf_layer_launch(const CUtensorMap &mapX, const BfLayerArgs &g, int g
         if (e != cudaSuccess) return e;
         return launch_pdl(kernel, grid, kLayerThreads, smem, st, mapX, g);
     };
-    return g.K == 3 ? go(tdc_bf_layer_kernel<3>) : go(tdc_bf_layer_kernel<0>);
+    if (g.tn) return go(tdc_bf_layer_kernel<3, true>);
+    return g.K == 3 ? go(tdc_bf_layer_kernel<3, false>) : go(tdc_bf_layer_kernel<0, false>);
 }
 
 }  // namespace tdc

@@ -22,7 +22,7 @@ torch.cuda.synchronize()
 tdc.lib.tdc_debug_layer_timeline(buf, n, cta)
 a = np.array(buf, dtype=np.int64).reshape(32, 24)
 names = ["prodX", "convD", "S1iss", "S2iss", "S3iss", "E1acc", "E1rdy", "E2acc", "E2done", "E3acc", "E3done",
-         "S2wait", "E2zfree", "S1start", "S1acc1", "S1conv", "cvw1", "cvw2", "cvw3", "Xland"]
+         "S2wait", "E2zfree", "S1start", "S1acc1", "S1conv", "E2ld0", "E2ld1", "E2xc0", "E2xc1"]
 rows = a[a[:, 5] > 0]
 t0 = a[a > 0].min()
 print("tile " + " ".join(f"{nm:>7s}" for nm in names))
