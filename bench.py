@@ -475,6 +475,27 @@ def impl_tdc(args):
             "math": "3xbf16 (fp32-grade)", "batch_per_gpu": tdist.shard(64, world, rank)[1], "global_batch": 64,
             "n_gpus": world, "scaling": "strong (global batch 64 sharded)", "ms_per_batch": round(vms, 4),
             "images_per_s": round(64 / (vms * 1e-3), 1), "launch": how}
+        # NEXT-2: Tucker ResNet-18 with the paper-style uniform ranks and with the
+        # per-layer ranks the hardware-aware selection picked from measured B200 tables
+        import glob
+        plans = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_rank_plan_r18_b32.json")))
+        r18 = {"batch_per_gpu": mb, "global_batch": mb * world, "input": "224x224x3 synthetic",
+               "math": "3xbf16 (fp32-grade)"}
+        variants = [("paper_style_r1/2", None, None)]
+        if plans:
+            with open(plans[-1]) as f:
+                rp = json.load(f)
+            r18["rank_plan"] = os.path.relpath(plans[-1], ROOT)
+            for meth in ("greedy", "exact"):
+                variants.append((f"selected_{meth}", {k: tuple(v) for k, v in rp[meth]["ranks"].items()},
+                                 rp[meth]["reduction"]))
+        for label, ranks, red in variants:
+            rms, how = time_model(sm.tucker_resnet(18, seed=synth.BASE_SEED, ranks=ranks), mb * world)
+            r18[label] = {"ms_per_batch": round(rms, 4), "images_per_s": round(mb * world / (rms * 1e-3), 1),
+                          "launch": how}
+            if red is not None:
+                r18[label]["flops_reduction"] = red
+        model["tucker_resnet18"] = r18
         if not args.no_model_sweep:  # BASELINE config 3: ResNet-50 at batch 1..256 per GPU
             sweep = {}
             for sb in (1, 8, 64, 128, 256):

@@ -76,8 +76,9 @@ def default_grid(C: int, N: int, fractions: Sequence[float] = FULL_GRID) -> List
 def measure_latency_us(layer: LayerSpec, d1: int, d2: int, batch: int, math_mode: str = "3xbf16",
                        iters: int = 50, warmup: int = 5, seed: int = 42) -> float:
     """Mean µs per forward of the layer at ranks (d1, d2), measured on the current GPU
-    through the C-ABI: back-to-back forwards on one stream between CUDA events, four
-    rotating input/output buffers."""
+    through the C-ABI: `iters` forwards (four rotating input/output buffers) captured as
+    one CUDA graph and replayed between CUDA events, so the table holds device time and
+    not the host's launch rate (plain launches flatten small layers at ~12 µs)."""
     import torch
 
     import synth
@@ -90,16 +91,25 @@ def measure_latency_us(layer: LayerSpec, d1: int, d2: int, batch: int, math_mode
     try:
         xs = [torch.from_numpy(synth.nchw_to_nhwc(d["x"])).cuda() for _ in range(4)]
         ys = [torch.empty((s.B, s.Ho, s.Wo, s.N), device="cuda") for _ in range(4)]
-        st = torch.cuda.current_stream()
-        for k in range(warmup):
-            plan.forward(xs[k % 4], ys[k % 4])
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            for k in range(warmup):
+                plan.forward(xs[k % 4], ys[k % 4], stream=st)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for k in range(iters):
+                plan.forward(xs[k % 4], ys[k % 4], stream=st)
+        with torch.cuda.stream(st):
+            g.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        for k in range(iters):
-            plan.forward(xs[k % 4], ys[k % 4])
+        with torch.cuda.stream(st):
+            g.replay()
         e1.record(st)
         torch.cuda.synchronize()
+        del g
         return e0.elapsed_time(e1) * 1e3 / iters
     finally:
         plan.close()

@@ -3,8 +3,8 @@ and the ResNet-18 layer list) on this GPU, then select ranks under the paper's b
 
   python scripts/rank_sweep.py [--math 3xbf16] [--out profiles] [--quick]
 
-Writes <out>/r01_rank_sweep_28x28x256_b{1,32}.json (config 5: D1, D2 in {8..128}),
-<out>/r01_rank_tables_r18_b32.json and <out>/r01_rank_plan_r18_b32.json (greedy and
+Writes <out>/<prefix>_rank_sweep_28x28x256_b{1,32}.json (config 5: D1, D2 in {8..128}),
+<out>/<prefix>_rank_tables_r18_b32.json and <out>/<prefix>_rank_plan_r18_b32.json (greedy and
 exact selections at B = 0.63, P:L555 / P:L582)."""
 import argparse
 import json
@@ -25,7 +25,8 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--budget", type=float, default=0.63)
     ap.add_argument("--slack", type=float, default=0.05)
-    ap.add_argument("--from-tables", help="re-run only the selection on a saved r01_rank_tables json")
+    ap.add_argument("--from-tables", help="re-run only the selection on a saved rank_tables json")
+    ap.add_argument("--prefix", default="r02", help="output file prefix (round)")
     a = ap.parse_args()
     if a.from_tables:
         with open(a.from_tables) as f:
@@ -46,7 +47,7 @@ def main():
     for b in (1, 32):
         tab = ranksel.measure_table(cfg5, grid5, b, a.math, iters)
         obj = ranksel.table_to_json(cfg5, tab, b, a.math)
-        ranksel.save_json(os.path.join(a.out, f"r01_rank_sweep_28x28x256_b{b}.json"), obj)
+        ranksel.save_json(os.path.join(a.out, f"{a.prefix}_rank_sweep_28x28x256_b{b}.json"), obj)
         print(f"config 5, batch {b}: " + " ".join(f"{k}:{v:.1f}" for k, v in sorted(tab.items())), flush=True)
     # ---- ResNet-18 layer list, grid at multiples of C/8, batch 32
     layers = ranksel.resnet18_layers()
@@ -56,7 +57,7 @@ def main():
         tables[l.name] = ranksel.measure_table(l, grid, 32, a.math, iters)
         dump.append(ranksel.table_to_json(l, tables[l.name], 32, a.math))
         print(f"{l.name}: measured {len(grid)} rank pairs", flush=True)
-    ranksel.save_json(os.path.join(a.out, "r01_rank_tables_r18_b32.json"), dump)
+    ranksel.save_json(os.path.join(a.out, f"{a.prefix}_rank_tables_r18_b32.json"), dump)
     select(layers, tables, a, a.math, 32, time.time() - t0)
 
 
@@ -70,7 +71,7 @@ def select(layers, tables, a, math, batch, seconds):
            "paper_style_C/2": {"ranks": {k: list(v) for k, v in paper.items()}, "latency_us": round(lat_p, 3),
                                "reduction": round(1 - tk_p / orig, 6)},
            "seconds": round(seconds, 1)}
-    ranksel.save_json(os.path.join(a.out, "r01_rank_plan_r18_b32.json"), out)
+    ranksel.save_json(os.path.join(a.out, f"{a.prefix}_rank_plan_r18_b32.json"), out)
     print(json.dumps(out, indent=1))
 
 

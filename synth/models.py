@@ -45,15 +45,18 @@ class _Builder:
         return np.stack([r.uniform(0.8, 1.2, n), r.uniform(-0.1, 0.1, n), r.uniform(-0.1, 0.1, n),
                          r.uniform(0.8, 1.2, n)]).astype(np.float32)
 
-    def conv(self, src, cout, k, s, p, relu=True, res=-1, tkd_ratio=None):
+    def conv(self, src, cout, k, s, p, relu=True, res=-1, tkd_ratio=None, tkd_ranks=None):
         H, W, C = self.geo[src]
         i = len(self.ops)
         Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
         op = {"kind": OP_CONV, "src": src, "res": res, "c_in": C, "c_out": cout, "height": H, "width": W,
               "kernel": k, "stride": s, "pad": p, "rank_in": 0, "rank_out": 0, "relu": int(relu),
               "bias": None, "bn": self._bn(i, cout)}
-        if tkd_ratio is not None:
-            d1, d2 = max(1, math.ceil(tkd_ratio * C)), max(1, math.ceil(tkd_ratio * cout))
+        if tkd_ratio is not None or tkd_ranks is not None:
+            if tkd_ranks is not None:  # per-layer (D1, D2), e.g. from hardware-aware rank selection
+                d1, d2 = int(tkd_ranks[0]), int(tkd_ranks[1])
+            else:
+                d1, d2 = max(1, math.ceil(tkd_ratio * C)), max(1, math.ceil(tkd_ratio * cout))
             op.update(kind=OP_TKD, rank_in=d1, rank_out=d2)
             op["u_in"] = _orthonormal(_rng(self.seed, i, 1), C, d1).astype(np.float32)
             op["w"] = (_rng(self.seed, i, 2).standard_normal((d2, d1, k, k)) *
@@ -84,14 +87,28 @@ class _Builder:
                           "kernel": 1, "stride": 1, "pad": 0, "relu": 0, "w": w, "bias": b, "bn": None}, 1, 1, n)
 
 
+def tkd_layer_name(depth: int, H: int, C: int, N: int, s: int) -> str:
+    """Shape key of a TKD layer, the names of ranksel.resnet18_layers() (r18_56_64_64_s1 ...)."""
+    return f"r{depth}_{H}_{C}_{N}_s{s}"
+
+
 def tucker_resnet(depth: int = 18, image: int = 224, num_classes: int = 1000, ratio: float | None = None,
-                  seed: int = 42, width: int = 64):
+                  seed: int = 42, width: int = 64, ranks: dict | None = None):
     """Op list of a Tucker ResNet-18 (basic blocks) or -50 (bottlenecks).  `width` scales
-    every stage (64 = the real network; tests use smaller widths)."""
+    every stage (64 = the real network; tests use smaller widths).  `ranks` maps a TKD
+    layer's shape key (tkd_layer_name, or "<C>_<N>_s<s>" for any image size) to its
+    (D1, D2) -- the per-layer plan of hardware-aware rank selection; layers
+    it does not name use the uniform ratio."""
     if depth not in (18, 50):
         raise ValueError("depth must be 18 or 50")
     r = ratio if ratio is not None else (0.5 if depth == 18 else 0.25)
     b = _Builder(seed, image, image, 3)
+
+    def rk(src, cin, cout, s):
+        if not ranks:
+            return None
+        H = b.geo[src][0]
+        return ranks.get(tkd_layer_name(depth, H, cin, cout, s)) or ranks.get(f"{cin}_{cout}_s{s}")
     x = b.conv(0, width, 7, 2, 3)                       # stem (dense), BN, ReLU
     x = b.maxpool(x, 3, 2, 1)
     blocks = [2, 2, 2, 2] if depth == 18 else [3, 4, 6, 3]
@@ -106,11 +123,12 @@ def tucker_resnet(depth: int = 18, image: int = 224, num_classes: int = 1000, ra
             if s != 1 or cin != cout:
                 shortcut = b.conv(x, cout, 1, s, 0, relu=False)          # downsample 1x1 (dense) + BN
             if depth == 18:
-                y = b.conv(x, planes, 3, s, 1, tkd_ratio=r)              # TKD + BN + ReLU
-                x = b.conv(y, cout, 3, 1, 1, relu=True, res=shortcut, tkd_ratio=r)  # TKD + BN + add + ReLU
+                y = b.conv(x, planes, 3, s, 1, tkd_ratio=r, tkd_ranks=rk(x, cin, planes, s))  # TKD + BN + ReLU
+                x = b.conv(y, cout, 3, 1, 1, relu=True, res=shortcut, tkd_ratio=r,
+                           tkd_ranks=rk(y, planes, cout, 1))                                # + add + ReLU
             else:
                 y = b.conv(x, planes, 1, 1, 0)                           # 1x1 (dense) + BN + ReLU
-                y = b.conv(y, planes, 3, s, 1, tkd_ratio=r)              # TKD + BN + ReLU
+                y = b.conv(y, planes, 3, s, 1, tkd_ratio=r, tkd_ranks=rk(y, planes, planes, s))  # TKD + BN + ReLU
                 x = b.conv(y, cout, 1, 1, 0, relu=True, res=shortcut)    # 1x1 (dense) + BN + add + ReLU
             cin = cout
     x = b.avgpool(x)

@@ -82,6 +82,34 @@ def test_builder_geometry_and_ranks():
     assert ops50[-1]["kind"] == sm.OP_FC and ops50[-1]["c_out"] == 1000
 
 
+def test_builder_per_layer_ranks():
+    """Per-layer ranks of a rank plan (NEXT-2) reach the op list: shape keys at the real
+    image size, "<C>_<N>_s<s>" keys at any size, the uniform ratio elsewhere."""
+    plan = {"r18_56_64_64_s1": (16, 24), "r18_7_512_512_s1": (128, 192)}
+    ops = sm.tucker_resnet(18, ranks=plan)
+    tkd = [o for o in ops if o["kind"] == sm.OP_TKD]
+    got = {(o["height"], o["c_in"], o["c_out"], o["stride"]): (o["rank_in"], o["rank_out"]) for o in tkd}
+    assert got[(56, 64, 64, 1)] == (16, 24) and got[(7, 512, 512, 1)] == (128, 192)
+    assert got[(28, 128, 128, 1)] == (64, 64)                       # not in the plan: r = 1/2
+    for o in tkd:
+        assert o["u_in"].shape == (o["c_in"], o["rank_in"]) and o["u_out"].shape == (o["c_out"], o["rank_out"])
+        assert o["w"].shape == (o["rank_out"], o["rank_in"], 3, 3)
+    small = sm.tucker_resnet(18, image=32, width=8, ranks={"8_8_s1": (3, 5)})
+    assert all((o["rank_in"], o["rank_out"]) == (3, 5) for o in small
+               if o["kind"] == sm.OP_TKD and o["c_in"] == 8 and o["c_out"] == 8 and o["stride"] == 1)
+
+
+def latest_rank_plan():
+    import glob
+    import json
+    import os
+    paths = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "..", "profiles", "r*_rank_plan_r18_b32.json")))
+    if not paths:
+        return None
+    with open(paths[-1]) as f:
+        return json.load(f)
+
+
 @pytest.fixture(scope="module")
 def gpu():
     torch = pytest.importorskip("torch")
@@ -110,6 +138,25 @@ def test_small_tucker_resnet(gpu, depth, width, image):
     ops = sm.tucker_resnet(depth, image=image, num_classes=37, width=width, seed=7)
     x = sm.model_input(3, image, seed=7)
     assert maxerr(run_model(gpu, ops, x), om.forward(ops, x)) <= MODEL_TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("method", ["greedy", "exact"])
+def test_tucker_resnet18_with_selected_ranks(gpu, method):
+    """NEXT-2 closed: a Tucker ResNet-18 built with the ranks the hardware-aware selection
+    picked from the measured B200 tables (profiles/r*_rank_plan_r18_b32.json), full size,
+    through tdc_model_forward, against the fp64 model oracle."""
+    plan = latest_rank_plan()
+    if plan is None:
+        pytest.skip("no rank plan in profiles/")
+    ranks = {k: tuple(v) for k, v in plan[method]["ranks"].items()}
+    ops = sm.tucker_resnet(18, ranks=ranks)
+    tkd = [o for o in ops if o["kind"] == sm.OP_TKD]
+    assert any((o["rank_in"], o["rank_out"]) != (o["c_in"] // 2, o["c_out"] // 2) for o in tkd) or \
+        all(tuple(v) == (int(k.split("_")[2]) // 2, int(k.split("_")[3]) // 2) for k, v in ranks.items())
+    x = sm.model_input(2, 224, seed=11)
+    got = run_model(gpu, ops, x)
+    assert maxerr(got, om.forward(ops, x)) <= MODEL_TOL
 
 
 @pytest.mark.gpu
