@@ -329,10 +329,18 @@ def impl_tdc(args):
     ridge = eng * 1e12 / (peaks["hbm_gbs"] * 1e9)
     compute_bound = row["ai_flop_per_byte"] > ridge
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            traffic = json.load(f).get(args.math, {}).get(row["layer"])
+    # per-layer ncu traffic of the newest capture: DRAM reads + bytes the SMs wrote into L2
+    # (scripts/ncu_step_r02.py; writes still in L2 when ncu closes the launch are not in
+    # dram__bytes_write), else the round-1 read-dominated figure
+    import glob
+    tpaths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json"))) + \
+        [os.path.join(ROOT, "profiles", "ncu_traffic.json")]
+    for tpath in tpaths:
+        if os.path.exists(tpath):
+            with open(tpath) as f:
+                traffic = json.load(f).get(args.math, {}).get(row["layer"])
+            if traffic is not None:
+                break
     if compute_bound:
         bound = "alu" if args.math == "fp32" else "tensor"
         roof = {"bound": bound, "achieved": row["tflops"], "peak": round(eng, 1), "unit": "TFLOP/s",

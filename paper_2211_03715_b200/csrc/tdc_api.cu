@@ -419,6 +419,10 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
     };
     int BN1 = pick(D1s, M1), BN3 = pick(N, M3);
     int BN2 = pick(D2s, M2);
+    // few output tiles (deep / strided layers): a narrower core N tile while the grid still
+    // fits one wave -- twice the CTAs streaming weight slices (14x14 s2: 26.8 -> 24.6 us,
+    // profiles/r02_tiling_search_r18_b32.json)
+    while (BN2 > 32 && (long long)div_up((int)M2, 128) * div_up(D2s, BN2 / 2) <= p->num_sms) BN2 /= 2;
     // Split K over a thread-block cluster (DSMEM reduction, deterministic order) when the
     // output tiles alone leave SMs idle: pick (BN, cluster size) maximising busy SMs,
     // larger BN on ties.  Opt-in (TDC_SPLITK=1): on the R18 shapes the per-tile
