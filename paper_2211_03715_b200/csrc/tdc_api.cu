@@ -907,12 +907,11 @@ tdc_status plan_layer(tdc_conv_plan_s *p, const float *core, const float *u_in, 
     g.D1s = D1s; g.D2s = D2s; g.N3p = N3p;
     {   // taps along N (K = 3, D2s = 32): 1 acc1 + 1 acc2 of 6*D2s columns + 2 acc3
         const char *ev = std::getenv("TDC_LAYER_TN");  // A/B knob: 0 disables
-        // opt-in (TDC_LAYER_TN=1): measured 2x slower on the 56x56 layer
-        g.tn = K == 3 && D2s == 32 && 4 * D1s + 6 * D2s + 2 * N3p <= 512 && ev && ev[0] == '1';
+        g.tn = K == 3 && D2s == 32 && 4 * D1s + 8 * D2s + 2 * N3p <= 512 && !(ev && ev[0] == '0');
         const char *e3 = std::getenv("TDC_LAYER_NCAT3");  // A/B knob
         g.ncat3 = e3 ? (e3[0] == '1') : 1;
     }
-    const int tcols = g.tn ? 4 * D1s + 6 * D2s + 2 * N3p : 4 * D1s + 4 * D2s + (g.ncat3 ? 4 : 2) * N3p;
+    const int tcols = g.tn ? 4 * D1s + 8 * D2s + 2 * N3p : 4 * D1s + 4 * D2s + (g.ncat3 ? 4 : 2) * N3p;
     if (tcols > 512) return TDC_OK;
     g.tmem_cols = 32;
     while (g.tmem_cols < tcols) g.tmem_cols *= 2;
@@ -957,10 +956,11 @@ tdc_status plan_layer(tdc_conv_plan_s *p, const float *core, const float *u_in, 
                     uint16_t hi, lo;
                     split(core[(((size_t)q * D1 + a) * K + r) * K + t], &hi, &lo);
                     const int tap = r * K + t, kc = a / 32, pl = (a % 32) / 8, e8 = a % 8;
-                    if (g.tn) {  // [kc][r][plane][rows: hi (t, q) = t*D2s + q | lo 3*D2s + t*D2s + q][8]
+                    if (g.tn) {  // [kc][r][plane][rows: C(r,0) lo | C(r,0) hi | C(r,1) hi | C(r,1) lo | C(r,2) hi | lo][8]
+                        static const int hi_grp[3] = {1, 2, 4}, lo_grp[3] = {0, 3, 5};
                         const size_t base = (((size_t)kc * K + r) * 4 + pl) * 6 * D2s;
-                        w2[(base + t * D2s + q) * 8 + e8] = hi;
-                        w2[(base + 3 * D2s + t * D2s + q) * 8 + e8] = lo;
+                        w2[(base + hi_grp[t] * D2s + q) * 8 + e8] = hi;
+                        w2[(base + lo_grp[t] * D2s + q) * 8 + e8] = lo;
                     } else {     // [kc][tap][plane][row: hi q | lo D2s + q][8]
                         const size_t base = (((size_t)kc * KK + tap) * 4 + pl) * 2 * D2s;
                         w2[(base + q) * 8 + e8] = hi;
@@ -1543,7 +1543,7 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
         info->launches_per_forward = 1 + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
         info->tile_h = g.R;
         info->tile_w = g.Wo;
-        info->threads_per_cta = 608;
+        info->threads_per_cta = 640;
         info->smem_bytes_per_cta = tdc::bf_layer_smem_bytes(g);
         info->ctas_per_image = g.T;  // tiles per image (persistent grid)
         info->bn_stage1 = g.D1s;

@@ -33,10 +33,11 @@
 // row after a window (its "guard") is read only by the junk columns/rows of the
 // tile, so the next tile may overwrite it while the MMAs run.
 //
-// Warp roles (19 warps, one CTA per SM):
+// Warp roles (20 warps, one CTA per SM):
 //   0 producer (weights once, then X blocks by TMA)   1 MMA issue of the core (stage 2)
 //   2-5 epilogue 1   6-9 epilogue 2   10-13 epilogue 3   14-17 converters
-//   18 MMA issue of stages 1 and 3 (separate thread: their waits never stall the core stream)
+//   18 / 19 MMA issue of stage 1 / stage 3 -- one issuing thread per stage, so no stage's
+//   hand-off waits ever hold back another stage's MMAs
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -75,8 +76,9 @@ extern "C" int tdc_debug_layer_timeline(unsigned long long *host, int n, int cta
 #define LKNOB(bit) 0
 #endif
 
-constexpr int kLayerThreads = 608;  // 19 warps
-constexpr int kS13Warp = 18;        // stage-1 / stage-3 MMA issue
+constexpr int kLayerThreads = 640;  // 20 warps
+constexpr int kS1Warp = 18;         // stage-1 MMA issue
+constexpr int kS3Warp = 19;         // stage-3 MMA issue
 #if defined(TDC_DEBUG_KNOBS) || defined(TDC_TIMELINE)
 #define S3_FIRST LKNOB(512)
 #else
@@ -105,7 +107,7 @@ __host__ __device__ inline LayerSmem layer_smem(const BfLayerArgs &g) {
     s.band = o; o += 2u * (g.D1s / 8) * g.NRB * g.Wq * 16;
     s.z = o;    o += 2u * 2u * (g.D2s / 8) * g.ZR * 16;  // two Z buffers (hi | lo each)
     s.scr = o;  o += kEpiScr;
-    s.xch = o;  o += g.tn ? 2 * 4 * 48 * 4 : 0;  // TN: epilogue-2 row exchange
+    s.xch = o;  o += g.tn ? 2 * 4 * 16 * 4 : 0;  // TN: epilogue-2 row exchange
     s.bars = o; o += 64 * 8 + 16;
     s.total = o + 1024;  // + alignment slack of the dynamic shared memory base
     return s;
@@ -129,12 +131,14 @@ __device__ __forceinline__ TileGeo tile_geo(const BfLayerArgs &g, int k, int k0)
     return t;
 }
 
-// KT: core size K at compile time (3), or 0 = any K.  TN ("taps along N", K = 3, D2 = 32):
-// the three taps of a core row share one A operand -- B = [taps (r,0),(r,1),(r,2) hi | lo],
-// N = 6*D2 -- so stage 2 issues 12 MMAs of N = 192/96 per tile instead of 36 of N = 64/32
-// (a third of the band re-reads); the horizontal shift t of tap (r,t) is applied by
-// epilogue 2 (Z[m] = sum_t acc[m + t][tap t], lane shuffles + a 2-row exchange between
-// the epilogue warps).  Its 192-column accumulator and one acc1 buffer fit TMEM.
+// KT: core size K at compile time (3), or 0 = any K.  TN ("tap pairs along N", K = 3,
+// D2 = 32): taps (r,0) and (r,1) of a core row share one A operand -- B = [C(r,0) lo | hi |
+// C(r,1) hi | lo], N = 4*D2 -- and tap (r,2) is the row-shifted A of the same accumulator
+// block 0, so stage 2 issues 24 MMAs per tile instead of 36 (and a quarter fewer band
+// re-reads); tap (r,1)'s accumulator block is shifted by one row in epilogue 2
+// (Z[m] = blk0[m] + blk1[m + 1]: a lane shuffle plus one row exchanged between the
+// epilogue warps).  Stage 3 then drops its hi|lo concatenation so every accumulator
+// stays double-buffered in the 512 TMEM columns.
 template <int KT, bool TN>
 __global__ void __launch_bounds__(kLayerThreads, 1)
 tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs g) {
@@ -188,11 +192,11 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
     const int k0 = (int)((long long)blockIdx.x * g.num_tiles / gridDim.x);
     const int k1 = (int)((long long)(blockIdx.x + 1) * g.num_tiles / gridDim.x);
     const int nt = k1 - k0;
-    // TN: acc2 is 6*D2s wide and single-buffered; stage 3 then skips the hi|lo concatenation
-    // (3 MMAs into N3p columns instead of 2 into 2*N3p) so both acc1 and acc3 stay double-buffered
-    constexpr int NA1 = 2, NA2 = TN ? 1 : 2;  // acc1 / acc2 buffers
+    // TN: acc2 is 4*D2s wide (two tap blocks x [hi part | lo part]); stage 3 then skips the hi|lo
+    // concatenation (3 MMAs into N3p columns instead of 2 into 2*N3p) to stay within 512 columns
+    constexpr int NA1 = 2, NA2 = 2;     // acc1 / acc2 buffers
     const bool s3cat = !TN && g.ncat3;  // stage 3 with [hi | lo] U_out along N (2 MMAs, 2*N3p columns)
-    const uint32_t acc1_cols = 2 * g.D1s, acc2_cols = (TN ? 6 : 2) * g.D2s, acc3_cols = (s3cat ? 2 : 1) * g.N3p;
+    const uint32_t acc1_cols = 2 * g.D1s, acc2_cols = (TN ? 4 : 2) * g.D2s, acc3_cols = (s3cat ? 2 : 1) * g.N3p;
     const uint32_t acc2_base = NA1 * acc1_cols, acc3_base = acc2_base + NA2 * acc2_cols;
     const uint32_t plane_stride = (uint32_t)g.NRB * g.Wq * 16;   // bytes between band planes
     const uint32_t band_half = (uint32_t)(g.D1s / 8) * plane_stride;  // hi -> lo
@@ -256,7 +260,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
                 }
             }
         }
-    } else if (warp == 1 || warp == kS13Warp) {  // ============================ MMA issue
+    } else if (warp == 1 || warp == kS1Warp || warp == kS3Warp) {  // ============== MMA issue
         const uint32_t id1 = idesc_bf16(128, 2 * g.D1s), id1h = idesc_bf16(128, g.D1s);
         const uint32_t id2 = idesc_bf16(128, 2 * g.D2s), id2h = idesc_bf16(128, g.D2s);
         const uint32_t id3 = idesc_bf16(128, 2 * g.N3p), id3h = idesc_bf16(128, g.N3p);
@@ -265,7 +269,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
         const uint64_t dband = sdesc_kmajor_none(smem_u32(smem + L.band), plane_stride, 128);
         const uint64_t dw2 = sdesc_kmajor_none(smem_u32(smem + L.w2), 2 * g.D2s * 16, 128);
         const uint64_t dw2tn = sdesc_kmajor_none(smem_u32(smem + L.w2), 6 * g.D2s * 16, 128);
-        const uint32_t id2tn = idesc_bf16(128, 6 * g.D2s), id2tnh = idesc_bf16(128, 3 * g.D2s);
+        const uint32_t id2tn = idesc_bf16(128, 4 * g.D2s), id2tnh = idesc_bf16(128, 2 * g.D2s);
         const uint64_t dz = sdesc_kmajor_none(smem_u32(smem + L.z), g.ZR * 16, 128);
         const uint64_t dw3 = sdesc_kmajor_none(smem_u32(smem + L.w3), 2 * g.N3p * 16, 128);
         const uint32_t w1_chunk = (uint32_t)2 * g.D1s * 128;
@@ -315,6 +319,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
             if (TN) {
                 const uint32_t wq = (uint32_t)g.Wq, p2a = (2 * plane_stride) >> 4, lo_a = band_half >> 4;
                 const uint32_t wr = (4 * 6 * g.D2s * 16) >> 4, p2b = (2 * 6 * g.D2s * 16) >> 4;  // per row r / K16
+                const uint32_t rows16 = ((uint32_t)g.D2s * 16) >> 4;  // one D2s-row group of B
                 for (int kc = 0; kc < (LKNOB(16) ? 0 : kc2); ++kc) {
                     const uint64_t ak = arow + (uint32_t)kc * ((4 * plane_stride) >> 4);
                     const uint64_t bk = dw2tn + (uint32_t)kc * 3 * wr;
@@ -324,8 +329,13 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
 #pragma unroll
                             for (int j = 0; j < 2; ++j) {
                                 const uint64_t aj = ak + r * wq + j * p2a, bj = bk + r * wr + j * p2b;
-                                mma_bf16(d, aj, bj, id2tn, (kc > 0) || r || j);  // hi * [3 taps hi | 3 taps lo]
-                                mma_bf16(d, aj + lo_a, bj, id2tnh, 1);           // lo * [3 taps hi]
+                                // taps (r,0),(r,1): hi x [C0 lo | C0 hi | C1 hi | C1 lo] -> cols [0, 4*D2)
+                                mma_bf16(d, aj, bj, id2tn, (kc > 0) || r || j);
+                                // lo x [C0 hi | C1 hi] -> cols [D2, 3*D2) (block 0 group 1, block 1 group 0)
+                                mma_bf16(d + g.D2s, aj + lo_a, bj + rows16, id2tnh, 1);
+                                // tap (r,2): A shifted by 2 rows, into block 0: hi x [C2 hi | C2 lo], lo x C2 hi
+                                mma_bf16(d, aj + 2, bj + 4 * rows16, id2, 1);
+                                mma_bf16(d, aj + 2 + lo_a, bj + 4 * rows16, id2h, 1);
                             }
                     }
                     __syncwarp();
@@ -415,28 +425,17 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
                 start += g.R;
                 if (start >= (uint32_t)g.NR) start -= g.NR;
             }
-        } else {  // stage 1 of the next tile and stage 3 of the previous one, issued by a
-                  // second thread so the core stream never waits behind their hand-offs
-            if (nt > 0) {
-                const TileGeo t0 = tile_geo(g, k0, k0);
-                for (int blk = 0; blk < t0.nb; ++blk) s1_block();
-            }
+        } else if (warp == kS1Warp) {  // stage 1 runs ahead (2 acc1 buffers), never behind stage 3
             for (int t = 0; t < nt; ++t) {
-                s1_tile = t + 1;
-                if (t + 1 < nt) {
-                    const int nb_next = tile_geo(g, k0 + t + 1, k0).nb;
-                    for (int blk = 0; blk < nb_next; ++blk) s1_block();
-                }
-                if (t > 0 && !S3_FIRST) {
-                    s3(t - 1);
-                    if (lane == 0) LTL(t - 1, 4);  // MMA: S3 issued
-                }
-                if (S3_FIRST && t + 1 < nt) {  // (A/B variant) S3(t) right after its Z
-                    s3(t);
-                    if (lane == 0) LTL(t, 4);
-                }
+                s1_tile = t;
+                const int nb = tile_geo(g, k0 + t, k0).nb;
+                for (int blk = 0; blk < nb; ++blk) s1_block();
             }
-            if (nt > 0) s3(nt - 1);
+        } else {  // stage 3: waits only for epilogue 2's Z
+            for (int t = 0; t < nt; ++t) {
+                s3(t);
+                if (lane == 0) LTL(t, 4);  // MMA: S3 issued
+            }
         }
     } else if (warp < 6) {  // ========================= epilogue 1: acc1 -> X' band ring
         const int q = warp & 3;  // TMEM lane quarter this warp may access = warp % 4
@@ -504,7 +503,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
         const int r = q * 32 + lane;
         const bool zrow = r < g.ZR;  // Z planes hold ZR rows (rows beyond: junk MMA rows)
-        float *xbuf = reinterpret_cast<float *>(smem + L.xch);  // TN: [chunk 2][quarter 4][3][16]
+        float *xbuf = reinterpret_cast<float *>(smem + L.xch);  // TN: [chunk 2][quarter 4][16]
         for (int t = 0; t < nt; ++t) {
             const uint32_t sb = t & 1, sph = (t >> 1) & 1;
             const uint32_t ab2 = NA2 == 1 ? 0u : sb, aph2 = NA2 == 1 ? (t & 1) : sph;
@@ -512,55 +511,47 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
             ewait(&a2_full[ab2], aph2);
             tc_fence_after();
             if (threadIdx.x == 192) LTL(t, 7);  // E2: acc2 full seen
-            if (TN) {  // Z[m] = sum_t (hi + lo part of tap t)[m + t]  (D2s = 32: two 16-column chunks)
-                const uint32_t a2 = tmem + lane_base + acc2_base;
-                const uint32_t lo3 = 3 * g.D2s;
+            if (TN) {  // Z[m] = blk0[m] + blk1[m + 1], each block = group 0 + group 1 (D2s = 32)
+                const uint32_t a2 = tmem + lane_base + acc2_base + ab2 * acc2_cols;
                 uint4 h0[4], l0[4];
 #pragma unroll
                 for (int ch = 0; ch < 2; ++ch) {
                     const int c = ch * 16;
-                    float p[3][16];
-#pragma unroll
-                    for (int tp = 0; tp < 3; ++tp) {
-                        uint32_t r0[16], r1[16];
-                        tmem_ld_32x32b_x16(a2 + tp * g.D2s + c, r0);
-                        tmem_ld_32x32b_x16(a2 + lo3 + tp * g.D2s + c, r1);
+                    float p0[16], p1[16];
+                    {
+                        uint32_t r0[16], r1[16], r2[16], r3[16];
+                        tmem_ld_32x32b_x16(a2 + c, r0);
+                        tmem_ld_32x32b_x16(a2 + g.D2s + c, r1);
+                        tmem_ld_32x32b_x16(a2 + 2 * g.D2s + c, r2);
+                        tmem_ld_32x32b_x16(a2 + 3 * g.D2s + c, r3);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) p[tp][jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
+                        for (int jj = 0; jj < 16; ++jj) {
+                            p0[jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
+                            p1[jj] = __uint_as_float(r2[jj]) + __uint_as_float(r3[jj]);
+                        }
                     }
-                    if (threadIdx.x == 192) LTL(t, 16 + ch);  // E2 (TN): chunk ch loaded
-                    if (ch == 1) {  // every TMEM read of this tile done: S2(t+1) may overwrite acc2
+                    if (ch == 1) {  // every TMEM read of this tile done: S2(t+2) may overwrite acc2
                         tc_fence_before();
-                        mbar_arrive_relaxed(&a2_empty[0]);
+                        mbar_arrive_relaxed(&a2_empty[ab2]);
                     }
-                    // rows m+1, m+2 of the last lanes live in the next lane quarter: publish ours
-                    float *mine = xbuf + (ch * 4 + q) * 48, *next = xbuf + (ch * 4 + ((q + 1) & 3)) * 48;
+                    // row m+1 of lane 31 lives in the next lane quarter (lane 0): exchange it
+                    float *mine = xbuf + (ch * 4 + q) * 16, *next = xbuf + (ch * 4 + ((q + 1) & 3)) * 16;
                     if (lane == 0)
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) {
-                            mine[jj] = p[1][jj];
-                            mine[16 + jj] = p[2][jj];
-                        }
-                    if (lane == 1)
-#pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) mine[32 + jj] = p[2][jj];
+                        for (int jj = 0; jj < 16; ++jj) mine[jj] = p1[jj];
                     asm volatile("bar.sync 3, 128;" ::: "memory");
-                    if (threadIdx.x == 192) LTL(t, 18 + ch);  // E2 (TN): exchange done
                     float v[16];
 #pragma unroll
                     for (int jj = 0; jj < 16; ++jj) {
-                        float s1 = __shfl_down_sync(0xffffffffu, p[1][jj], 1);
-                        float s2 = __shfl_down_sync(0xffffffffu, p[2][jj], 2);
+                        float s1 = __shfl_down_sync(0xffffffffu, p1[jj], 1);
                         if (lane == 31) s1 = next[jj];
-                        if (lane >= 30) s2 = next[16 + (lane - 30) * 16 + jj];
-                        v[jj] = p[0][jj] + s1 + s2;
+                        v[jj] = p0[jj] + s1;
                     }
                     split_bf16x8(v, h0[2 * ch], l0[2 * ch]);
                     split_bf16x8(v + 8, h0[2 * ch + 1], l0[2 * ch + 1]);
                 }
                 ewait(&z_empty[sb], sph ^ 1);  // S3 two tiles back has read this Z buffer
-                if (threadIdx.x == 192) LTL(t, 12);
                 if (!LKNOB(8) && zrow)
 #pragma unroll
                     for (int pl = 0; pl < 4; ++pl) {
