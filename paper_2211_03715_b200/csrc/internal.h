@@ -206,6 +206,30 @@ struct BfLayerArgs {
 };
 int bf_layer_smem_bytes(const BfLayerArgs &g);
 cudaError_t bf_layer_launch(const CUtensorMap &mapX, const BfLayerArgs &g, int grid, cudaStream_t st);
+// IEEE-fp32 3-launch path on CUDA cores (tkd_sgemm.cu): C[out(m)] = sum_tap A[m + a_off[tap]] . B[tap]
+struct SgemmArgs {
+    const float *A;           // rows of K (padded to 8) fp32, row stride lda
+    long long lda;
+    int M, K, taps;           // output rows, K per tap (multiple of 8), taps
+    int kmask, K_valid;       // 1: columns >= K_valid of A are read as 0 (stage 1, C % 8 != 0)
+    long long a_off[kMaxTaps];// per-tap row offset (phase plane + tap shift)
+    const float *B;           // [taps][K][ldb] fp32, zero-padded to the N tiles
+    int ldb, N;
+    float *C;                 // output rows, stride ldc; columns >= N untouched
+    int ldc;
+    const float *bias;        // [N] or null
+    int remap;                // 0 identity, 1 input pixel -> phase grid row, 2 phase grid -> compact
+    int H, W, s, p, Hq, Wq, Ho, Wo;
+    long long phase_rows;
+    int phase_idx[kMaxTaps];  // (py*s+px) -> compact phase or -1
+    int tile;                 // 0: 128x128, 1: 128x64, 2: 256x32
+    int ksplit;               // > 1: K loop split over grid.z, partials in `part`, reduce kernel
+    float *part;
+};
+cudaError_t sgemm_taps_launch(const SgemmArgs &g, cudaStream_t st);
+int sgemm_pick_tile(long long M, int N, int num_sms);
+int sgemm_pick_ksplit(long long M, int N, int K, int taps, int tile, int num_sms);
+long long sgemm_part_floats(long long M, int N, int tile, int ksplit);
 // NCHW <-> NHWC for the NCHW API layout.
 cudaError_t nchw_to_nhwc(const float *src, float *dst, int B, int C, int H, int W,
                          cudaStream_t st);

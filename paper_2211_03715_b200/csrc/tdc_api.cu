@@ -143,6 +143,10 @@ struct tdc_conv_plan_s {
     const float *tc_last_x = nullptr;
     int tc_last_x_batch = 0;
     int max_smem = 0;
+    // IEEE-fp32 three-launch CUDA-core path (variant 6, tkd_sgemm.cu)
+    tdc::SgemmArgs sg[3];
+    float *d_sg = nullptr;         // B1 | B2 | B3 | bias | X' phase grid | Z
+    float *d_sg_part = nullptr;    // split-K partial tiles
     // single-launch 3xBF16 layer (variant 5, tkd_layer.cu)
     tdc::BfLayerArgs bl;
     CUtensorMap lmapX;
@@ -858,6 +862,115 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
     return TDC_OK;
 }
 
+// Plan the IEEE-fp32 path (variant 6): three register-blocked GEMM-with-taps launches on
+// CUDA cores over the whole GPU (tkd_sgemm.cu).  Needs 16-byte pixel rows (C % 4 == 0);
+// otherwise the single-kernel SIMT variant stays.
+tdc_status plan_sgemm(tdc_conv_plan_s *p, const float *core, const float *u_in, const float *u_out,
+                      const float *bias, bool *used) {
+    *used = false;
+    const tdc_conv_desc &d = p->desc;
+    const int C = d.c_in, N = d.c_out, D1 = d.rank_in, D2 = d.rank_out, K = d.kernel;
+    const int s = d.stride, pad = d.pad, H = d.height, W = d.width, Bm = d.batch;
+    const int Ho = p->dims.Ho, Wo = p->dims.Wo, KK = K * K;
+    {
+        const char *ev = std::getenv("TDC_NO_SGEMM");
+        if (ev && ev[0] && ev[0] != '0') return TDC_OK;
+    }
+    if (C % 4 || KK > tdc::kMaxTaps) return TDC_OK;
+    const int K1 = round_up(C, 8), D1p = round_up(D1, 8), D2p = round_up(D2, 8);
+    const int ldb1 = round_up(D1p, 128), ldb2 = round_up(D2, 128), ldb3 = round_up(N, 128);
+    const int Hq = div_up(H + 2 * pad, s), Wq = div_up(W + 2 * pad, s);
+    const long long phase_rows = (long long)Bm * Hq * Wq;
+    const long long M1 = (long long)Bm * H * W, M2 = phase_rows, M3 = (long long)Bm * Ho * Wo;
+    std::vector<int> idx_of((size_t)s * s, -1);
+    int phase_of[tdc::kMaxTaps], nphase = 0;
+    for (int r = 0; r < K; ++r)
+        for (int t = 0; t < K; ++t) {
+            const int ph = (r % s) * s + (t % s);
+            if (idx_of[ph] < 0) idx_of[ph] = nphase++;
+            phase_of[r * K + t] = idx_of[ph];
+        }
+    if (s * s > tdc::kMaxTaps || nphase * M2 + 1024 > (1LL << 31) || M1 > (1LL << 31) - 256) return TDC_OK;
+    const long long maxoff = (long long)((K - 1) / s) * Wq + (K - 1) / s;
+    const long long xg_rows = nphase * phase_rows + maxoff + 512;
+    const size_t nb1 = (size_t)K1 * ldb1, nb2 = (size_t)KK * D1p * ldb2, nb3 = (size_t)D2p * ldb3,
+                 nbias = round_up(N, 4), nxg = (size_t)xg_rows * D1p, nz = (size_t)(M3 + 512) * D2p;
+    // ---- a0: weight re-layout (CRSN idea), zero-padded to the tiles ----
+    std::vector<float> hw(nb1 + nb2 + nb3 + nbias, 0.f);
+    float *b1 = hw.data(), *b2 = b1 + nb1, *b3 = b2 + nb2, *bb = b3 + nb3;
+    for (int c = 0; c < C; ++c)
+        for (int a = 0; a < D1; ++a) b1[(size_t)c * ldb1 + a] = u_in[(size_t)c * D1 + a];
+    for (int q = 0; q < D2; ++q)
+        for (int a = 0; a < D1; ++a)
+            for (int r = 0; r < K; ++r)
+                for (int t = 0; t < K; ++t)
+                    b2[((size_t)(r * K + t) * D1p + a) * ldb2 + q] = core[(((size_t)q * D1 + a) * K + r) * K + t];
+    for (int n = 0; n < N; ++n)
+        for (int q = 0; q < D2; ++q) b3[(size_t)q * ldb3 + n] = u_out[(size_t)n * D2 + q];
+    if (bias)
+        for (int n = 0; n < N; ++n) bb[n] = bias[n];
+    const size_t wbytes = hw.size() * sizeof(float), tot = wbytes + (nxg + nz) * sizeof(float);
+    cudaError_t e = cudaMalloc(&p->d_sg, tot);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(fp32 weights + workspace)");
+    e = cudaMemcpy(p->d_sg, hw.data(), wbytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(p->d_sg + hw.size(), 0, (nxg + nz) * sizeof(float));  // zero borders / pads
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(fp32 weights)");
+    p->weight_bytes += wbytes;
+    p->tc_ws_bytes += (nxg + nz) * sizeof(float);
+    float *dB1 = p->d_sg, *dB2 = dB1 + nb1, *dB3 = dB2 + nb2, *dbias = dB3 + nb3, *xg = dbias + nbias, *z = xg + nxg;
+    for (auto &a : p->sg) {
+        std::memset(&a, 0, sizeof a);
+        a.H = H; a.W = W; a.s = s; a.p = pad; a.Hq = Hq; a.Wq = Wq; a.Ho = Ho; a.Wo = Wo;
+        a.phase_rows = phase_rows;
+        for (int i = 0; i < tdc::kMaxTaps; ++i) a.phase_idx[i] = i < s * s ? idx_of[i] : -1;
+        a.taps = 1;
+    }
+    tdc::SgemmArgs &s1 = p->sg[0], &s2 = p->sg[1], &s3 = p->sg[2];
+    s1.lda = C; s1.M = (int)M1; s1.K = K1; s1.kmask = K1 != C; s1.K_valid = C; s1.B = dB1; s1.ldb = ldb1;
+    s1.N = D1p; s1.C = xg; s1.ldc = D1p; s1.remap = 1;
+    s2.A = xg; s2.lda = D1p; s2.M = (int)M2; s2.K = D1p; s2.taps = KK; s2.B = dB2; s2.ldb = ldb2;
+    s2.N = D2; s2.C = z; s2.ldc = D2p; s2.remap = 2;
+    for (int r = 0; r < K; ++r)
+        for (int t = 0; t < K; ++t)
+            s2.a_off[r * K + t] = (long long)phase_of[r * K + t] * phase_rows + (r / s) * Wq + t / s;
+    s3.A = z; s3.lda = D2p; s3.M = (int)M3; s3.K = D2p; s3.B = dB3; s3.ldb = ldb3; s3.N = N; s3.ldc = N;
+    s3.bias = bias ? dbias : nullptr; s3.remap = 0;
+    // tiles and split-K pieces for the plan's batch (a smaller batch keeps them: bit-identical
+    // results for a partial batch); one partial workspace shared by the three stages
+    long long part = 0;
+    for (auto &a : p->sg) {
+        a.tile = tdc::sgemm_pick_tile(a.M, a.N, p->num_sms);
+        a.ksplit = tdc::sgemm_pick_ksplit(a.M, a.N, a.K, a.taps, a.tile, p->num_sms);
+        part = std::max(part, tdc::sgemm_part_floats(a.M, a.N, a.tile, a.ksplit));
+    }
+    if (part) {
+        float *pw = nullptr;
+        e = cudaMalloc(&pw, part * sizeof(float));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(fp32 split-K workspace)");
+        p->d_sg_part = pw;
+        p->tc_ws_bytes += part * sizeof(float);
+        for (auto &a : p->sg) a.part = pw;
+    }
+    p->variant = 6;
+    *used = true;
+    return TDC_OK;
+}
+
+tdc_status forward_sgemm(tdc_conv_plan_s *p, const float *x, float *y, int batch, cudaStream_t st) {
+    const tdc::LayerDims &d = p->dims;
+    tdc::SgemmArgs a1 = p->sg[0], a2 = p->sg[1], a3 = p->sg[2];
+    a1.A = x;
+    a1.M = batch * d.H * d.W;
+    a2.M = batch * a2.Hq * a2.Wq;
+    a3.M = batch * d.Ho * d.Wo;
+    a3.C = y;
+    cudaError_t e = tdc::sgemm_taps_launch(a1, st);
+    if (e == cudaSuccess) e = tdc::sgemm_taps_launch(a2, st);
+    if (e == cudaSuccess) e = tdc::sgemm_taps_launch(a3, st);
+    if (e != cudaSuccess) return cuda_fail(e, "fp32 CUDA-core GEMM launch");
+    return TDC_OK;
+}
+
 // Plan the single-launch 3xBF16 layer kernel (variant 5): stage 1, the core and stage 3
 // in one persistent kernel with X' and Z on chip.  Used when the
 // layer has stride 1, its ranks / output channels fit one tile (<= 128, hi|lo
@@ -1445,6 +1558,14 @@ tdc_status tdc_conv_plan_ex(const tdc_conv_desc *desc, const float *core, const 
             return s;
         }
     }
+    if (d.math == TDC_MATH_FP32) {
+        bool sg = false;
+        s = plan_sgemm(p, core, u_in, u_out, bias, &sg);
+        if (s != TDC_OK) {
+            tdc_conv_plan_destroy(p);
+            return s;
+        }
+    }
     bool bf = false;
     if (d.math == TDC_MATH_3XBF16) {
         s = plan_layer(p, core, u_in, u_out, bias, &bf);
@@ -1491,7 +1612,7 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
     info->variant = p->variant;
     const bool tc = p->variant == 2 || p->variant == 4, fz = p->variant == 3;
     std::snprintf(info->variant_name, sizeof info->variant_name, "%s",
-                  p->variant == 5 ? "layer_3xbf16_fused" :
+                  p->variant == 6 ? "simt3_fp32" : p->variant == 5 ? "layer_3xbf16_fused" :
                   p->variant == 4 ? (p->fuse3 ? "tc2_3xbf16_core3" : "tc3_3xbf16_band") : fz ? "fused_tc_tf32"
                      : tc ? (p->split ? (p->tc_core ? "tc3_3xtf32_band" : "tc3_3xtf32")
                                       : (p->tc_core ? "tc3_tf32_band" : "tc3_tf32"))
@@ -1538,6 +1659,12 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
         info->ctas_per_image = p->fargs.tiles_per_img;  // tiles per image (persistent grid)
         info->concurrent_forward = p->desc.layout == TDC_LAYOUT_NHWC ? 1 : 0;
     }
+    if (p->variant == 6) {
+        info->launches_per_forward = 3 + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
+        info->concurrent_forward = 0;
+        info->threads_per_cta = 256;
+        info->ctas_per_image = 0;
+    }
     if (p->variant == 5) {
         const tdc::BfLayerArgs &g = p->bl;
         info->launches_per_forward = 1 + (p->desc.layout == TDC_LAYOUT_NCHW ? 2 : 0);
@@ -1575,6 +1702,7 @@ tdc_status tdc_conv_forward(tdc_conv_plan_t p, const float *x, float *y, int32_t
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
     if (p->desc.layout == TDC_LAYOUT_NHWC) {
+        if (p->variant == 6) return forward_sgemm(p, x, y, batch, st);
         if (p->variant == 5) return forward_layer(p, x, y, batch, st);
         if (p->variant == 4) return forward_bf16(p, x, y, batch, st);
         if (p->variant == 3) return forward_fused(p, x, y, batch, st);
@@ -1585,7 +1713,10 @@ tdc_status tdc_conv_forward(tdc_conv_plan_t p, const float *x, float *y, int32_t
     }
     e = tdc::nchw_to_nhwc(x, p->d_ws_in, batch, d.C, d.H, d.W, st);
     if (e != cudaSuccess) return cuda_fail(e, "NCHW->NHWC launch");
-    if (p->variant == 5) {
+    if (p->variant == 6) {
+        tdc_status s = forward_sgemm(p, p->d_ws_in, p->d_ws_out, batch, st);
+        if (s != TDC_OK) return s;
+    } else if (p->variant == 5) {
         tdc_status s = forward_layer(p, p->d_ws_in, p->d_ws_out, batch, st);
         if (s != TDC_OK) return s;
     } else if (p->variant == 4) {
@@ -1795,6 +1926,8 @@ tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t p) {
     cudaFree(p->d_xg);
     cudaFree(p->d_z);
     cudaFree(p->d_gs);
+    cudaFree(p->d_sg);
+    cudaFree(p->d_sg_part);
     delete p;
     return TDC_OK;
 }

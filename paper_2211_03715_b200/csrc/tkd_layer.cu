@@ -158,6 +158,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef TDC_TIMELINE
     const bool tl_on = (int)blockIdx.x == *(volatile int *)&g_tdc_ltl_cta;  // read once
+    if (threadIdx.x == 0) LTL(0, 21);  // kernel entry
 #endif
     if (threadIdx.x == 0) {
         for (int i = 0; i < g.XS; ++i) {
@@ -187,6 +188,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
     tc_fence_after();
     pdl_launch_dependents();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) LTL(0, 22);  // setup done (barriers, TMEM)
 
     // contiguous tile range of this CTA (sliding band within it)
     const int k0 = (int)((long long)blockIdx.x * g.num_tiles / gridDim.x);
@@ -279,6 +281,7 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
         Ring xr(g.XS);
         uint32_t ublk = 0;  // stage-1 block counter (acc1 buffer = ublk & 1)
         mbar_wait(w_full, 0);
+        if (warp == kS1Warp && lane == 0) LTL(0, 23);  // weights landed
         int s1_tile = 0;  // (timeline) local tile of the next stage-1 block
         auto s1_block = [&]() {
             const uint32_t ab = NA1 == 1 ? 0u : (ublk & 1), aph = NA1 == 1 ? (ublk & 1) : ((ublk >> 1) & 1);

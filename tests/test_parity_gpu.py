@@ -99,8 +99,11 @@ def test_ragged_and_edge_shapes(env, shape, math):
     got, info = run_layer(env, shape, d, "nhwc", math)
     # the variant that ran is asserted, so no case silently exercises another kernel:
     # TMA needs 16-byte pixel rows (C % 4 == 0); otherwise every mode uses the FP32 kernel
-    if math == "fp32" or shape.C % 4:
+    if shape.C % 4:
         assert info.variant_name == "fused_simt_fp32", info.variant_name
+    elif math == "fp32":  # CUDA-core three-launch GEMM-with-taps path (s*s phases <= 49)
+        assert info.variant_name == ("simt3_fp32" if shape.stride ** 2 <= 49 else "fused_simt_fp32"), \
+            info.variant_name
     elif math == "3xbf16":  # fp32-grade split; 3xTF32 where the 3xBF16 band does not fit (stride 3: 9 phases)
         assert "3xbf16" in info.variant_name or "3xtf32" in info.variant_name, info.variant_name
     else:
@@ -130,6 +133,24 @@ def test_r18_shapes_batch32_sampled(env, shape, count, math):
     vals = np.array([got[p] for p in pts], dtype=np.float64)
     scale = np.max(np.abs(ref))
     assert np.max(np.abs(vals - ref)) / scale <= TOL[math]
+
+
+@pytest.mark.parametrize("shape,count", synth.R18_SHAPES, ids=[s.name for s, _ in synth.R18_SHAPES])
+def test_fp32_variant_is_the_cuda_core_gemm(env, shape, count):
+    torch, tdc = env
+    plan = tdc.ConvPlan(shape.with_batch(32), synth.make_layer(shape), math=tdc.TDC_MATH_FP32)
+    assert plan.info().variant_name == "simt3_fp32" and plan.info().launches_per_forward == 3
+    plan.close()
+
+
+def test_fp32_old_single_kernel_path_still_matches(env, monkeypatch):
+    """TDC_NO_SGEMM keeps the single-kernel SIMT variant reachable (C % 4 != 0 uses it)."""
+    monkeypatch.setenv("TDC_NO_SGEMM", "1")
+    s = LayerShape(2, 32, 24, 10, 9, 8, 12, 3, 2, 1)
+    d = synth.make_layer(s, seed=3, bias=True)
+    got, info = run_layer(env, s, d, "nhwc", "fp32")
+    assert info.variant_name == "fused_simt_fp32"
+    assert err(got, ref_of(s, d)) <= TOL["fp32"]
 
 
 @pytest.mark.parametrize("shape,count", synth.R18_SHAPES, ids=[s.name for s, _ in synth.R18_SHAPES])
