@@ -9,6 +9,9 @@ from paper_2211_03715_b200 import tdc
 idx = int(sys.argv[1])
 B = int(os.environ.get("LAYER_B", "32"))
 s = synth.R18_SHAPES[idx][0].with_batch(B)
+if os.environ.get("LAYER_HW"):
+    hw = int(os.environ["LAYER_HW"])
+    s = synth.LayerShape(B, s.C, s.N, hw, hw, s.D1, s.D2, s.K, s.stride, s.pad, f"{s.name}_{hw}x{hw}")
 d = synth.make_layer(s)
 xs = [torch.from_numpy(synth.nchw_to_nhwc(d["x"])).cuda() for _ in range(4)]
 ys = [torch.empty((s.B, s.Ho, s.Wo, s.N), device="cuda") for _ in range(4)]

@@ -7,7 +7,10 @@ import synth
 from paper_2211_03715_b200 import tdc
 idx = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 cta = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-shape = synth.R18_SHAPES[idx][0].with_batch(32)
+shape = synth.R18_SHAPES[idx][0].with_batch(int(os.environ.get("LAYER_B", "32")))
+if os.environ.get("LAYER_HW"):  # e.g. LAYER_HW=8 -> the 8x8 variant of the shape
+    hw = int(os.environ["LAYER_HW"])
+    shape = synth.LayerShape(shape.B, shape.C, shape.N, hw, hw, shape.D1, shape.D2, shape.K, shape.stride, shape.pad)
 d = synth.make_layer(shape)
 plan = tdc.ConvPlan(shape, d, math=tdc.TDC_MATH_3XBF16)
 print(plan.info().variant_name)
@@ -22,7 +25,7 @@ torch.cuda.synchronize()
 tdc.lib.tdc_debug_layer_timeline(buf, n, cta)
 a = np.array(buf, dtype=np.int64).reshape(32, 24)
 names = ["prodX", "convD", "S1iss", "S2iss", "S3iss", "E1acc", "E1rdy", "E2acc", "E2done", "E3acc", "E3done",
-         "S2wait", "E2zfree", "S1start", "S1acc1", "S1conv", "E2ld0", "E2ld1", "E2xc0", "E2xc1"]
+         "S2wait", "E2zfree", "S1start", "S1acc1", "S1conv", "E2ld0", "E2ld1", "E2xc0", "E2xc1", "entry", "setup", "wloaded"]
 rows = a[a[:, 5] > 0]
 t0 = a[a > 0].min()
 print("tile " + " ".join(f"{nm:>7s}" for nm in names))
