@@ -222,13 +222,17 @@ struct SgemmArgs {
     int H, W, s, p, Hq, Wq, Ho, Wo;
     long long phase_rows;
     int phase_idx[kMaxTaps];  // (py*s+px) -> compact phase or -1
-    int tile;                 // 0: 128x128, 1: 128x64, 2: 256x32
-    int ksplit;               // > 1: K loop split over grid.z, partials in `part`, reduce kernel
+    int tile;                 // 0: 64x128, 1: 128x64, 2: 256x32 (8x8 per thread, 128 threads)
+    int ksplit;               // > 1: K split over grid.z, partial tiles in `part`, reduce kernel
     float *part;
+    int ctas;                 // co-resident CTAs of the tile shape (split-K choice)
 };
 cudaError_t sgemm_taps_launch(const SgemmArgs &g, cudaStream_t st);
+cudaError_t sgemm_prepare();
 int sgemm_pick_tile(long long M, int N, int num_sms);
-int sgemm_pick_ksplit(long long M, int N, int K, int taps, int tile, int num_sms);
+int sgemm_pick_ksplit(long long M, int N, int K, int taps, int tile, int ctas);
+long long sgemm_tiles(long long M, int N, int tile);
+int sgemm_ctas(int tile, int num_sms);
 long long sgemm_part_floats(long long M, int N, int tile, int ksplit);
 // NCHW <-> NHWC for the NCHW API layout.
 cudaError_t nchw_to_nhwc(const float *src, float *dst, int B, int C, int H, int W,

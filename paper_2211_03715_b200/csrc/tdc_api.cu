@@ -877,7 +877,7 @@ tdc_status plan_sgemm(tdc_conv_plan_s *p, const float *core, const float *u_in, 
         if (ev && ev[0] && ev[0] != '0') return TDC_OK;
     }
     if (C % 4 || KK > tdc::kMaxTaps) return TDC_OK;
-    const int K1 = round_up(C, 8), D1p = round_up(D1, 8), D2p = round_up(D2, 8);
+    const int K1 = round_up(C, 16), D1p = round_up(D1, 16), D2p = round_up(D2, 16);  // K-step 16
     const int ldb1 = round_up(D1p, 128), ldb2 = round_up(D2, 128), ldb3 = round_up(N, 128);
     const int Hq = div_up(H + 2 * pad, s), Wq = div_up(W + 2 * pad, s);
     const long long phase_rows = (long long)Bm * Hq * Wq;
@@ -910,7 +910,9 @@ tdc_status plan_sgemm(tdc_conv_plan_s *p, const float *core, const float *u_in, 
     if (bias)
         for (int n = 0; n < N; ++n) bb[n] = bias[n];
     const size_t wbytes = hw.size() * sizeof(float), tot = wbytes + (nxg + nz) * sizeof(float);
-    cudaError_t e = cudaMalloc(&p->d_sg, tot);
+    cudaError_t e = tdc::sgemm_prepare();
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fp32 GEMM)");
+    e = cudaMalloc(&p->d_sg, tot);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(fp32 weights + workspace)");
     e = cudaMemcpy(p->d_sg, hw.data(), wbytes, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(p->d_sg + hw.size(), 0, (nxg + nz) * sizeof(float));  // zero borders / pads
@@ -938,12 +940,18 @@ tdc_status plan_sgemm(tdc_conv_plan_s *p, const float *core, const float *u_in, 
     // tiles and split-K pieces for the plan's batch (a smaller batch keeps them: bit-identical
     // results for a partial batch); one partial workspace shared by the three stages
     long long part = 0;
-    for (auto &a : p->sg) {
+    const char *ev_t = std::getenv("TDC_SG_TILES"), *ev_k = std::getenv("TDC_SG_KSPLIT");  // tuning: "t1,t2,t3"
+    for (int i = 0; i < 3; ++i) {
+        tdc::SgemmArgs &a = p->sg[i];
         a.tile = tdc::sgemm_pick_tile(a.M, a.N, p->num_sms);
-        a.ksplit = tdc::sgemm_pick_ksplit(a.M, a.N, a.K, a.taps, a.tile, p->num_sms);
+        if (ev_t && (int)std::strlen(ev_t) > 2 * i && ev_t[2 * i] >= '0' && ev_t[2 * i] <= '2') a.tile = ev_t[2 * i] - '0';
+        a.ctas = tdc::sgemm_ctas(a.tile, p->num_sms);
+        a.ksplit = tdc::sgemm_pick_ksplit(a.M, a.N, a.K, a.taps, a.tile, a.ctas);
+        if (ev_k && (int)std::strlen(ev_k) > 2 * i && ev_k[2 * i] >= '1' && ev_k[2 * i] <= '8') a.ksplit = ev_k[2 * i] - '0';
+        a.ksplit = std::min(a.ksplit, std::max(1, a.taps * (a.K / 16)));
         part = std::max(part, tdc::sgemm_part_floats(a.M, a.N, a.tile, a.ksplit));
     }
-    if (part) {
+    if (part) {  // partial tiles of the split stages (one workspace, stages run in order)
         float *pw = nullptr;
         e = cudaMalloc(&pw, part * sizeof(float));
         if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(fp32 split-K workspace)");
