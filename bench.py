@@ -64,6 +64,8 @@ def parse():
                     help="issue the timed steps as individual launches instead of replaying a CUDA graph")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-b1", action="store_true", help="skip the batch-1 latency section")
+    ap.add_argument("--no-math-steps", action="store_true",
+                    help="skip re-timing the step in the other math modes (fp32, tf32, 3xtf32, 3xbf16)")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     return ap.parse_args()
 
@@ -216,7 +218,8 @@ def impl_tdc(args):
         plan = tdc.ConvPlan(s, d, layout=tdc.TDC_LAYOUT_NHWC, math=math, device=local)
         x = torch.from_numpy(synth.nchw_to_nhwc(d["x"])).cuda()
         y = torch.empty((s.B, s.Ho, s.Wo, s.N), device="cuda")
-        layers.append({"lid": lid, "shape": s, "plan": plan, "x": x, "y": y, "xnp": d["x"]})
+        layers.append({"lid": lid, "shape": s, "plan": plan, "x": x, "y": y, "xnp": d["x"],
+                       "w": {k: v for k, v in d.items() if k != "x"}})
     launches_per_step = sum(L["plan"].info().launches_per_forward for L in layers)
     torch.cuda.synchronize()
 
@@ -406,6 +409,53 @@ def impl_tdc(args):
                 "launch_us": round(plain, 2), "host_sync_us": round(statistics.median(lat), 2),
                 "bytes": rl.tkd_bytes(shape), "flops": rl.tkd_flops(shape)}
 
+    # ---- the other math modes on the same step: each layer re-planned
+    # in that mode over the same resident inputs, one step captured as a CUDA graph and
+    # replayed back to back; ms/step and algorithmic GB/s beside the headline mode's.
+    def math_step(mname, reps):
+        plans = [tdc.ConvPlan(L["shape"], L["w"], layout=tdc.TDC_LAYOUT_NHWC,
+                              math=tdc.MATH_NAMES[mname], device=local) for L in layers]
+        ys = [torch.empty_like(L["y"]) for L in layers]
+
+        def one():
+            for pl, L, yy in zip(plans, layers, ys):
+                pl.forward(L["x"], yy, stream=stream)
+
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                one()
+        torch.cuda.synchronize()
+        gm = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gm, stream=stream):
+            one()
+        with torch.cuda.stream(stream):
+            gm.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(reps):
+                gm.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        variants = sorted({pl.info().variant_name for pl in plans})
+        launches = sum(pl.info().launches_per_forward for pl in plans)
+        del gm
+        for pl in plans:
+            pl.close()
+        return {"ms_per_step": round(ms, 4), "value": round(step_bytes / (ms * 1e-3) / 1e9, 2), "unit": UNIT,
+                "launches_per_step": launches, "variants": variants, "launch": "cuda_graph_replay",
+                "timed_steps": reps}
+
+    math_steps = None
+    if not args.no_math_steps:
+        math_steps = {args.math: {"ms_per_step": round(total_ms / args.steps, 4), "value": round(value, 2),
+                                  "unit": UNIT, "headline": True}}
+        for mname in ("3xbf16", "3xtf32", "tf32", "fp32"):
+            if mname != args.math:
+                math_steps[mname] = math_step(mname, 10 if mname == "fp32" else 30)
+
     batch1 = None
     if not args.no_b1:
         batch1 = [b1_latency(synth.CONFIG1, "fp32"), b1_latency(synth.CONFIG1, args.math)]
@@ -570,6 +620,7 @@ def impl_tdc(args):
                                        "tolerance 1e-4"}[args.math],
                 "data": "synthetic", "config": config_dict(args, world),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "model": model, "batch1": batch1,
+                "math_steps": math_steps,
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": sampler.summary(), "layers": layer_rows,
                 "step_bytes": step_bytes, "step_flops": sum(rl.tkd_flops(L["shape"]) for L in layers)}
