@@ -184,6 +184,7 @@ struct BfLayerArgs {
     int NR, NRB;              // band ring rows (2R+e) and buffer rows incl. the mirror rows
     int XR, ZR;               // rows of an X staging tile / a Z plane (multiples of 8, <= 128)
     int tn;                   // 1: K = 3, D2s = 32, the 3 taps of a core row along N (tkd_layer.cu)
+    int xt;                   // 1 (with tn): X hi/lo and Z hi/lo in tensor memory, stages 1 and 3 as TS-MMAs
     int ncat3;                // 1: stage 3 as [hi | lo] along N (2 MMAs, 2*N3p accumulator columns)
     int cchunks;              // 64-channel chunks of C (TMA zero-fills channels >= C)
     int D1s, D2s, N3p;        // ranks / output channels padded to multiples of 32

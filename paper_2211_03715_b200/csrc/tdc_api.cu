@@ -1031,8 +1031,12 @@ tdc_status plan_layer(tdc_conv_plan_s *p, const float *core, const float *u_in, 
         g.tn = K == 3 && D2s == 32 && 4 * D1s + 8 * D2s + 2 * N3p <= 512 && !(ev && ev[0] == '0');
         const char *e3 = std::getenv("TDC_LAYER_NCAT3");  // A/B knob
         g.ncat3 = e3 ? (e3[0] == '1') : 1;
+        // X and Z in tensor memory (variant 5b): TMEM = X 2x64 | acc1 | 2 acc2 | one acc3
+        const char *ex = std::getenv("TDC_LAYER_XT");  // A/B knob: 0 disables
+        g.xt = g.tn && D1s == 32 && N3p <= 64 && 128 + 4 * D1s + 8 * D2s <= 512 && !(ex && ex[0] == '0');
     }
-    const int tcols = g.tn ? 4 * D1s + 8 * D2s + 2 * N3p : 4 * D1s + 4 * D2s + (g.ncat3 ? 4 : 2) * N3p;
+    const int tcols = g.xt ? 128 + 4 * D1s + 8 * D2s
+                           : g.tn ? 4 * D1s + 8 * D2s + 2 * N3p : 4 * D1s + 4 * D2s + (g.ncat3 ? 4 : 2) * N3p;
     if (tcols > 512) return TDC_OK;
     g.tmem_cols = 32;
     while (g.tmem_cols < tcols) g.tmem_cols *= 2;

@@ -105,7 +105,7 @@ __host__ __device__ inline LayerSmem layer_smem(const BfLayerArgs &g) {
     s.w2 = o;   o += (uint32_t)(g.D1s / 32) * g.KK * 4 * 2 * g.D2s * 16;
     s.w3 = o;   o += (uint32_t)(g.D2s / 8) * 2 * g.N3p * 16;
     s.band = o; o += 2u * (g.D1s / 8) * g.NRB * g.Wq * 16;
-    s.z = o;    o += 2u * 2u * (g.D2s / 8) * g.ZR * 16;  // two Z buffers (hi | lo each)
+    s.z = o;    o += g.xt ? 0u : 2u * 2u * (g.D2s / 8) * g.ZR * 16;  // two Z buffers (hi | lo each)
     s.scr = o;  o += kEpiScr;
     s.xch = o;  o += g.tn ? 2 * 4 * 16 * 4 : 0;  // TN: epilogue-2 row exchange
     s.bars = o; o += 64 * 8 + 16;
@@ -730,6 +730,471 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
     if (warp == 1) tmem_dealloc(tmem, (uint32_t)g.tmem_cols);
 }
 
+// Variant 5b: the tap-pair layer kernel with the stage-1 and stage-3 A operands in TENSOR
+// memory.  The kernel above is bound by shared-memory bandwidth (~415 KB of shared-memory
+// traffic per 56x56 tile at 128 B/cycle ~ 1.65 us against a measured ~1.95 us tile period):
+// every SS-MMA re-reads its A tile from shared memory.  Here
+//   * the converters split X into bf16 hi/lo straight into a TMEM slot (tcgen05.st) and
+//     release the fp32 staging slot as soon as they have read it, and stage 1 is a TS-MMA
+//     (A = X hi / lo from TMEM): no bf16 X tile is written to or read from shared memory;
+//   * epilogue 2 writes Z hi/lo back into the first D2s columns of the acc2 buffer it has
+//     just read, and stage 3 is a TS-MMA reading Z from there (acc2 is released by the
+//     stage-3 commit): Z never touches shared memory;
+//   * the freed Z buffers become a third fp32 staging slot.
+// TMEM: X 2 x 64 | acc1 2*D1s | acc2 2 x 4*D2s | acc3 N3p columns (R18 56x56: 512); acc1 and
+// acc3 are single-buffered -- epilogues 1 and 3 read the whole accumulator into registers
+// and release it before their shared-memory / global stores.  K = 3, D1s = D2s = 32,
+// N3p <= 64 (the layer's ranks / channels are what the single-buffer register reads allow).
+__global__ void __launch_bounds__(kLayerThreads, 1)
+tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs g) {
+    constexpr int KT = 3;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const LayerSmem L = layer_smem(g);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L.bars);
+    uint64_t *x_full = bars, *x_empty = bars + 4;      // fp32 staging ring (XS <= 4)
+    uint64_t *xt_full = bars + 8, *xt_empty = bars + 10;  // TMEM X slots (2)
+    uint64_t *w_full = bars + 12;
+    uint64_t *a1_full = bars + 13, *a1_empty = bars + 15;
+    uint64_t *band_ready = bars + 17, *band_free = bars + 19;
+    uint64_t *a2_full = bars + 21, *a2_empty = bars + 23;
+    uint64_t *z_full = bars + 25;
+    uint64_t *a3_full = bars + 29;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 40);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef TDC_TIMELINE
+    const bool tl_on = (int)blockIdx.x == *(volatile int *)&g_tdc_ltl_cta;
+    if (threadIdx.x == 0) LTL(0, 21);
+#endif
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < g.XS; ++i) {
+            mbar_init(&x_full[i], 1);
+            mbar_init(&x_empty[i], 128);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&xt_full[i], 128);
+            mbar_init(&xt_empty[i], 1);
+            mbar_init(&band_ready[i], 128);
+            mbar_init(&band_free[i], 1);
+            mbar_init(&a2_full[i], 1);
+            mbar_init(&a2_empty[i], 128);  // epilogue 3 (acc3 lives in the acc2 buffer)
+            mbar_init(&a1_full[i], 1);
+            mbar_init(&a1_empty[i], 128);
+            mbar_init(&a3_full[i], 1);
+            mbar_init(&z_full[i], 128);
+        }
+        mbar_init(w_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) tma_prefetch(&mapX);
+    if (warp == 1) tmem_alloc(tmem_slot, (uint32_t)g.tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    pdl_launch_dependents();
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) LTL(0, 22);
+
+    const int k0 = (int)((long long)blockIdx.x * g.num_tiles / gridDim.x);
+    const int k1 = (int)((long long)(blockIdx.x + 1) * g.num_tiles / gridDim.x);
+    const int nt = k1 - k0;
+    // TMEM columns
+    // TMEM columns: X slots [0, 128) | acc1 x 2 | acc2 x 2; the acc2 buffer of tile t also holds,
+    // once epilogue 2 has read it, Z hi/lo (columns [64, 96)) and then acc3 (columns [0, N3p))
+    const uint32_t acc1_base = 128, acc2_cols = 4 * g.D2s, acc1_cols = 2 * g.D1s;
+    const uint32_t acc2_base = acc1_base + 2 * acc1_cols, z_off = 64;
+    const uint32_t plane_stride = (uint32_t)g.NRB * g.Wq * 16;
+    const uint32_t band_half = (uint32_t)(g.D1s / 8) * plane_stride;
+    const uint32_t xslot = 2u * g.XR * 128, xhalf = (uint32_t)g.XR * 128;
+
+    if (warp == 0) {  // =============================================== producer
+        const int w1b = (int)(L.w2 - L.w1), w2b = (int)(L.w3 - L.w2), w3b = (int)(L.band - L.w3);
+        auto load_split = [&](uint8_t *dst, const void *src, uint32_t bytes) {
+            const uint32_t piece = 16384;
+            for (uint32_t o = (uint32_t)lane * piece; o < bytes; o += 32 * piece)
+                bulk_load(dst + o, reinterpret_cast<const uint8_t *>(src) + o, bytes - o < piece ? bytes - o : piece,
+                          w_full);
+        };
+        if (lane == 0) mbar_arrive_expect_tx(w_full, (uint32_t)(w1b + w2b + w3b));
+        __syncwarp();
+        load_split(smem + L.w1, g.w1, w1b);
+        load_split(smem + L.w2, g.w2, w2b);
+        load_split(smem + L.w3, g.w3, w3b);
+        __syncwarp();
+        pdl_wait();
+        const uint32_t box_bytes = (uint32_t)g.rpb * g.Wp * 128;
+        int pk = k0, pblk = 0;
+        auto prefetch_next = [&]() {
+            if (pk >= k1) return;
+            const TileGeo pg = tile_geo(g, pk, k0);
+            if (lane == 0)
+                for (int cc = 0; cc < g.cchunks; ++cc) {
+                    tma_prefetch_l2_4d(&mapX, cc * 64, -g.p, pg.ylo + pblk * g.rpb - g.p, pg.b);
+                    tma_prefetch_l2_4d(&mapX, cc * 64 + 32, -g.p, pg.ylo + pblk * g.rpb - g.p, pg.b);
+                }
+            if (++pblk == pg.nb) {
+                pblk = 0;
+                ++pk;
+            }
+        };
+        for (int i = 0; i < g.pf_blocks; ++i) prefetch_next();
+        Ring xr(g.XS);
+        for (int k = k0; k < k1; ++k) {
+            const TileGeo tg = tile_geo(g, k, k0);
+            for (int blk = 0; blk < tg.nb; ++blk) {
+                const int u0 = tg.ylo + blk * g.rpb;
+                prefetch_next();
+                for (int cc = 0; cc < g.cchunks; ++cc, xr.next()) {
+                    mbar_wait(&x_empty[xr.slot], xr.phase ^ 1);
+                    if (lane == 0 && blk == 0 && cc == 0) LTL(k - k0, 0);
+                    if (LKNOB(128) && (k > k0 + 1)) {  // debug: no X traffic after the first tiles
+                        if (elect_one()) mbar_arrive(&x_full[xr.slot]);
+                        __syncwarp();
+                        continue;
+                    }
+                    if (elect_one()) {
+                        uint8_t *dst = smem + L.xs + (size_t)xr.slot * xslot;
+                        mbar_arrive_expect_tx(&x_full[xr.slot], 2 * box_bytes);
+                        tma_load_4d(dst, &mapX, &x_full[xr.slot], cc * 64, -g.p, u0 - g.p, tg.b);
+                        tma_load_4d(dst + xhalf, &mapX, &x_full[xr.slot], cc * 64 + 32, -g.p, u0 - g.p, tg.b);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else if (warp == 1 || warp == kS1Warp || warp == kS3Warp) {  // ============== MMA issue
+        const uint32_t id1 = idesc_bf16(128, 2 * g.D1s), id1h = idesc_bf16(128, g.D1s);
+        const uint32_t id2 = idesc_bf16(128, 2 * g.D2s), id2h = idesc_bf16(128, g.D2s);
+        const uint32_t id3h = idesc_bf16(128, g.N3p);
+        const uint64_t dw1 = sdesc_kmajor_sw128(smem_u32(smem + L.w1));
+        const uint64_t dband = sdesc_kmajor_none(smem_u32(smem + L.band), plane_stride, 128);
+        const uint64_t dw2tn = sdesc_kmajor_none(smem_u32(smem + L.w2), 6 * g.D2s * 16, 128);
+        const uint32_t id2tn = idesc_bf16(128, 4 * g.D2s), id2tnh = idesc_bf16(128, 2 * g.D2s);
+        const uint64_t dw3 = sdesc_kmajor_none(smem_u32(smem + L.w3), 2 * g.N3p * 16, 128);
+        const uint32_t w1_chunk = (uint32_t)2 * g.D1s * 128;
+        const uint32_t w3_plane2 = (uint32_t)2 * 2 * g.N3p * 16;
+        const int kc2 = g.D1s / 32, k3 = g.D2s / 16;
+        mbar_wait(w_full, 0);
+        if (warp == kS1Warp && lane == 0) LTL(0, 23);
+        if (warp == 1) {  // the core stream (stage 2): tap pairs along N, as in the kernel above
+            uint32_t start = 0;
+            for (int t = 0; t < nt; ++t) {
+                if (lane == 0) LTL(t, 11);
+                const uint32_t sb = t & 1, sph = (t >> 1) & 1;
+                mbar_wait(&band_ready[sb], sph);
+                mbar_wait(&a2_empty[sb], sph ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc2_base + sb * acc2_cols;
+                const uint64_t arow = dband + start * (uint32_t)g.Wq;
+                const uint32_t wq = (uint32_t)g.Wq, p2a = (2 * plane_stride) >> 4, lo_a = band_half >> 4;
+                const uint32_t wr = (4 * 6 * g.D2s * 16) >> 4, p2b = (2 * 6 * g.D2s * 16) >> 4;
+                const uint32_t rows16 = ((uint32_t)g.D2s * 16) >> 4;
+                for (int kc = 0; kc < (LKNOB(16) ? 0 : kc2); ++kc) {
+                    const uint64_t ak = arow + (uint32_t)kc * ((4 * plane_stride) >> 4);
+                    const uint64_t bk = dw2tn + (uint32_t)kc * KT * wr;
+                    if (elect_one()) {
+#pragma unroll
+                        for (int r = 0; r < KT; ++r)
+#pragma unroll
+                            for (int j = 0; j < 2; ++j) {
+                                const uint64_t aj = ak + r * wq + j * p2a, bj = bk + r * wr + j * p2b;
+                                mma_bf16(d, aj, bj, id2tn, (kc > 0) || r || j);
+                                mma_bf16(d + g.D2s, aj + lo_a, bj + rows16, id2tnh, 1);
+                                mma_bf16(d, aj + 2, bj + 4 * rows16, id2, 1);
+                                mma_bf16(d, aj + 2 + lo_a, bj + 4 * rows16, id2h, 1);
+                            }
+                    }
+                    __syncwarp();
+                }
+                if (elect_one()) {
+                    mma_commit(&band_free[sb]);
+                    mma_commit(&a2_full[sb]);
+                }
+                __syncwarp();
+                if (lane == 0) LTL(t, 3);
+                start += g.R;
+                if (start >= (uint32_t)g.NR) start -= g.NR;
+            }
+        } else if (warp == kS1Warp) {  // stage 1: A = X hi / lo from TMEM slots
+            Ring xt(2);
+            uint32_t ublk = 0;
+            for (int t = 0; t < nt; ++t) {
+                const int nb = tile_geo(g, k0 + t, k0).nb;
+                for (int blk = 0; blk < nb; ++blk, ++ublk) {
+                    if (lane == 0 && blk == 0) LTL(t, 13);
+                    const uint32_t ab = ublk & 1, aph = (ublk >> 1) & 1;
+                    mbar_wait(&a1_empty[ab], aph ^ 1);
+                    tc_fence_after();
+                    const uint32_t d = tmem + acc1_base + ab * acc1_cols;
+                    for (int cc = 0; cc < g.cchunks; ++cc, xt.next()) {
+                        mbar_wait(&xt_full[xt.slot], xt.phase);
+                        tc_fence_after();
+                        if (elect_one()) {
+                            const uint32_t a = tmem + xt.slot * 64;
+                            const uint64_t b = dw1 + ((cc * w1_chunk) >> 4);
+#pragma unroll
+                            for (int j = 0; j < (LKNOB(32) ? 0 : 4); ++j) {  // K = 16 channels = 8 TMEM columns
+                                mma_bf16_ts(d, a + j * 8, b + j * 2, id1, (cc > 0) || (j > 0));  // hi * [hi | lo]
+                                mma_bf16_ts(d, a + 32 + j * 8, b + j * 2, id1h, 1);            // lo * hi
+                            }
+                            mma_commit(&xt_empty[xt.slot]);
+                        }
+                        __syncwarp();
+                    }
+                    if (elect_one()) mma_commit(&a1_full[ab]);
+                    __syncwarp();
+                    if (lane == 0 && blk == nb - 1) LTL(t, 2);
+                }
+            }
+        } else {  // stage 3: A = Z hi / lo from the first D2s columns of the acc2 buffer
+            for (int t = 0; t < nt; ++t) {
+                const uint32_t sb = t & 1, sph = (t >> 1) & 1;
+                mbar_wait(&z_full[sb], sph);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t d = tmem + acc2_base + sb * acc2_cols, z = d + z_off;
+                    for (int j = 0; j < (LKNOB(64) ? 0 : k3); ++j) {
+                        const uint64_t b = dw3 + ((j * w3_plane2) >> 4);
+                        // Z channels [16j, 16j+16): hi in columns [16j, 16j+8), lo in [16j+8, 16j+16)
+                        mma_bf16_ts(d, z + j * 16, b, id3h, j > 0);                          // hi * hi
+                        mma_bf16_ts(d, z + j * 16, b + ((g.N3p * 16) >> 4), id3h, 1);         // hi * lo
+                        mma_bf16_ts(d, z + j * 16 + 8, b, id3h, 1);                          // lo * hi
+                    }
+                    mma_commit(&a3_full[sb]);
+                }
+                __syncwarp();
+                if (lane == 0) LTL(t, 4);
+            }
+        }
+    } else if (warp < 6) {  // ========================= epilogue 1: acc1 -> X' band ring
+        const int q = warp & 3;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        const uint32_t bandA = smem_u32(smem + L.band);
+        const int i = q * 32 + lane;
+        const int yy = i / g.Wp, xx = i - yy * g.Wp;
+        uint32_t ublk = 0;
+        int start = 0;
+        for (int t = 0; t < nt; ++t) {
+            const TileGeo tg = tile_geo(g, k0 + t, k0);
+            for (int blk = 0; blk < tg.nb; ++blk, ++ublk) {
+                if (blk == 0 && t > 0) {
+                    const int tw = tg.fresh ? t - 1 : t - 2;
+                    if (tw >= 0) ewait(&band_free[tw & 1], (tw >> 1) & 1);
+                }
+                const uint32_t ab = ublk & 1, aph = (ublk >> 1) & 1;
+                ewait(&a1_full[ab], aph);
+                tc_fence_after();
+                if (threadIdx.x == 64 && blk == 0) LTL(t, 5);
+                uint32_t r0[2][16], r1[2][16];  // D1s = 32: hi part | lo part, two 16-column halves
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    tmem_ld_32x32b_x16(tmem + lane_base + acc1_base + ab * acc1_cols + 16 * h, r0[h]);
+                    tmem_ld_32x32b_x16(tmem + lane_base + acc1_base + ab * acc1_cols + g.D1s + 16 * h, r1[h]);
+                }
+                tmem_ld_wait();
+                tc_fence_before();
+                mbar_arrive_relaxed(&a1_empty[ab]);  // acc1 buffer free for stage-1 block ublk + 2
+                const int y = tg.ylo + blk * g.rpb + yy;
+                const bool valid = i < g.rpb * g.Wp && y < tg.yhi;
+                if (valid && !LKNOB(4)) {
+                    int slot = start + (y - tg.j * g.R);
+                    if (slot >= g.NR) slot -= g.NR;
+                    const bool mirror = slot < g.NRB - g.NR;
+                    const uint32_t pos = (uint32_t)(slot * g.Wq + xx) * 16;
+                    const uint32_t pos2 = pos + (uint32_t)g.NR * g.Wq * 16;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        float v[16];
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(r0[h][jj]) + __uint_as_float(r1[h][jj]);
+#pragma unroll
+                        for (int pl = 0; pl < 2; ++pl) {
+                            uint4 hh, ll;
+                            split_bf16x8(v + 8 * pl, hh, ll);
+                            const uint32_t po = (uint32_t)(2 * h + pl) * plane_stride;
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(bandA + po + pos), "r"(hh.x),
+                                         "r"(hh.y), "r"(hh.z), "r"(hh.w) : "memory");
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(bandA + band_half + po + pos),
+                                         "r"(ll.x), "r"(ll.y), "r"(ll.z), "r"(ll.w) : "memory");
+                            if (mirror) {
+                                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(bandA + po + pos2),
+                                             "r"(hh.x), "r"(hh.y), "r"(hh.z), "r"(hh.w) : "memory");
+                                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(bandA + band_half + po + pos2),
+                                             "r"(ll.x), "r"(ll.y), "r"(ll.z), "r"(ll.w) : "memory");
+                            }
+                        }
+                    }
+                }
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(&band_ready[t & 1]);
+            if (threadIdx.x == 64) LTL(t, 6);
+            start += g.R;
+            if (start >= g.NR) start -= g.NR;
+        }
+    } else if (warp < 10) {  // ======================= epilogue 2: acc2 -> Z hi/lo (TMEM)
+        const int q = warp & 3;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        float *xbuf = reinterpret_cast<float *>(smem + L.xch);  // [chunk 2][quarter 4][16]
+        for (int t = 0; t < nt; ++t) {
+            const uint32_t sb = t & 1, sph = (t >> 1) & 1;
+            ewait(&a2_full[sb], sph);
+            tc_fence_after();
+            if (threadIdx.x == 192) LTL(t, 7);
+            const uint32_t a2 = tmem + lane_base + acc2_base + sb * acc2_cols;
+#pragma unroll
+            for (int ch = 0; ch < 2; ++ch) {  // Z[m] = blk0[m] + blk1[m + 1] (tap pairs, see above)
+                const int c = ch * 16;
+                float p0[16], p1[16];
+                {
+                    uint32_t r0[16], r1[16], r2[16], r3[16];
+                    tmem_ld_32x32b_x16(a2 + c, r0);
+                    tmem_ld_32x32b_x16(a2 + g.D2s + c, r1);
+                    tmem_ld_32x32b_x16(a2 + 2 * g.D2s + c, r2);
+                    tmem_ld_32x32b_x16(a2 + 3 * g.D2s + c, r3);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        p0[jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
+                        p1[jj] = __uint_as_float(r2[jj]) + __uint_as_float(r3[jj]);
+                    }
+                }
+                float *mine = xbuf + (ch * 4 + q) * 16, *next = xbuf + (ch * 4 + ((q + 1) & 3)) * 16;
+                if (lane == 0)
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) mine[jj] = p1[jj];
+                asm volatile("bar.sync 3, 128;" ::: "memory");
+                float v[16];
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                    float s1 = __shfl_down_sync(0xffffffffu, p1[jj], 1);
+                    if (lane == 31) s1 = next[jj];
+                    v[jj] = p0[jj] + s1;
+                }
+                uint32_t zh[8], zl[8];
+#pragma unroll
+                for (int g8 = 0; g8 < 2; ++g8) {
+                    uint4 hh, ll;
+                    split_bf16x8(v + 8 * g8, hh, ll);
+                    zh[4 * g8] = hh.x; zh[4 * g8 + 1] = hh.y; zh[4 * g8 + 2] = hh.z; zh[4 * g8 + 3] = hh.w;
+                    zl[4 * g8] = ll.x; zl[4 * g8 + 1] = ll.y; zl[4 * g8 + 2] = ll.z; zl[4 * g8 + 3] = ll.w;
+                }
+                // Z channels [c, c+16): hi -> columns [c, c+8), lo -> [c+8, c+16) of the buffer
+                // just read -- columns this warp has already loaded for its own lanes (chunk 0
+                // read [0,16) of every block, so chunk 0's Z cannot clobber chunk 1's inputs)
+                if (!LKNOB(8)) {
+                    tmem_st_32x32b_x8(a2 + z_off + c, zh);
+                    tmem_st_32x32b_x8(a2 + z_off + c + 8, zl);
+                }
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&z_full[sb]);
+            if (threadIdx.x == 192) LTL(t, 8);
+        }
+    } else if (warp < 14) {  // ======================= epilogue 3: acc3 (+bias, res, relu) -> Y
+        const int q = warp & 3;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        float *scratch = reinterpret_cast<float *>(smem + L.scr) + q * 1024;
+        const int m = q * 32 + lane;
+        const int yo = m / g.Wq, xo = m - yo * g.Wq;
+        const bool vec = (g.N & 3) == 0;
+        const int nch = g.N3p / 32;  // 1 or 2
+        for (int t = 0; t < nt; ++t) {
+            const int k = k0 + t, b = k / g.T, j = k - b * g.T;
+            const int oy = j * g.R + yo;
+            const bool valid = yo < g.R && oy < g.Ho && xo < g.Wo;
+            const long long orow = ((long long)b * g.Ho + oy) * g.Wo + xo;
+            float *dst = g.y + orow * g.N;
+            const uint32_t sb = t & 1, sph = (t >> 1) & 1;
+            const uint32_t a3 = tmem + lane_base + acc2_base + sb * acc2_cols;
+            ewait(&a3_full[sb], sph);
+            tc_fence_after();
+            if (threadIdx.x == 320) LTL(t, 9);
+            // chunk by chunk; acc3 is released once its last chunk has been read, so stage 3 of
+            // the next tile overlaps the last chunk's stores
+            for (int c2 = 0; c2 < nch; ++c2) {
+                const int c = 32 * c2;
+                float v[32];
+                {
+                    uint32_t r0[16], r1[16];
+                    tmem_ld_32x32b_x16(a3 + c, r0);
+                    tmem_ld_32x32b_x16(a3 + c + 16, r1);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) {
+                        v[jj] = __uint_as_float(r0[jj]);
+                        v[16 + jj] = __uint_as_float(r1[jj]);
+                    }
+                }
+                if (c2 == nch - 1) {
+                    tc_fence_before();
+                    mbar_arrive_relaxed(&a2_empty[sb]);  // the acc2 buffer is free for S2(t + 2)
+                }
+                if (c >= g.N) continue;  // warp-uniform
+                epi_bias_res_relu<32>(v, c, g.N, g.bias, (g.res && valid) ? g.res + orow * g.N : nullptr, g.relu);
+                if (LKNOB(1)) {
+                } else if (vec && c + 32 <= g.N) {
+                    warp_store_block32(scratch, v, valid ? dst + c : nullptr, lane);
+                } else if (valid) {
+                    _Pragma("unroll") for (int jj = 0; jj < 32; ++jj) if (c + jj < g.N) dst[c + jj] = v[jj];
+                }
+            }
+            if (threadIdx.x == 320) LTL(t, 10);
+        }
+    } else {  // ======================= converters: fp32 staging -> bf16 hi/lo in a TMEM slot
+        const int q = warp & 3;  // TMEM lane quarter = warp % 4; thread = X block row
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        const int row = q * 32 + lane;
+        const bool crow = row < g.XR;
+        Ring xr(g.XS), xt(2);
+        for (int k = k0; k < k1; ++k) {
+            const TileGeo tg = tile_geo(g, k, k0);
+            for (int blk = 0; blk < tg.nb; ++blk)
+                for (int cc = 0; cc < g.cchunks; ++cc, xr.next(), xt.next()) {
+                    mbar_wait(&x_full[xr.slot], xr.phase);
+                    if (row == 0 && blk == tg.nb - 1 && cc == g.cchunks - 1) LTL(k - k0, 20);
+                    mbar_wait(&xt_empty[xt.slot], xt.phase ^ 1);
+                    tc_fence_after();
+                    const uint32_t base = smem_u32(smem + L.xs + (size_t)xr.slot * xslot);
+                    const uint32_t tx = tmem + lane_base + xt.slot * 64;
+#pragma unroll
+                    for (int hf = 0; hf < (LKNOB(2) ? 0 : 2); ++hf) {  // box hf = channels 32*hf .. 32*hf + 31
+                        float v[32];
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (crow) f = ld_shared_v4(base + hf * xhalf + row * 128 + ((jj ^ (row & 7)) << 4));
+                            v[4 * jj] = f.x; v[4 * jj + 1] = f.y; v[4 * jj + 2] = f.z; v[4 * jj + 3] = f.w;
+                        }
+                        uint32_t h[16], l[16];
+#pragma unroll
+                        for (int g8 = 0; g8 < 4; ++g8) {
+                            uint4 hh, ll;
+                            split_bf16x8(v + 8 * g8, hh, ll);
+                            h[4 * g8] = hh.x; h[4 * g8 + 1] = hh.y; h[4 * g8 + 2] = hh.z; h[4 * g8 + 3] = hh.w;
+                            l[4 * g8] = ll.x; l[4 * g8 + 1] = ll.y; l[4 * g8 + 2] = ll.z; l[4 * g8 + 3] = ll.w;
+                        }
+                        tmem_st_32x32b_x16(tx + 16 * hf, h);       // hi: columns [0, 32)
+                        tmem_st_32x32b_x16(tx + 32 + 16 * hf, l);  // lo: columns [32, 64)
+                    }
+                    mbar_arrive(&x_empty[xr.slot]);  // the fp32 staging slot has been read
+                    tmem_st_wait();
+                    tc_fence_before();
+                    mbar_arrive(&xt_full[xt.slot]);
+                    if ((row & 31) == 0 && blk == tg.nb - 1 && cc == g.cchunks - 1) LTL(k - k0, row == 0 ? 1 : 16 + row / 32);
+                }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (g.dbg && blockIdx.x == 0)
+        for (uint32_t o = threadIdx.x * 16; o + 16 <= L.total - 1024; o += kLayerThreads * 16)
+            *reinterpret_cast<uint4 *>(g.dbg + o) = *reinterpret_cast<const uint4 *>(smem + o);
+    if (warp == 1) tmem_dealloc(tmem, (uint32_t)g.tmem_cols);
+}
+
 cudaError_t bf_layer_launch(const CUtensorMap &mapX, const BfLayerArgs &g, int grid, cudaStream_t st) {
     const int smem = bf_layer_smem_bytes(g);
     auto go = [&](auto kernel) {
@@ -737,6 +1202,7 @@ cudaError_t bf_layer_launch(const CUtensorMap &mapX, const BfLayerArgs &g, int g
         if (e != cudaSuccess) return e;
         return launch_pdl(kernel, grid, kLayerThreads, smem, st, mapX, g);
     };
+    if (g.xt) return go(tdc_bf_layer_tm_kernel);
     if (g.tn) return go(tdc_bf_layer_kernel<3, true>);
     return g.K == 3 ? go(tdc_bf_layer_kernel<3, false>) : go(tdc_bf_layer_kernel<0, false>);
 }
