@@ -80,6 +80,30 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
         : "memory");
 }
 
+// Non-blocking probe of a phase, and a wait that backs off with __nanosleep between probes:
+// for warps whose spinning would take issue slots from working warps on the same SM
+// sub-partition (ncu: the try_wait loops of the epilogue warps were ~30 % of all issued
+// instructions of the layer kernel, the suspend-time hint notwithstanding).
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+template <int MAXNS>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity) {
+    uint32_t ns = 8;
+    while (!mbar_try(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns * 2 > MAXNS ? MAXNS : ns * 2;
+    }
+}
+
 // ---------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");

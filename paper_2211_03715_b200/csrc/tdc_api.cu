@@ -1147,6 +1147,8 @@ tdc_status forward_layer(tdc_conv_plan_s *p, const float *x, float *y, int batch
     g.res = res;
     g.relu = relu;
     const int grid = std::max(1, std::min(g.num_tiles, p->num_sms));
+    if ((long long)g.num_tiles * grid >= (1LL << 32))  // the kernel splits tiles in 32-bit arithmetic
+        return fail(TDC_ERR_INVALID_ARGUMENT, "batch too large for the single-launch layer kernel");
     cudaError_t e = tdc::bf_layer_launch(p->lmapX, g, grid, st);
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 single-launch layer kernel");
     return TDC_OK;

@@ -730,6 +730,32 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
     if (warp == 1) tmem_dealloc(tmem, (uint32_t)g.tmem_cols);
 }
 
+// Incremental tile walk of a CTA's contiguous range (tile_geo without a division per tile:
+// the epilogue / converter warps are issue-bound).  nbf / nbr: stage-1 blocks of a fresh /
+// regular tile.
+struct TileWalk {
+    int b, j;
+    bool first = true;
+    __device__ TileWalk(const BfLayerArgs &g, int k0) : b(k0 / g.T), j(k0 - (k0 / g.T) * g.T) {}
+    __device__ __forceinline__ TileGeo geo(const BfLayerArgs &g, int nbf, int nbr) const {
+        TileGeo t;
+        t.b = b;
+        t.j = j;
+        t.fresh = first || j == 0;
+        t.ylo = j * g.R + (t.fresh ? 0 : g.e);
+        t.yhi = j * g.R + g.R + g.e;
+        t.nb = t.fresh ? nbf : nbr;
+        return t;
+    }
+    __device__ __forceinline__ void next(const BfLayerArgs &g) {
+        first = false;
+        if (++j == g.T) {
+            j = 0;
+            ++b;
+        }
+    }
+};
+
 // Variant 5b: the tap-pair layer kernel with the stage-1 and stage-3 A operands in TENSOR
 // memory.  The kernel above is bound by shared-memory bandwidth (~415 KB of shared-memory
 // traffic per 56x56 tile at 128 B/cycle ~ 1.65 us against a measured ~1.95 us tile period):
@@ -767,6 +793,9 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
     const bool tl_on = (int)blockIdx.x == *(volatile int *)&g_tdc_ltl_cta;
     if (threadIdx.x == 0) LTL(0, 21);
 #endif
+    // epilogue / converter / producer waits back off (debug knob 256: plain spin)
+#define BWAIT(bar, par) (LKNOB(256) ? mbar_wait((bar), (par)) : mbar_wait_backoff<128>((bar), (par)))
+    const int nbf = (g.R + g.e + g.rpb - 1) / g.rpb, nbr = (g.R + g.rpb - 1) / g.rpb;
     if (threadIdx.x == 0) {
         for (int i = 0; i < g.XS; ++i) {
             mbar_init(&x_full[i], 1);
@@ -796,8 +825,8 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) LTL(0, 22);
 
-    const int k0 = (int)((long long)blockIdx.x * g.num_tiles / gridDim.x);
-    const int k1 = (int)((long long)(blockIdx.x + 1) * g.num_tiles / gridDim.x);
+    const int k0 = (int)(blockIdx.x * (unsigned)g.num_tiles / gridDim.x);  // num_tiles * grid < 2^32 (plan)
+    const int k1 = (int)((blockIdx.x + 1) * (unsigned)g.num_tiles / gridDim.x);
     const int nt = k1 - k0;
     // TMEM columns
     // TMEM columns: X slots [0, 128) | acc1 x 2 | acc2 x 2; the acc2 buffer of tile t also holds,
@@ -824,29 +853,16 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
         __syncwarp();
         pdl_wait();
         const uint32_t box_bytes = (uint32_t)g.rpb * g.Wp * 128;
-        int pk = k0, pblk = 0;
-        auto prefetch_next = [&]() {
-            if (pk >= k1) return;
-            const TileGeo pg = tile_geo(g, pk, k0);
-            if (lane == 0)
-                for (int cc = 0; cc < g.cchunks; ++cc) {
-                    tma_prefetch_l2_4d(&mapX, cc * 64, -g.p, pg.ylo + pblk * g.rpb - g.p, pg.b);
-                    tma_prefetch_l2_4d(&mapX, cc * 64 + 32, -g.p, pg.ylo + pblk * g.rpb - g.p, pg.b);
-                }
-            if (++pblk == pg.nb) {
-                pblk = 0;
-                ++pk;
-            }
-        };
-        for (int i = 0; i < g.pf_blocks; ++i) prefetch_next();
+        // no L2 prefetch here: the three fp32 staging slots cover the load latency (TDC_LAYER_PF
+        // measured no gain), and the prefetch loop was ~1400 instructions of code
         Ring xr(g.XS);
-        for (int k = k0; k < k1; ++k) {
-            const TileGeo tg = tile_geo(g, k, k0);
+        TileWalk tw(g, k0);
+        for (int k = k0; k < k1; ++k, tw.next(g)) {
+            const TileGeo tg = tw.geo(g, nbf, nbr);
             for (int blk = 0; blk < tg.nb; ++blk) {
                 const int u0 = tg.ylo + blk * g.rpb;
-                prefetch_next();
                 for (int cc = 0; cc < g.cchunks; ++cc, xr.next()) {
-                    mbar_wait(&x_empty[xr.slot], xr.phase ^ 1);
+                    BWAIT(&x_empty[xr.slot], xr.phase ^ 1);
                     if (lane == 0 && blk == 0 && cc == 0) LTL(k - k0, 0);
                     if (LKNOB(128) && (k > k0 + 1)) {  // debug: no X traffic after the first tiles
                         if (elect_one()) mbar_arrive(&x_full[xr.slot]);
@@ -894,7 +910,9 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
                     const uint64_t ak = arow + (uint32_t)kc * ((4 * plane_stride) >> 4);
                     const uint64_t bk = dw2tn + (uint32_t)kc * KT * wr;
                     if (elect_one()) {
-#pragma unroll
+                        // rolled over the core rows: the whole kernel's per-tile code does not fit the
+                        // 32 KB instruction cache, and a smaller stream measured faster
+#pragma unroll 1
                         for (int r = 0; r < KT; ++r)
 #pragma unroll
                             for (int j = 0; j < 2; ++j) {
@@ -920,7 +938,7 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
             Ring xt(2);
             uint32_t ublk = 0;
             for (int t = 0; t < nt; ++t) {
-                const int nb = tile_geo(g, k0 + t, k0).nb;
+                const int nb = (t == 0 || (k0 + t) % g.T == 0) ? nbf : nbr;
                 for (int blk = 0; blk < nb; ++blk, ++ublk) {
                     if (lane == 0 && blk == 0) LTL(t, 13);
                     const uint32_t ab = ublk & 1, aph = (ublk >> 1) & 1;
@@ -975,15 +993,16 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
         const int yy = i / g.Wp, xx = i - yy * g.Wp;
         uint32_t ublk = 0;
         int start = 0;
-        for (int t = 0; t < nt; ++t) {
-            const TileGeo tg = tile_geo(g, k0 + t, k0);
+        TileWalk tw(g, k0);
+        for (int t = 0; t < nt; ++t, tw.next(g)) {
+            const TileGeo tg = tw.geo(g, nbf, nbr);
             for (int blk = 0; blk < tg.nb; ++blk, ++ublk) {
                 if (blk == 0 && t > 0) {
-                    const int tw = tg.fresh ? t - 1 : t - 2;
-                    if (tw >= 0) ewait(&band_free[tw & 1], (tw >> 1) & 1);
+                    const int tb = tg.fresh ? t - 1 : t - 2;
+                    if (tb >= 0) BWAIT(&band_free[tb & 1], (tb >> 1) & 1);
                 }
                 const uint32_t ab = ublk & 1, aph = (ublk >> 1) & 1;
-                ewait(&a1_full[ab], aph);
+                BWAIT(&a1_full[ab], aph);
                 tc_fence_after();
                 if (threadIdx.x == 64 && blk == 0) LTL(t, 5);
                 uint32_t r0[2][16], r1[2][16];  // D1s = 32: hi part | lo part, two 16-column halves
@@ -1039,11 +1058,11 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
         float *xbuf = reinterpret_cast<float *>(smem + L.xch);  // [chunk 2][quarter 4][16]
         for (int t = 0; t < nt; ++t) {
             const uint32_t sb = t & 1, sph = (t >> 1) & 1;
-            ewait(&a2_full[sb], sph);
+            BWAIT(&a2_full[sb], sph);
             tc_fence_after();
             if (threadIdx.x == 192) LTL(t, 7);
             const uint32_t a2 = tmem + lane_base + acc2_base + sb * acc2_cols;
-#pragma unroll
+#pragma unroll 1
             for (int ch = 0; ch < 2; ++ch) {  // Z[m] = blk0[m] + blk1[m + 1] (tap pairs, see above)
                 const int c = ch * 16;
                 float p0[16], p1[16];
@@ -1101,15 +1120,17 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
         const int yo = m / g.Wq, xo = m - yo * g.Wq;
         const bool vec = (g.N & 3) == 0;
         const int nch = g.N3p / 32;  // 1 or 2
+        TileWalk e3w(g, k0);
         for (int t = 0; t < nt; ++t) {
-            const int k = k0 + t, b = k / g.T, j = k - b * g.T;
+            const int b = e3w.b, j = e3w.j;
+            e3w.next(g);
             const int oy = j * g.R + yo;
             const bool valid = yo < g.R && oy < g.Ho && xo < g.Wo;
             const long long orow = ((long long)b * g.Ho + oy) * g.Wo + xo;
             float *dst = g.y + orow * g.N;
             const uint32_t sb = t & 1, sph = (t >> 1) & 1;
             const uint32_t a3 = tmem + lane_base + acc2_base + sb * acc2_cols;
-            ewait(&a3_full[sb], sph);
+            BWAIT(&a3_full[sb], sph);
             tc_fence_after();
             if (threadIdx.x == 320) LTL(t, 9);
             // chunk by chunk; acc3 is released once its last chunk has been read, so stage 3 of
@@ -1149,17 +1170,18 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
         const int row = q * 32 + lane;
         const bool crow = row < g.XR;
         Ring xr(g.XS), xt(2);
-        for (int k = k0; k < k1; ++k) {
-            const TileGeo tg = tile_geo(g, k, k0);
+        TileWalk tw(g, k0);
+        for (int k = k0; k < k1; ++k, tw.next(g)) {
+            const TileGeo tg = tw.geo(g, nbf, nbr);
             for (int blk = 0; blk < tg.nb; ++blk)
                 for (int cc = 0; cc < g.cchunks; ++cc, xr.next(), xt.next()) {
-                    mbar_wait(&x_full[xr.slot], xr.phase);
+                    BWAIT(&x_full[xr.slot], xr.phase);
                     if (row == 0 && blk == tg.nb - 1 && cc == g.cchunks - 1) LTL(k - k0, 20);
-                    mbar_wait(&xt_empty[xt.slot], xt.phase ^ 1);
+                    BWAIT(&xt_empty[xt.slot], xt.phase ^ 1);
                     tc_fence_after();
                     const uint32_t base = smem_u32(smem + L.xs + (size_t)xr.slot * xslot);
                     const uint32_t tx = tmem + lane_base + xt.slot * 64;
-#pragma unroll
+#pragma unroll 1
                     for (int hf = 0; hf < (LKNOB(2) ? 0 : 2); ++hf) {  // box hf = channels 32*hf .. 32*hf + 31
                         float v[32];
 #pragma unroll
@@ -1193,6 +1215,7 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
         for (uint32_t o = threadIdx.x * 16; o + 16 <= L.total - 1024; o += kLayerThreads * 16)
             *reinterpret_cast<uint4 *>(g.dbg + o) = *reinterpret_cast<const uint4 *>(smem + o);
     if (warp == 1) tmem_dealloc(tmem, (uint32_t)g.tmem_cols);
+#undef BWAIT
 }
 
 cudaError_t bf_layer_launch(const CUtensorMap &mapX, const BfLayerArgs &g, int grid, cudaStream_t st) {
