@@ -129,6 +129,7 @@ struct tdc_conv_plan_s {
     tdc::BfCoreArgs bf_core;
     bool fuse3 = false;            // 3xBF16: core + stage 3 in one kernel (Z on chip)
     tdc_plan_hints hints = {-1, 0, 0, 0, 0, 0, 0, 0, 0, 0, -1};  // planner overrides (tdc_conv_plan_ex)
+    int latency_mode = 0;          // 3xBF16 3-launch plan for a small batch (plan_bf16)
     CUtensorMap mapY3;             // 3xBF16 stage 3: TMA map of the output (per y pointer)
     const float *last_y3 = nullptr;
     long long last_y3_rows = 0;
@@ -401,8 +402,20 @@ tdc_status plan_tc(tdc_conv_plan_s *p, const float *core, const float *u_in, con
 // Plan the 3xBF16 3-launch variant (fp32-grade accuracy, bf16 tensor cores).
 // Returns TDC_OK with *used = false when the band-resident core kernel does not
 // fit (the caller then plans 3xTF32 instead).
+tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_in, const float *u_out,
+                          const float *bias, bool *used);
 tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, const float *u_out,
                      const float *bias, bool *used) {
+    const tdc_plan_hints saved = p->hints;
+    const tdc_status st = plan_bf16_impl(p, core, u_in, u_out, bias, used);
+    if (st != TDC_OK || !*used) {  // latency-mode hints belong to this variant only
+        p->hints = saved;
+        p->latency_mode = 0;
+    }
+    return st;
+}
+tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_in, const float *u_out,
+                          const float *bias, bool *used) {
     *used = false;
     const tdc_conv_desc &d = p->desc;
     const int C = d.c_in, N = d.c_out, D1 = d.rank_in, D2 = d.rank_out, K = d.kernel;
@@ -415,6 +428,24 @@ tdc_status plan_bf16(tdc_conv_plan_s *p, const float *core, const float *u_in, c
     const long long phase_rows = (long long)Bm * Hq * Wq;
     const long long M1 = (long long)Bm * H * W, M2 = phase_rows, M3 = (long long)Bm * Ho * Wo;
     if (M1 > (1LL << 31) - 256 || M2 * s * s > (1LL << 31) - 256) return TDC_OK;
+    {   // Latency mode (small batches): when even 32-wide core N tiles leave half of the SMs
+        // idle, every kernel is a chain of a few tiles and its length, not throughput, sets the
+        // time -- 32-wide N tiles everywhere and the core's K split over a 4-CTA cluster
+        // (batch 1, scripts/b1_sweep_hints2.sh: 7x7 24.8 -> 18.4 us, 14x14 17.5 -> 14.4 us,
+        // 28x28 s1 13.8 -> 12.8 us).  Only without explicit planner hints.
+        tdc_plan_hints &h = p->hints;
+        const bool none = h.core3 < 0 && h.fused_layer < 0 && !h.bn_stage1 && !h.bn_core && !h.bn_stage3 &&
+                          !h.ksplit_stage1 && !h.ksplit_core && !h.ksplit_stage3 && !h.gsplit_stage1 &&
+                          !h.gsplit_core && !h.gsplit_stage3;
+        const char *ev = std::getenv("TDC_NO_LATENCY_MODE");
+        if (none && !(ev && ev[0] && ev[0] != '0') &&
+            (long long)div_up((int)M2, 128) * div_up(D2s, 32) * 2 <= p->num_sms) {
+            h.bn_stage1 = h.bn_core = h.bn_stage3 = 32;
+            if (D1s / 32 >= 2) h.ksplit_core = 4;
+            h.core3 = 0;
+            p->latency_mode = 1;
+        }
+    }
     auto pick = [&](int nn, long long mrows) {
         int b = 32;
         while (b < nn && b < 256) b *= 2;
