@@ -348,8 +348,11 @@ def impl_tdc(args):
         bound = "alu" if args.math == "fp32" else "tensor"
         roof = {"bound": bound, "achieved": row["tflops"], "peak": round(eng, 1), "unit": "TFLOP/s",
                 "frac": round(row["tflops"] / eng, 4)}
-        peak_src = ("FP32 FFMA: 148 SMs x 128 lanes x 2 x sm_max_mhz (DESIGN.md)" if args.math == "fp32"
-                    else f"TF32 = measured bf16 burst x 1.1/2.25 ({peaks['source']})")
+        peak_src = {"fp32": "FP32 FFMA: 148 SMs x 128 lanes x 2 x sm_max_mhz (DESIGN.md)",
+                    "tf32": f"TF32 = measured bf16 burst x 1.1/2.25 ({peaks['source']})",
+                    "3xtf32": f"3xTF32 = (measured bf16 burst x 1.1/2.25) / 3 ({peaks['source']})",
+                    "3xbf16": f"3xBF16 = measured bf16 burst / 3, three bf16 products per fp32-grade "
+                              f"product ({peaks['source']})"}[args.math]
     else:
         roof = {"bound": "hbm", "achieved": row["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(row["gbs"] / peaks["hbm_gbs"], 4)}

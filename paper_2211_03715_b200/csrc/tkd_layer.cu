@@ -1079,16 +1079,25 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
                         p1[jj] = __uint_as_float(r2[jj]) + __uint_as_float(r3[jj]);
                     }
                 }
-                float *mine = xbuf + (ch * 4 + q) * 16, *next = xbuf + (ch * 4 + ((q + 1) & 3)) * 16;
+                const uint32_t mine = smem_u32(xbuf + (ch * 4 + q) * 16),
+                               next = smem_u32(xbuf + (ch * 4 + ((q + 1) & 3)) * 16);
                 if (lane == 0)
 #pragma unroll
-                    for (int jj = 0; jj < 16; ++jj) mine[jj] = p1[jj];
+                    for (int j4 = 0; j4 < 4; ++j4)
+                        st_shared_v4(mine + 16 * j4, p1[4 * j4], p1[4 * j4 + 1], p1[4 * j4 + 2], p1[4 * j4 + 3]);
                 asm volatile("bar.sync 3, 128;" ::: "memory");
+                float nx[16];
+                if (lane == 31)
+#pragma unroll
+                    for (int j4 = 0; j4 < 4; ++j4) {
+                        const float4 f = ld_shared_v4(next + 16 * j4);
+                        nx[4 * j4] = f.x; nx[4 * j4 + 1] = f.y; nx[4 * j4 + 2] = f.z; nx[4 * j4 + 3] = f.w;
+                    }
                 float v[16];
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) {
                     float s1 = __shfl_down_sync(0xffffffffu, p1[jj], 1);
-                    if (lane == 31) s1 = next[jj];
+                    if (lane == 31) s1 = nx[jj];
                     v[jj] = p0[jj] + s1;
                 }
                 uint32_t zh[8], zl[8];
@@ -1212,7 +1221,7 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
     tc_fence_before();
     __syncthreads();
     if (g.dbg && blockIdx.x == 0)
-        for (uint32_t o = threadIdx.x * 16; o + 16 <= L.total - 1024; o += kLayerThreads * 16)
+        for (uint32_t o = threadIdx.x * 16; o + 16 <= L.total - 1024; o += blockDim.x * 16)
             *reinterpret_cast<uint4 *>(g.dbg + o) = *reinterpret_cast<const uint4 *>(smem + o);
     if (warp == 1) tmem_dealloc(tmem, (uint32_t)g.tmem_cols);
 #undef BWAIT
