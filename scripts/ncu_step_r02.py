@@ -29,7 +29,7 @@ for r in rows[1:]:
 ks = [ks[i] for i in sorted(ks)]
 short = lambda n: re.sub(r"\(.*", "", n).replace("void ", "").replace("tdc::", "")
 # a layer forward starts at a stage-1 gemm or a single-launch layer kernel
-starts = [i for i, k in enumerate(ks) if "tdc_bf_layer_kernel" in k["name"] or
+starts = [i for i, k in enumerate(ks) if "tdc_bf_layer_" in k["name"] or
           re.search(r"tdc_bf_gemm_kernel<(\(bool\))?(1|true)[,>]", k["name"])]
 groups = [ks[a:b] for a, b in zip(starts, starts[1:] + [len(ks)])]
 names = [s for s, c in synth.R18_SHAPES for _ in range(c)]
