@@ -392,3 +392,33 @@ def test_forward_host_many_matches_device(env):
         assert np.array_equal(y.numpy(), r.cpu().numpy())
     for p in plans:
         p.close()
+
+
+# Batch 1 (the paper's regime, P:L509 / P:L595): the 56x56 layer runs the TMEM-operand
+# single-launch kernel, every other R18 shape a latency-mode three-launch plan (32-wide N
+# tiles, core K split over a 4-CTA cluster).  Full outputs against the oracle.
+@pytest.mark.parametrize("idx", range(len(synth.R18_SHAPES)))
+@pytest.mark.parametrize("bias", [False, True])
+def test_batch1_plans_match_oracle(env, idx, bias):
+    shape = synth.R18_SHAPES[idx][0].with_batch(1)
+    d = synth.make_layer(shape, layer_id=40 + idx, bias=bias)
+    got, info = run_layer(env, shape, d, math="3xbf16")
+    if idx == 0:
+        assert info.variant_name == "layer_3xbf16_fused"
+    else:
+        assert info.variant_name == "tc3_3xbf16_band", info.variant_name
+        assert info.bn_core == 32 and info.bn_stage1 == 32 and info.bn_stage3 == 32
+        assert info.ksplit_core == min(4, (shape.D1 + 31) // 32)  # the cluster splits whole 32-channel chunks
+    e = err(got, ref_of(shape, d))
+    assert e <= TOL["3xbf16"], (shape.name, info.variant_name, e)
+
+
+def test_batch32_plans_are_not_latency_mode(env):
+    # the bench-batch plans keep the throughput tiling (no forced cluster split of the core)
+    torch, tdc = env
+    for shape, _ in synth.R18_SHAPES[1:]:
+        s = shape.with_batch(32)
+        plan = tdc.ConvPlan(s, synth.make_layer(s), math=tdc.TDC_MATH_3XBF16)
+        info = plan.info()
+        plan.close()
+        assert info.ksplit_core == 1, (s.name, info)
