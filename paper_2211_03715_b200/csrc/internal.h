@@ -172,6 +172,9 @@ int bf_core3_smem_bytes(const BfCoreArgs &g);
 int bf_core3_tmem_cols(const BfCoreArgs &g);
 cudaError_t bf_core3_launch(const BfCoreArgs &g, int grid, cudaStream_t st);
 cudaError_t bf_core_launch(const BfCoreArgs &g, int grid, cudaStream_t st);
+// stage 2 on CTA pairs (cta_group::2, tdc_bf_core2_kernel): weights [kc][ntile][half hi|lo][tap][plane][BN][8]
+int bf_core2_smem_bytes(int BN, int nphase, int band_rows, int w_slots);
+cudaError_t bf_core2_launch(const BfCoreArgs &g, int grid, cudaStream_t st);
 bool make_tma_2d_bf16(CUtensorMap *map, const void *base, long long rows, int k_extent, int pitch,
                       int box_rows);
 

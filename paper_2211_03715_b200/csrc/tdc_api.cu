@@ -130,6 +130,8 @@ struct tdc_conv_plan_s {
     bool fuse3 = false;            // 3xBF16: core + stage 3 in one kernel (Z on chip)
     tdc_plan_hints hints = {-1, 0, 0, 0, 0, 0, 0, 0, 0, 0, -1};  // planner overrides (tdc_conv_plan_ex)
     int latency_mode = 0;          // 3xBF16 3-launch plan for a small batch (plan_bf16)
+    bool core2 = false;            // 3xBF16 stage 2 on CTA pairs (tdc_bf_core2_kernel)
+    void *d_c2w = nullptr;         // its weight image [kc][ntile][hi|lo][tap][plane][BN][8]
     CUtensorMap mapY3;             // 3xBF16 stage 3: TMA map of the output (per y pointer)
     const float *last_y3 = nullptr;
     long long last_y3_rows = 0;
@@ -860,6 +862,43 @@ tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_
             g.bias = dbias;
             g.N3 = N; g.N3p = N3p; g.ncat3 = ncat3;
         }
+        // Stage 2 on CTA pairs (cta_group::2): each SM streams half of every weight slice.
+        // For the streamed-weight 3x3 cores (deep layers), whose time is the per-SM weight
+        // streaming, not the MMAs.  TDC_CORE2=0 disables.
+        const char *e2 = std::getenv("TDC_CORE2");
+        const int mt2 = div_up((int)M2, 128);
+        if (!fuse3 && !(e2 && e2[0] == '0') && KK == 9 && tg == 9 && !resident && ks2 == 1 && gs2 <= 1 &&
+            2 * BN2 <= 256 && mt2 >= 2 && p->hints.ksplit_core <= 0 && p->hints.gsplit_core <= 0) {
+            int ws2 = 0;
+            for (int ws = 6; ws >= 2 && !ws2; --ws)
+                if (tdc::bf_core2_smem_bytes(BN2, nphase, band_rows, ws) <= p->max_smem) ws2 = ws;
+            if (ws2) {
+                const size_t nc2 = (size_t)k2chunks * nt2 * 2 * 9 * 4 * BN2 * 8;
+                std::vector<uint16_t> c2(nc2, 0);
+                for (int r = 0; r < K; ++r)
+                    for (int t = 0; t < K; ++t)
+                        for (int q = 0; q < D2; ++q)
+                            for (int a = 0; a < D1; ++a) {
+                                const int kc = a / 32, pl = (a % 32) / 8, e8 = a % 8, tap = r * K + t;
+                                const int ntl = q / BN2, n = q % BN2;
+                                const float v = core[(((size_t)q * D1 + a) * K + r) * K + t];
+                                const uint16_t hi = bf16_bits_host(v);
+                                const uint16_t lo = bf16_bits_host(v - bf16_to_float_host(hi));
+                                for (int half = 0; half < 2; ++half) {
+                                    const size_t at =
+                                        (((((((size_t)kc * nt2 + ntl) * 2 + half) * 9 + tap) * 4 + pl) * BN2 + n) * 8) + e8;
+                                    c2[at] = half ? lo : hi;
+                                }
+                            }
+                cudaError_t ce = cudaMalloc(&p->d_c2w, nc2 * sizeof(uint16_t));
+                if (ce == cudaSuccess) ce = cudaMemcpy(p->d_c2w, c2.data(), nc2 * sizeof(uint16_t), cudaMemcpyHostToDevice);
+                if (ce != cudaSuccess) return cuda_fail(ce, "core weights for the CTA-pair kernel");
+                p->weight_bytes += nc2 * sizeof(uint16_t);
+                g.w = reinterpret_cast<const uint16_t *>(p->d_c2w);
+                g.w_slots = ws2;
+                p->core2 = true;
+            }
+        }
     }
     p->fuse3 = fuse3 != 0;
     if (!fuse3) {   // stage 3: A = Z hi/lo bf16, B = U_out bf16; out = Y fp32 (+bias)
@@ -1236,9 +1275,14 @@ tdc_status forward_bf16(tdc_conv_plan_s *p, const float *x, float *y, int batch,
         if (e != cudaSuccess) return cuda_fail(e, "3xBF16 fused core+stage-3 launch");
         return TDC_OK;
     }
-    e = tdc::bf_core_launch(
-        c, grid_ks(c.M, c.ntiles, tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots, c.ksplit),
-                   c.ncat ? 2 * c.BN : c.BN, c.ksplit, c.gsplit), st);
+    if (p->core2) {  // one CTA pair per (pair of M tiles, N tile), persistent over the units
+        const long long units = (long long)div_up(div_up((int)c.M, 128), 2) * c.ntiles;
+        e = tdc::bf_core2_launch(c, 2 * (int)std::max<long long>(1, std::min<long long>(units, p->num_sms / 2)), st);
+    } else {
+        e = tdc::bf_core_launch(
+            c, grid_ks(c.M, c.ntiles, tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots, c.ksplit),
+                       c.ncat ? 2 * c.BN : c.BN, c.ksplit, c.gsplit), st);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "3xBF16 stage-2 launch");
     if (a3.tma_y && (y != p->last_y3 || a3.M != p->last_y3_rows)) {
         // extent = this call's rows, so the stores of the last tile clip at the batch end
@@ -1658,7 +1702,7 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
     const bool tc = p->variant == 2 || p->variant == 4, fz = p->variant == 3;
     std::snprintf(info->variant_name, sizeof info->variant_name, "%s",
                   p->variant == 6 ? "simt3_fp32" : p->variant == 5 ? "layer_3xbf16_fused" :
-                  p->variant == 4 ? (p->fuse3 ? "tc2_3xbf16_core3" : "tc3_3xbf16_band") : fz ? "fused_tc_tf32"
+                  p->variant == 4 ? (p->fuse3 ? "tc2_3xbf16_core3" : p->core2 ? "tc3_3xbf16_pair" : "tc3_3xbf16_band") : fz ? "fused_tc_tf32"
                      : tc ? (p->split ? (p->tc_core ? "tc3_3xtf32_band" : "tc3_3xtf32")
                                       : (p->tc_core ? "tc3_tf32_band" : "tc3_tf32"))
                           : "fused_simt_fp32");
@@ -1973,6 +2017,7 @@ tdc_status tdc_conv_plan_destroy(tdc_conv_plan_t p) {
     cudaFree(p->d_gs);
     cudaFree(p->d_sg);
     cudaFree(p->d_sg_part);
+    cudaFree(p->d_c2w);
     delete p;
     return TDC_OK;
 }

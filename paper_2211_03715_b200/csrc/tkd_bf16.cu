@@ -1286,6 +1286,270 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
     if (warp == 1) tmem_dealloc(tmem, tcols);
 }
 
+// ============================================================ core conv, CTA pair
+// Stage 2 alone on a CTA PAIR (cta_group::2, M = 256): the two CTAs of a cluster run the M
+// tiles 2p and 2p + 1 of the same N tile, and the leader issues every MMA for both.  B (the
+// core weights, N = 2*BN = [hi | lo]) is split along N between the pair: CTA 0 holds the hi
+// rows of each (chunk, tap, plane), CTA 1 the lo rows, so each SM streams HALF of the weight
+// slice per 32-channel chunk while its tensor core does the same MMA work -- the deep layers'
+// core kernels are bound by that per-SM weight streaming (~40-60 GB/s per SM measured;
+// DESIGN.md §8, §7d).  A (the X' band) is per CTA: each loads its own tile's band.
+// Hand-offs: each CTA's producer signals its own full barriers; the peer's idle MMA warp
+// relays "peer slot full" to the leader (remote arrive); the leader's commits are
+// multicast to both CTAs' empty / accumulator-full barriers; the peer's epilogue releases
+// the accumulator on the leader's barrier.  3x3 core (9 taps in one weight slice), streamed
+// weights, Z hi/lo to global like tdc_bf_core_kernel<false, 0, false>.
+__host__ __device__ inline uint32_t bf_core2_wslot(int BN) { return 9u * 4u * (uint32_t)BN * 16u; }
+int bf_core2_smem_bytes(int BN, int nphase, int band_rows, int w_slots) {
+    return 1024 + 2 * 2 * (int)bf_core_a_half(nphase, band_rows) + w_slots * (int)bf_core2_wslot(BN) +
+           kEpiScratch16 + (8 + 3 * w_slots) * 8 + 16;
+}
+
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// commit the leader's MMAs to the barrier at this smem offset in BOTH CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote_release(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAITQ_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITQ_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) tdc_bf_core2_kernel(const BfCoreArgs g) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int BN = g.BN, WS = g.w_slots;
+    const uint32_t band_bytes = (uint32_t)g.band_rows * 16;
+    const uint32_t a_half = bf_core_a_half(g.nphase, g.band_rows), a_bytes = 2 * a_half;
+    const uint32_t w_slot = bf_core2_wslot(BN), w_tap = (uint32_t)BN * 64;  // [tap][4 planes][BN rows][16 B]
+    uint8_t *a_slots = smem;
+    uint8_t *w_slots = smem + 2 * (size_t)a_bytes;
+    float *epi_scratch = reinterpret_cast<float *>(w_slots + (size_t)WS * w_slot);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(epi_scratch) + kEpiScratch16);
+    uint64_t *a_full = bars, *a_empty = bars + 2, *tfull = bars + 4, *tempty = bars + 6;
+    uint64_t *w_full = bars + 8, *w_empty = w_full + WS, *w_peer = w_empty + WS;
+    uint64_t *a_peer = w_peer + WS;  // 2
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_peer + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int ncols = 2 * BN;  // one accumulator buffer: [hi-weight products | lo-weight products]
+    uint32_t tcols = 32;
+    while ((int)tcols < 2 * ncols) tcols *= 2;
+    const int mtiles = (g.M + kBM16 - 1) / kBM16, mpairs = (mtiles + 1) / 2;
+    const int num_units = mpairs * g.ntiles;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], 1);
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 128 + 4);  // own epilogue threads + one arrive per peer epilogue warp
+            mbar_init(&a_peer[i], 1);
+        }
+        for (int i = 0; i < WS; ++i) {
+            mbar_init(&w_full[i], 1);
+            mbar_init(&w_empty[i], 1);
+            mbar_init(&w_peer[i], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(tcols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // both CTAs' barriers initialised, TMEM allocated
+    tc_fence_after();
+    pdl_launch_dependents();
+    const uint32_t tmem = *tmem_slot;
+
+    auto out_row = [&](int m, long long *dst_row) {
+        if (m >= g.M) return false;
+        const int ox = m % g.Wq;
+        const int tt = m / g.Wq;
+        const int oy = tt % g.Hq;
+        const int b = tt / g.Hq;
+        *dst_row = ((long long)b * g.Ho + oy) * g.Wo + ox;
+        return oy < g.Ho && ox < g.Wo;
+    };
+
+    if (warp == 0) {  // ---------------------------------- bulk-copy producer (both CTAs)
+        const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(g.w);
+        pdl_wait();  // X' is written by the previous kernel (stage 1)
+        Ring ra(2), rw(WS);
+        for (int u = cid; u < num_units; u += ncl) {
+            const int pr = u % mpairs, nt = u / mpairs;
+            const int m0 = (2 * pr + (int)rank) * kBM16;  // a phantom tile (odd tile count) reads slack rows
+            for (int kc = 0; kc < g.kchunks; ++kc, ra.next(), rw.next()) {
+                mbar_wait_sleep(&a_empty[ra.slot], ra.phase ^ 1);
+                if (lane == 0) mbar_arrive_expect_tx(&a_full[ra.slot], a_bytes);
+                __syncwarp();
+                uint8_t *dst = a_slots + (size_t)ra.slot * a_bytes;
+                for (int c = lane; c < g.nphase * 8; c += 32) {  // (phase, plane, hi/lo)
+                    const int ph = c >> 3, kg = (c >> 1) & 3, lo = c & 1;
+                    const long long off =
+                        ((long long)(kc * 4 + kg) * g.plane_rows + (long long)g.phase_src[ph] * g.phase_rows + m0) * 8;
+                    bulk_load(dst + lo * a_half + (size_t)(ph * 4 + kg) * band_bytes, (lo ? g.xg_lo : g.xg) + off,
+                              band_bytes, &a_full[ra.slot]);
+                }
+                __syncwarp();
+                mbar_wait(&w_empty[rw.slot], rw.phase ^ 1);
+                if (lane == 0) mbar_arrive_expect_tx(&w_full[rw.slot], w_slot);
+                __syncwarp();
+                // this CTA's half (rank 0: hi rows, rank 1: lo rows) of the (kc, nt) slice
+                const uint8_t *src = wsrc + (((size_t)kc * g.ntiles + nt) * 2 + rank) * w_slot;
+                for (uint32_t o = (uint32_t)lane * 16384; o < w_slot; o += 32 * 16384)
+                    bulk_load(w_slots + (size_t)rw.slot * w_slot + o, src + o, w_slot - o < 16384 ? w_slot - o : 16384,
+                              &w_full[rw.slot]);
+                __syncwarp();
+            }
+        }
+    } else if (warp == 1 && !leader) {  // ------------- peer: relay "my slot is full" to the leader
+        const uint32_t a_peer_l = mapa_shared(smem_u32(a_peer), 0), w_peer_l = mapa_shared(smem_u32(w_peer), 0);
+        Ring ra(2), rw(WS);
+        for (int u = cid; u < num_units; u += ncl)
+            for (int kc = 0; kc < g.kchunks; ++kc, ra.next(), rw.next()) {
+                // cheap release (no GPU-scope membar): the TMA writes are complete
+                mbar_wait(&a_full[ra.slot], ra.phase);
+                if (lane == 0) {
+                    fence_release_smem_cluster();
+                    mbar_arrive_cluster(a_peer_l + ra.slot * 8);
+                }
+                mbar_wait(&w_full[rw.slot], rw.phase);
+                if (lane == 0) {
+                    fence_release_smem_cluster();
+                    mbar_arrive_cluster(w_peer_l + rw.slot * 8);
+                }
+                __syncwarp();
+            }
+    } else if (warp == 1) {  // ---------------------------- leader: MMA issue for the pair
+        const uint32_t idesc = idesc_bf16(2 * kBM16, ncols);
+        const uint64_t da = sdesc_kmajor_none(smem_u32(a_slots), band_bytes, 128);
+        const uint64_t db = sdesc_kmajor_none(smem_u32(w_slots), BN * 16, 128);
+        const uint32_t a_lo = a_half >> 4, wtap16 = w_tap >> 4;
+        const uint32_t plane2a = (2 * band_bytes) >> 4, plane2b = (2 * BN * 16) >> 4;
+        Ring ra(2), rw(WS), acc(2);
+        for (int u = cid; u < num_units; u += ncl, acc.next()) {
+            mbar_wait_acq_cluster(&tempty[acc.slot], acc.phase ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem + acc.slot * ncols;
+            uint32_t accum = 0;
+            for (int kc = 0; kc < g.kchunks; ++kc, ra.next(), rw.next()) {
+                mbar_wait(&a_full[ra.slot], ra.phase);
+                mbar_wait_cluster(&a_peer[ra.slot], ra.phase);
+                mbar_wait(&w_full[rw.slot], rw.phase);
+                mbar_wait_cluster(&w_peer[rw.slot], rw.phase);
+                tc_fence_after();
+                const uint64_t aslot = da + ((ra.slot * a_bytes) >> 4);
+                const uint64_t bslot = db + ((rw.slot * w_slot) >> 4);
+                if (elect_one()) {
+#pragma unroll 1
+                    for (int tt = 0; tt < 9; ++tt) {
+                        const uint64_t a = aslot + (((uint32_t)g.tap_phase[tt] * 4 * band_bytes +
+                                                     (uint32_t)g.tap_off[tt] * 16) >> 4);
+                        const uint64_t b = bslot + tt * wtap16;
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {  // K = 16 = two 8-channel planes
+                            const uint64_t aj = a + j * plane2a, bj = b + j * plane2b;
+                            mma_bf16_pair(d, aj, bj, idesc, accum);       // X' hi x [C hi | C lo]
+                            mma_bf16_pair(d, aj + a_lo, bj, idesc, 1);    // X' lo x [C hi | C lo]
+                            accum = 1;
+                        }
+                    }
+                    mma_commit_pair(&w_empty[rw.slot]);
+                    mma_commit_pair(&a_empty[ra.slot]);
+                }
+                __syncwarp();
+            }
+            if (elect_one()) mma_commit_pair(&tfull[acc.slot]);
+            __syncwarp();
+        }
+    } else if (warp < 6) {  // ------------------ epilogue warps 2..5 (both CTAs): acc -> Z hi/lo
+        const int q = warp & 3;
+        float *scratch = epi_scratch + q * 1024;
+        __nv_bfloat16 *z = reinterpret_cast<__nv_bfloat16 *>(g.z);
+        __nv_bfloat16 *z_lo = reinterpret_cast<__nv_bfloat16 *>(g.z_lo);
+        const int r = q * 32 + lane;  // tile row = TMEM lane
+        const uint32_t tempty_l = mapa_shared(smem_u32(tempty), 0);
+        Ring acc(2);
+        for (int u = cid; u < num_units; u += ncl, acc.next()) {
+            const int pr = u % mpairs, nt = u / mpairs;
+            const int m0 = (2 * pr + (int)rank) * kBM16, n0 = nt * BN;
+            mbar_wait_sleep(&tfull[acc.slot], acc.phase);
+            tc_fence_after();
+            long long dst_row = 0;
+            const bool valid = out_row(m0 + r, &dst_row);
+            const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + acc.slot * ncols;
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t rr[32], r2[32];
+                float v[32];
+                tmem_ld_32x32b_x32(src + c, rr);
+                tmem_ld_32x32b_x32(src + BN + c, r2);
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]) + __uint_as_float(r2[j]);
+                if (n0 + c >= g.Nn) continue;  // warp-uniform
+                uint32_t hw[16], lw[16];
+#pragma unroll
+                for (int pl = 0; pl < 4; ++pl) {
+                    uint4 h, l;
+                    split_bf16x8(v + 8 * pl, h, l);
+                    hw[4 * pl] = h.x; hw[4 * pl + 1] = h.y; hw[4 * pl + 2] = h.z; hw[4 * pl + 3] = h.w;
+                    lw[4 * pl] = l.x; lw[4 * pl + 1] = l.y; lw[4 * pl + 2] = l.z; lw[4 * pl + 3] = l.w;
+                }
+                const long long off = dst_row * g.ldz + n0 + c;
+                warp_store_block32_b16(scratch, hw, valid ? (void *)(z + off) : nullptr, lane);
+                warp_store_block32_b16(scratch, lw, valid ? (void *)(z_lo + off) : nullptr, lane);
+            }
+            tc_fence_before();
+            if (leader) {
+                mbar_arrive_relaxed(&tempty[acc.slot]);
+            } else {
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote_release(tempty_l + acc.slot * 8);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // the leader's MMAs read the peer's shared memory: nobody leaves early
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols) : "memory");
+}
+
+cudaError_t bf_core2_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
+    const int smem = bf_core2_smem_bytes(g.BN, g.nphase, g.band_rows, g.w_slots);
+    cudaError_t e = cudaFuncSetAttribute(tdc_bf_core2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(tdc_bf_core2_kernel, grid, 192, smem, st, g);  // cluster dims are static (2)
+}
+
 cudaError_t bf_core_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
     const int smem = bf_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.tg, g.w_slots, g.ksplit);
     auto go = [&](auto kernel) {

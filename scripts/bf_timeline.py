@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth
 from paper_2211_03715_b200 import tdc
 idx = int(sys.argv[1]) if len(sys.argv) > 1 else 0
-shape = synth.R18_SHAPES[idx][0].with_batch(32)
+shape = synth.R18_SHAPES[idx][0].with_batch(int(os.environ.get("LAYER_B", "32")))
 d = synth.make_layer(shape)
 plan = tdc.ConvPlan(shape, d, math=tdc.TDC_MATH_3XBF16)
 x = torch.from_numpy(synth.nchw_to_nhwc(d["x"])).cuda()

@@ -242,7 +242,7 @@ def test_3xbf16_core3_and_three_launch(env, shape, fuse3, monkeypatch):
     got, info = run_layer(env, s, d, "nhwc", "3xbf16")
     assert "3xbf16" in info.variant_name, info.variant_name
     if not fuse3:
-        assert info.variant_name == "tc3_3xbf16_band"
+        assert info.variant_name in ("tc3_3xbf16_band", "tc3_3xbf16_pair")
     assert err(got, ref_of(s, d)) <= TOL["3xbf16"]
 
 
@@ -252,9 +252,9 @@ def test_3xbf16_variant_names(env, shape, count):
     d = synth.make_layer(shape)
     plan = tdc.ConvPlan(shape.with_batch(32), d, math=tdc.TDC_MATH_3XBF16)
     info = plan.info()
-    assert info.variant_name in ("layer_3xbf16_fused", "tc2_3xbf16_core3", "tc3_3xbf16_band")
+    assert info.variant_name in ("layer_3xbf16_fused", "tc2_3xbf16_core3", "tc3_3xbf16_band", "tc3_3xbf16_pair")
     assert info.launches_per_forward == {"layer_3xbf16_fused": 1, "tc2_3xbf16_core3": 2,
-                                         "tc3_3xbf16_band": 3}[info.variant_name]
+                                         "tc3_3xbf16_band": 3, "tc3_3xbf16_pair": 3}[info.variant_name]
     plan.close()
 
 
@@ -422,3 +422,28 @@ def test_batch32_plans_are_not_latency_mode(env):
         info = plan.info()
         plan.close()
         assert info.ksplit_core == 1, (s.name, info)
+
+
+# Stage 2 on CTA pairs (cta_group::2, tdc_bf_core2_kernel): streamed-weight 3x3 cores.
+# Odd M-tile counts (a phantom tile in the last pair), ragged ranks, a smaller
+# batch than planned, bias; against the oracle and run to run bit-identical.
+@pytest.mark.parametrize("shape", [
+    LayerShape(9, 256, 256, 10, 10, 256, 256, 3, 1, 1),   # 11 M tiles: phantom tile in the last pair
+    LayerShape(10, 192, 320, 9, 11, 160, 224, 3, 1, 1),   # ragged ranks / channels
+    synth.R18_SHAPES[6][0].with_batch(32),                 # the 7x7 R18 layer at the bench batch
+], ids=lambda s: f"{s.B}x{s.C}x{s.H}x{s.W}_D{s.D1}-{s.D2}_s{s.stride}")
+def test_core_on_cta_pairs(env, shape):
+    torch, tdc = env
+    d = synth.make_layer(shape, seed=33, bias=True)
+    plan = tdc.ConvPlan(shape, d, math=tdc.TDC_MATH_3XBF16)
+    info = plan.info()
+    plan.close()
+    if info.variant_name != "tc3_3xbf16_pair":
+        pytest.skip(f"planner chose {info.variant_name} for this shape")
+    for b in (shape.B, max(1, shape.B - 1)):
+        got, info = run_layer(env, shape, d, math="3xbf16", batch=b)
+        assert info.variant_name == "tc3_3xbf16_pair"
+        e = err(got, ref_of(shape, d, b))
+        assert e <= TOL["3xbf16"], (shape, b, e)
+        again, _ = run_layer(env, shape, d, math="3xbf16", batch=b)
+        assert np.array_equal(got, again)
