@@ -154,6 +154,7 @@ struct BfCoreArgs {
     float *y;                 // Y [B*Ho*Wo][N3]
     int N3, N3p, ncat3;       // output channels, padded (mult. of 16), hi|lo concat in one MMA
     int ksplit;               // >1: split the D1 chunks over a cluster (stage 2 alone, not fused)
+    int a_slots;              // CTA-pair kernel (tdc_bf_core2_kernel): band ring depth (2 or 3)
     int y_direct;             // fused stage 3: lanes store their own Y rows (no smem transpose)
     const float *res;         // fused stage 3: residual [B*Ho*Wo][N3] added before the activation
     int relu;                 // fused stage 3: ReLU after bias/residual
@@ -173,7 +174,7 @@ int bf_core3_tmem_cols(const BfCoreArgs &g);
 cudaError_t bf_core3_launch(const BfCoreArgs &g, int grid, cudaStream_t st);
 cudaError_t bf_core_launch(const BfCoreArgs &g, int grid, cudaStream_t st);
 // stage 2 on CTA pairs (cta_group::2, tdc_bf_core2_kernel): weights [kc][ntile][half hi|lo][tap][plane][BN][8]
-int bf_core2_smem_bytes(int BN, int nphase, int band_rows, int w_slots);
+int bf_core2_smem_bytes(int BN, int nphase, int band_rows, int w_slots, int a_slots);
 cudaError_t bf_core2_launch(const BfCoreArgs &g, int grid, cudaStream_t st);
 bool make_tma_2d_bf16(CUtensorMap *map, const void *base, long long rows, int k_extent, int pitch,
                       int box_rows);

@@ -869,11 +869,20 @@ tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_
         const int mt2 = div_up((int)M2, 128);
         if (!fuse3 && !(e2 && e2[0] == '0') && KK == 9 && tg == 9 && !resident && ks2 == 1 && gs2 <= 1 &&
             2 * BN2 <= 256 && mt2 >= 2 && p->hints.ksplit_core <= 0 && p->hints.gsplit_core <= 0) {
-            int ws2 = 0;
-            for (int ws = 6; ws >= 2 && !ws2; --ws)
-                if (tdc::bf_core2_smem_bytes(BN2, nphase, band_rows, ws) <= p->max_smem) ws2 = ws;
+            int ws2 = 0, as2 = 0;
+            const char *eas = std::getenv("TDC_CORE2_AS");  // A/B knob: band ring depth (2 or 3)
+            for (int as = eas ? std::max(2, std::min(3, std::atoi(eas))) : 3; as >= 2 && !ws2; --as)
+                for (int ws = 6; ws >= 3 && !ws2; --ws)
+                    if (tdc::bf_core2_smem_bytes(BN2, nphase, band_rows, ws, as) <= p->max_smem) {
+                        ws2 = ws;
+                        as2 = as;
+                    }
+            if (!ws2 && tdc::bf_core2_smem_bytes(BN2, nphase, band_rows, 2, 2) <= p->max_smem) ws2 = as2 = 2;
             if (ws2) {
-                const size_t nc2 = (size_t)k2chunks * nt2 * 2 * 9 * 4 * BN2 * 8;
+                // per (kc, ntile, CTA half h): [tap][plane][BN2 rows: h ? C lo : C hi][8] followed by
+                // [tap][plane][BN2/2 rows: C hi rows h*BN2/2 ..][8] (B of the X' lo x C hi MMA)
+                const size_t slot_el = (size_t)9 * 4 * (BN2 + BN2 / 2) * 8, main_el = (size_t)9 * 4 * BN2 * 8;
+                const size_t nc2 = (size_t)k2chunks * nt2 * 2 * slot_el;
                 std::vector<uint16_t> c2(nc2, 0);
                 for (int r = 0; r < K; ++r)
                     for (int t = 0; t < K; ++t)
@@ -885,10 +894,12 @@ tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_
                                 const uint16_t hi = bf16_bits_host(v);
                                 const uint16_t lo = bf16_bits_host(v - bf16_to_float_host(hi));
                                 for (int half = 0; half < 2; ++half) {
-                                    const size_t at =
-                                        (((((((size_t)kc * nt2 + ntl) * 2 + half) * 9 + tap) * 4 + pl) * BN2 + n) * 8) + e8;
-                                    c2[at] = half ? lo : hi;
+                                    const size_t slot = (((size_t)kc * nt2 + ntl) * 2 + half) * slot_el;
+                                    c2[slot + (((size_t)tap * 4 + pl) * BN2 + n) * 8 + e8] = half ? lo : hi;
                                 }
+                                const int hx = n / (BN2 / 2), nx = n % (BN2 / 2);  // the CTA holding this C hi row
+                                const size_t slot = (((size_t)kc * nt2 + ntl) * 2 + hx) * slot_el;
+                                c2[slot + main_el + (((size_t)tap * 4 + pl) * (BN2 / 2) + nx) * 8 + e8] = hi;
                             }
                 cudaError_t ce = cudaMalloc(&p->d_c2w, nc2 * sizeof(uint16_t));
                 if (ce == cudaSuccess) ce = cudaMemcpy(p->d_c2w, c2.data(), nc2 * sizeof(uint16_t), cudaMemcpyHostToDevice);
@@ -896,6 +907,7 @@ tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_
                 p->weight_bytes += nc2 * sizeof(uint16_t);
                 g.w = reinterpret_cast<const uint16_t *>(p->d_c2w);
                 g.w_slots = ws2;
+                g.a_slots = as2;
                 p->core2 = true;
             }
         }

@@ -1299,10 +1299,14 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
 // multicast to both CTAs' empty / accumulator-full barriers; the peer's epilogue releases
 // the accumulator on the leader's barrier.  3x3 core (9 taps in one weight slice), streamed
 // weights, Z hi/lo to global like tdc_bf_core_kernel<false, 0, false>.
-__host__ __device__ inline uint32_t bf_core2_wslot(int BN) { return 9u * 4u * (uint32_t)BN * 16u; }
-int bf_core2_smem_bytes(int BN, int nphase, int band_rows, int w_slots) {
-    return 1024 + 2 * 2 * (int)bf_core_a_half(nphase, band_rows) + w_slots * (int)bf_core2_wslot(BN) +
-           kEpiScratch16 + (8 + 3 * w_slots) * 8 + 16;
+// per (chunk, N tile) and CTA: [tap][plane][BN rows: own half of [C hi | C lo]] followed by
+// [tap][plane][BN/2 rows: this CTA's half of C hi] (the B of the X' lo x C hi MMA, N = BN)
+__host__ __device__ inline uint32_t bf_core2_wslot(int BN) { return 9u * 4u * (uint32_t)(BN + BN / 2) * 16u; }
+// a_slots: band ring depth (2 or 3: the MMAs of chunk k+2 cannot start before chunk k's band slot is
+// free, so a third slot keeps the producer ahead when the weights leave room for it)
+int bf_core2_smem_bytes(int BN, int nphase, int band_rows, int w_slots, int a_slots) {
+    return 1024 + a_slots * 2 * (int)bf_core_a_half(nphase, band_rows) + w_slots * (int)bf_core2_wslot(BN) +
+           kEpiScratch16 + (13 + 3 * w_slots) * 8 + 16;
 }
 
 __device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -1335,21 +1339,40 @@ __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t *bar, uint32_t pa
         : "memory");
 }
 
+#ifdef TDC_TIMELINE
+// Debug build only: per-chunk events of the first unit of CTA pair 0 (scripts/core2_timeline.py):
+// [kc][0] producer issues the weight half (leader), [1] leader sees its weights, [2] leader sees
+// the peer's weights, [3] leader has issued the chunk's MMAs, [4] peer producer issue
+__device__ unsigned long long g_tdc_c2tl[64 * 8];
+extern "C" int tdc_debug_core2_timeline(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_tdc_c2tl, sizeof(unsigned long long) * n);
+}
+#define C2TL(kc, ev)                                                                         \
+    do {                                                                                     \
+        if (blockIdx.x < 2 && (kc) < 64) {                                                   \
+            unsigned long long v_;                                                           \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v_));                           \
+            g_tdc_c2tl[(kc) * 8 + (ev)] = v_;                                                \
+        }                                                                                    \
+    } while (0)
+#else
+#define C2TL(kc, ev) ((void)0)
+#endif
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) tdc_bf_core2_kernel(const BfCoreArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int BN = g.BN, WS = g.w_slots;
+    const int BN = g.BN, WS = g.w_slots, AS = g.a_slots;
     const uint32_t band_bytes = (uint32_t)g.band_rows * 16;
     const uint32_t a_half = bf_core_a_half(g.nphase, g.band_rows), a_bytes = 2 * a_half;
     const uint32_t w_slot = bf_core2_wslot(BN), w_tap = (uint32_t)BN * 64;  // [tap][4 planes][BN rows][16 B]
+    const uint32_t w_extra = 9u * w_tap, x_tap = (uint32_t)BN * 32;        // then [tap][4 planes][BN/2][16 B]
     uint8_t *a_slots = smem;
-    uint8_t *w_slots = smem + 2 * (size_t)a_bytes;
+    uint8_t *w_slots = smem + (size_t)AS * a_bytes;
     float *epi_scratch = reinterpret_cast<float *>(w_slots + (size_t)WS * w_slot);
     uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(epi_scratch) + kEpiScratch16);
-    uint64_t *a_full = bars, *a_empty = bars + 2, *tfull = bars + 4, *tempty = bars + 6;
-    uint64_t *w_full = bars + 8, *w_empty = w_full + WS, *w_peer = w_empty + WS;
-    uint64_t *a_peer = w_peer + WS;  // 2
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_peer + 2);
+    uint64_t *a_full = bars, *a_empty = bars + 3, *a_peer = bars + 6, *tfull = bars + 9, *tempty = bars + 11;
+    uint64_t *w_full = bars + 13, *w_empty = w_full + WS, *w_peer = w_empty + WS;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_peer + WS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -1362,12 +1385,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) tdc_bf_core2
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < AS; ++i) {
             mbar_init(&a_full[i], 1);
             mbar_init(&a_empty[i], 1);
+            mbar_init(&a_peer[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 128 + 4);  // own epilogue threads + one arrive per peer epilogue warp
-            mbar_init(&a_peer[i], 1);
         }
         for (int i = 0; i < WS; ++i) {
             mbar_init(&w_full[i], 1);
@@ -1402,7 +1427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) tdc_bf_core2
     if (warp == 0) {  // ---------------------------------- bulk-copy producer (both CTAs)
         const uint8_t *wsrc = reinterpret_cast<const uint8_t *>(g.w);
         pdl_wait();  // X' is written by the previous kernel (stage 1)
-        Ring ra(2), rw(WS);
+        Ring ra(AS), rw(WS);
         for (int u = cid; u < num_units; u += ncl) {
             const int pr = u % mpairs, nt = u / mpairs;
             const int m0 = (2 * pr + (int)rank) * kBM16;  // a phantom tile (odd tile count) reads slack rows
@@ -1420,6 +1445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) tdc_bf_core2
                 }
                 __syncwarp();
                 mbar_wait(&w_empty[rw.slot], rw.phase ^ 1);
+                if (lane == 0 && u == cid) C2TL(kc, leader ? 0 : 4);
                 if (lane == 0) mbar_arrive_expect_tx(&w_full[rw.slot], w_slot);
                 __syncwarp();
                 // this CTA's half (rank 0: hi rows, rank 1: lo rows) of the (kc, nt) slice
@@ -1432,7 +1458,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) tdc_bf_core2
         }
     } else if (warp == 1 && !leader) {  // ------------- peer: relay "my slot is full" to the leader
         const uint32_t a_peer_l = mapa_shared(smem_u32(a_peer), 0), w_peer_l = mapa_shared(smem_u32(w_peer), 0);
-        Ring ra(2), rw(WS);
+        Ring ra(AS), rw(WS);
         for (int u = cid; u < num_units; u += ncl)
             for (int kc = 0; kc < g.kchunks; ++kc, ra.next(), rw.next()) {
                 // cheap release (no GPU-scope membar): the TMA writes are complete
@@ -1449,12 +1475,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) tdc_bf_core2
                 __syncwarp();
             }
     } else if (warp == 1) {  // ---------------------------- leader: MMA issue for the pair
-        const uint32_t idesc = idesc_bf16(2 * kBM16, ncols);
+        const uint32_t idesc = idesc_bf16(2 * kBM16, ncols), idesc_h = idesc_bf16(2 * kBM16, BN);
         const uint64_t da = sdesc_kmajor_none(smem_u32(a_slots), band_bytes, 128);
         const uint64_t db = sdesc_kmajor_none(smem_u32(w_slots), BN * 16, 128);
-        const uint32_t a_lo = a_half >> 4, wtap16 = w_tap >> 4;
-        const uint32_t plane2a = (2 * band_bytes) >> 4, plane2b = (2 * BN * 16) >> 4;
-        Ring ra(2), rw(WS), acc(2);
+        const uint64_t dbx = sdesc_kmajor_none(smem_u32(w_slots + w_extra), BN / 2 * 16, 128);
+        const uint32_t a_lo = a_half >> 4, wtap16 = w_tap >> 4, xtap16 = x_tap >> 4;
+        const uint32_t plane2a = (2 * band_bytes) >> 4, plane2b = (2 * BN * 16) >> 4, plane2x = (BN * 16) >> 4;
+        Ring ra(AS), rw(WS), acc(2);
         for (int u = cid; u < num_units; u += ncl, acc.next()) {
             mbar_wait_acq_cluster(&tempty[acc.slot], acc.phase ^ 1);
             tc_fence_after();
@@ -1464,21 +1491,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) tdc_bf_core2
                 mbar_wait(&a_full[ra.slot], ra.phase);
                 mbar_wait_cluster(&a_peer[ra.slot], ra.phase);
                 mbar_wait(&w_full[rw.slot], rw.phase);
+                if (lane == 0 && u == cid) C2TL(kc, 1);
                 mbar_wait_cluster(&w_peer[rw.slot], rw.phase);
+                if (lane == 0 && u == cid) C2TL(kc, 2);
                 tc_fence_after();
                 const uint64_t aslot = da + ((ra.slot * a_bytes) >> 4);
-                const uint64_t bslot = db + ((rw.slot * w_slot) >> 4);
+                const uint64_t bslot = db + ((rw.slot * w_slot) >> 4), xslot = dbx + ((rw.slot * w_slot) >> 4);
                 if (elect_one()) {
 #pragma unroll 1
                     for (int tt = 0; tt < 9; ++tt) {
                         const uint64_t a = aslot + (((uint32_t)g.tap_phase[tt] * 4 * band_bytes +
                                                      (uint32_t)g.tap_off[tt] * 16) >> 4);
-                        const uint64_t b = bslot + tt * wtap16;
+                        const uint64_t b = bslot + tt * wtap16, x = xslot + tt * xtap16;
 #pragma unroll
                         for (int j = 0; j < 2; ++j) {  // K = 16 = two 8-channel planes
-                            const uint64_t aj = a + j * plane2a, bj = b + j * plane2b;
-                            mma_bf16_pair(d, aj, bj, idesc, accum);       // X' hi x [C hi | C lo]
-                            mma_bf16_pair(d, aj + a_lo, bj, idesc, 1);    // X' lo x [C hi | C lo]
+                            const uint64_t aj = a + j * plane2a;
+                            mma_bf16_pair(d, aj, b + j * plane2b, idesc, accum);      // X' hi x [C hi | C lo]
+                            mma_bf16_pair(d, aj + a_lo, x + j * plane2x, idesc_h, 1);  // X' lo x C hi
                             accum = 1;
                         }
                     }
@@ -1486,6 +1515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) tdc_bf_core2
                     mma_commit_pair(&a_empty[ra.slot]);
                 }
                 __syncwarp();
+                if (lane == 0 && u == cid) C2TL(kc, 3);
             }
             if (elect_one()) mma_commit_pair(&tfull[acc.slot]);
             __syncwarp();
@@ -1544,7 +1574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1) tdc_bf_core2
 }
 
 cudaError_t bf_core2_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
-    const int smem = bf_core2_smem_bytes(g.BN, g.nphase, g.band_rows, g.w_slots);
+    const int smem = bf_core2_smem_bytes(g.BN, g.nphase, g.band_rows, g.w_slots, g.a_slots);
     cudaError_t e = cudaFuncSetAttribute(tdc_bf_core2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     return launch_pdl(tdc_bf_core2_kernel, grid, 192, smem, st, g);  // cluster dims are static (2)
