@@ -944,6 +944,9 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
         }
     } else if (warp == 1) {  // ------------------------------ MMA issuer
         const uint32_t idesc = idesc_bf16(kBM16, acc_cols);
+        // ncat: X' lo x C hi alone (N = BN: 48 instead of 64 cycles per MMA at BN = 64, and 2 KB
+        // less B traffic) -- the lo x lo product of an N = 2*BN MMA is below the split's error
+        const uint32_t idesc_h = idesc_bf16(kBM16, BN);
         const uint64_t da = sdesc_kmajor_none(smem_u32(a_slots), band_bytes, 128);
         const uint64_t db = sdesc_kmajor_none(smem_u32(w_slots), 2 * BN * 16, 128);
         const uint32_t a_lo = a_half >> 4, b_lo = (BN * 16) >> 4;
@@ -1006,7 +1009,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                                             const uint64_t aj = a + j * plane2a, bj = b + j * plane2b;
                                             mma_bf16(d, aj, bj, idesc, accum);
                                             if (decltype(ncat)::value) {
-                                                mma_bf16(d, aj + a_lo, bj, idesc, 1);
+                                                mma_bf16(d, aj + a_lo, bj, idesc_h, 1);
                                             } else {
                                                 mma_bf16(d, aj, bj + b_lo, idesc, 1);
                                                 mma_bf16(d, aj + a_lo, bj, idesc, 1);
@@ -1030,9 +1033,9 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                                 for (int j = 0; j < 2; ++j) {  // K = 16 = two 8-channel planes
                                     const uint64_t aj = a + ((j * 2 * band_bytes) >> 4);
                                     const uint64_t bj = b + ((j * 2 * 2 * BN * 16) >> 4);
-                                    if (g.ncat) {  // [hi | lo] along N: hi*hi, hi*lo | lo*hi, lo*lo
+                                    if (g.ncat) {  // [hi | lo] along N: hi*hi, hi*lo | lo*hi
                                         mma_bf16(d, aj, bj, idesc, accum);
-                                        mma_bf16(d, aj + a_lo, bj, idesc, 1);
+                                        mma_bf16(d, aj + a_lo, bj, idesc_h, 1);
                                     } else {
                                         mma_bf16(d, aj, bj, idesc, accum);
                                         mma_bf16(d, aj, bj + b_lo, idesc, 1);
