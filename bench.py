@@ -463,6 +463,10 @@ def impl_tdc(args):
     if not args.no_b1:
         batch1 = [b1_latency(synth.CONFIG1, "fp32"), b1_latency(synth.CONFIG1, args.math)]
         batch1 += [b1_latency(sh.with_batch(1), args.math) for sh, _ in synth.R18_SHAPES]
+        # the paper's two weak VGG-16 shapes, as whole TKD layers at batch 1
+        batch1 += [dict(b1_latency(sh, args.math), paper_weak_shape="P:L599-602") for sh in synth.PAPER_WEAK_SHAPES]
+        for b in batch1:  # algorithmic bytes over the graph-replayed time, against the HBM peak
+            b["hbm_frac"] = round(b["bytes"] / (b["graph_us"] * 1e-6) / (peaks["hbm_gbs"] * 1e9), 4)
 
     # ---- whole-model inference (BASELINE metric part 2): Tucker ResNet-50 (config 3,
     # batch 32 per GPU, weak scaling) and Tucker VGG-16 (config 4, global batch 64

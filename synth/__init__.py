@@ -69,6 +69,15 @@ R18_SHAPES = [
     (LayerShape(1, 512, 512, 7, 7, 256, 256, 3, 1, 1, "r18_7_512_512_s1"), 3),
 ]
 
+# The two VGG-16 core-convolution shapes the paper names as its weak cases (P:L599-602:
+# "(64, 32, 224, 224) and (64, 32, 112, 112) ... slower than or similar to TVM and cuDNN"),
+# read as core D1 = 64 -> D2 = 32 at H = W = 224 / 112 inside the VGG-16 block's C = N = 64 /
+# 128 layer, batch 1 (the paper's kernel-evaluation batch).
+PAPER_WEAK_SHAPES = [
+    LayerShape(1, 64, 64, 224, 224, 64, 32, 3, 1, 1, "vgg_224_64_64_core64x32"),
+    LayerShape(1, 128, 128, 112, 112, 64, 32, 3, 1, 1, "vgg_112_128_128_core64x32"),
+]
+
 # BASELINE.json configs[4]: rank sweep on a 28x28x256 -> 256 3x3 layer.
 RANK_GRID = (8, 16, 32, 64, 128)
 

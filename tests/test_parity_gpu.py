@@ -447,3 +447,13 @@ def test_core_on_cta_pairs(env, shape):
         assert e <= TOL["3xbf16"], (shape, b, e)
         again, _ = run_layer(env, shape, d, math="3xbf16", batch=b)
         assert np.array_equal(got, again)
+
+
+# The paper's two weak VGG-16 shapes as TKD layers at batch 1: full outputs
+# against the oracle in the headline math mode.
+@pytest.mark.parametrize("shape", synth.PAPER_WEAK_SHAPES, ids=lambda s: s.name)
+def test_paper_weak_vgg_shapes(env, shape):
+    d = synth.make_layer(shape, layer_id=60, bias=True)
+    got, info = run_layer(env, shape, d, math="3xbf16")
+    e = err(got, ref_of(shape, d))
+    assert e <= TOL["3xbf16"], (shape.name, info.variant_name, e)
