@@ -184,6 +184,8 @@ bool make_tma_2d_bf16(CUtensorMap *map, const void *base, long long rows, int k_
 struct BfLayerArgs {
     int B, H, W, C, N, K, KK, s, p, Ho, Wo, Wp, Wq, Hq;
     int R, e, T;              // output rows per tile (R*Wq <= 128), (K-1)/s, tiles per image
+    int TH, nstrips, sw;      // row blocks per image, column strips (Wp > 128: 128-position
+                              // strips of sw = 128 - (K-1) output columns; else 1 strip, sw = Wo)
     int rpb;                  // padded input rows per stage-1 block (rpb*Wp <= 128)
     int NR, NRB;              // band ring rows (2R+e) and buffer rows incl. the mirror rows
     int XR, ZR;               // rows of an X staging tile / a Z plane (multiples of 8, <= 128)

@@ -1086,15 +1086,28 @@ tdc_status plan_layer(tdc_conv_plan_s *p, const float *core, const float *u_in, 
     if (s != 1 || C % 4 || K * K > tdc::kMaxTaps) return TDC_OK;
     const int Wp = W + 2 * pad, Hp = H + 2 * pad;
     const int D1s = round_up(D1, 32), D2s = round_up(D2, 32), N3p = round_up(N, 32);
-    if (D1s > 128 || D2s > 128 || N3p > 128 || Wp > 128 || Wp > 256) return TDC_OK;
+    // rows wider than one 128-row tile: column strips of 128 padded positions, one output row
+    // per tile -- only the TMEM-operand kernel (variant 5b) walks strips
+    const char *ex0 = std::getenv("TDC_LAYER_XT");
+    const bool strips = Wp > 128;
+    if (strips && !(K == 3 && D1s == 32 && D2s == 32 && N3p <= 64 && !(ex0 && ex0[0] == '0'))) return TDC_OK;
+    if (D1s > 128 || D2s > 128 || N3p > 128) return TDC_OK;
     tdc::BfLayerArgs g;
     std::memset(&g, 0, sizeof g);
     g.B = d.batch; g.H = H; g.W = W; g.C = C; g.N = N; g.K = K; g.KK = K * K; g.s = s; g.p = pad;
     g.Ho = p->dims.Ho; g.Wo = p->dims.Wo; g.Wp = Wp; g.Wq = Wp; g.Hq = Hp;
-    g.R = std::min(128 / Wp, g.Ho);
+    g.nstrips = 1;
+    g.sw = g.Wo;
+    if (strips) {
+        g.Wp = g.Wq = 128;
+        g.sw = 128 - (K - 1);
+        g.nstrips = div_up(g.Wo, g.sw);
+    }
+    g.R = std::min(128 / g.Wp, g.Ho);
     g.e = K - 1;
     if (g.R < 1) return TDC_OK;
-    g.T = div_up(g.Ho, g.R);
+    g.TH = div_up(g.Ho, g.R);
+    g.T = g.TH * g.nstrips;
     g.rpb = g.R;
     g.NR = 2 * g.R + g.e;
     {   // windows start at multiples of gcd(R, NR) below NR; the last one (+ its guard row)
@@ -1103,7 +1116,7 @@ tdc_status plan_layer(tdc_conv_plan_s *p, const float *core, const float *u_in, 
         while (b) { const int t = a % b; a = b; b = t; }
         g.NRB = g.NR - a + g.R + g.e + 1;
     }
-    g.XR = round_up(g.R * Wp, 8);   // rpb = R: one block = R padded rows
+    g.XR = round_up(g.R * g.Wp, 8);   // rpb = R: one block = R padded rows
     g.ZR = round_up(g.R * g.Wq, 8);
     if (g.XR > 128 || g.ZR > 128) return TDC_OK;
     g.cchunks = div_up(C, 64);
@@ -1116,6 +1129,10 @@ tdc_status plan_layer(tdc_conv_plan_s *p, const float *core, const float *u_in, 
         // X and Z in tensor memory (variant 5b): TMEM = X 2x64 | acc1 | 2 acc2 | one acc3
         const char *ex = std::getenv("TDC_LAYER_XT");  // A/B knob: 0 disables
         g.xt = g.tn && D1s == 32 && N3p <= 64 && 128 + 4 * D1s + 8 * D2s <= 512 && !(ex && ex[0] == '0');
+        if (strips && !g.xt) return TDC_OK;
+        // one output row per tile: a tap's A spans one ring row (+ 2 positions that only feed
+        // junk columns), so the 5b kernel wraps rows instead of mirroring them
+        if (g.xt && g.R == 1) g.NRB = g.NR;
     }
     const int tcols = g.xt ? 128 + 4 * D1s + 8 * D2s
                            : g.tn ? 4 * D1s + 8 * D2s + 2 * N3p : 4 * D1s + 4 * D2s + (g.ncat3 ? 4 : 2) * N3p;

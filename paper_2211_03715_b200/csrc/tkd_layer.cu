@@ -117,6 +117,7 @@ int bf_layer_smem_bytes(const BfLayerArgs &g) { return (int)layer_smem(g).total;
 struct TileGeo {
     int b, j, ylo, yhi, nb;
     bool fresh;
+    int x0;  // first output column of the tile's strip (variant 5b; 0 elsewhere)
 };
 // Tile k of the CTA whose range starts at k0: image b, row block j, the new band
 // (phase) rows [ylo, yhi) it computes, and the number of stage-1 blocks.  s = 1.
@@ -128,6 +129,7 @@ __device__ __forceinline__ TileGeo tile_geo(const BfLayerArgs &g, int k, int k0)
     t.ylo = t.fresh ? t.j * g.R : t.j * g.R + g.e;
     t.yhi = t.j * g.R + g.R + g.e;
     t.nb = (t.yhi - t.ylo + g.rpb - 1) / g.rpb;
+    t.x0 = 0;
     return t;
 }
 
@@ -733,10 +735,17 @@ tdc_bf_layer_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerArgs 
 // Incremental tile walk of a CTA's contiguous range (tile_geo without a division per tile:
 // the epilogue / converter warps are issue-bound).  nbf / nbr: stage-1 blocks of a fresh /
 // regular tile.
+// Tiles of an image are ordered (strip, row block), so consecutive tiles of a strip slide the
+// band ring down its rows.
 struct TileWalk {
-    int b, j;
+    int b, strip, j;
     bool first = true;
-    __device__ TileWalk(const BfLayerArgs &g, int k0) : b(k0 / g.T), j(k0 - (k0 / g.T) * g.T) {}
+    __device__ TileWalk(const BfLayerArgs &g, int k0) {
+        b = k0 / g.T;
+        const int rem = k0 - b * g.T;
+        strip = rem / g.TH;
+        j = rem - strip * g.TH;
+    }
     __device__ __forceinline__ TileGeo geo(const BfLayerArgs &g, int nbf, int nbr) const {
         TileGeo t;
         t.b = b;
@@ -745,13 +754,17 @@ struct TileWalk {
         t.ylo = j * g.R + (t.fresh ? 0 : g.e);
         t.yhi = j * g.R + g.R + g.e;
         t.nb = t.fresh ? nbf : nbr;
+        t.x0 = strip * g.sw;
         return t;
     }
     __device__ __forceinline__ void next(const BfLayerArgs &g) {
         first = false;
-        if (++j == g.T) {
+        if (++j == g.TH) {
             j = 0;
-            ++b;
+            if (++strip == g.nstrips) {
+                strip = 0;
+                ++b;
+            }
         }
     }
 };
@@ -872,8 +885,8 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
                     if (elect_one()) {
                         uint8_t *dst = smem + L.xs + (size_t)xr.slot * xslot;
                         mbar_arrive_expect_tx(&x_full[xr.slot], 2 * box_bytes);
-                        tma_load_4d(dst, &mapX, &x_full[xr.slot], cc * 64, -g.p, u0 - g.p, tg.b);
-                        tma_load_4d(dst + xhalf, &mapX, &x_full[xr.slot], cc * 64 + 32, -g.p, u0 - g.p, tg.b);
+                        tma_load_4d(dst, &mapX, &x_full[xr.slot], cc * 64, tg.x0 - g.p, u0 - g.p, tg.b);
+                        tma_load_4d(dst + xhalf, &mapX, &x_full[xr.slot], cc * 64 + 32, tg.x0 - g.p, u0 - g.p, tg.b);
                     }
                     __syncwarp();
                 }
@@ -902,26 +915,29 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
                 mbar_wait(&a2_empty[sb], sph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + acc2_base + sb * acc2_cols;
-                const uint64_t arow = dband + start * (uint32_t)g.Wq;
                 const uint32_t wq = (uint32_t)g.Wq, p2a = (2 * plane_stride) >> 4, lo_a = band_half >> 4;
                 const uint32_t wr = (4 * 6 * g.D2s * 16) >> 4, p2b = (2 * 6 * g.D2s * 16) >> 4;
                 const uint32_t rows16 = ((uint32_t)g.D2s * 16) >> 4;
+                const bool wrap = g.R == 1;  // ring rows wrap (no mirror rows, see the planner)
                 for (int kc = 0; kc < (LKNOB(16) ? 0 : kc2); ++kc) {
-                    const uint64_t ak = arow + (uint32_t)kc * ((4 * plane_stride) >> 4);
+                    const uint64_t ak = dband + (uint32_t)kc * ((4 * plane_stride) >> 4);
                     const uint64_t bk = dw2tn + (uint32_t)kc * KT * wr;
                     if (elect_one()) {
                         // rolled over the core rows: the whole kernel's per-tile code does not fit the
                         // 32 KB instruction cache, and a smaller stream measured faster
 #pragma unroll 1
-                        for (int r = 0; r < KT; ++r)
+                        for (int r = 0; r < KT; ++r) {
+                            uint32_t row = start + r;
+                            if (wrap && row >= (uint32_t)g.NR) row -= g.NR;
 #pragma unroll
                             for (int j = 0; j < 2; ++j) {
-                                const uint64_t aj = ak + r * wq + j * p2a, bj = bk + r * wr + j * p2b;
+                                const uint64_t aj = ak + row * wq + j * p2a, bj = bk + r * wr + j * p2b;
                                 mma_bf16(d, aj, bj, id2tn, (kc > 0) || r || j);
                                 mma_bf16(d + g.D2s, aj + lo_a, bj + rows16, id2tnh, 1);
                                 mma_bf16(d, aj + 2, bj + 4 * rows16, id2, 1);
                                 mma_bf16(d, aj + 2 + lo_a, bj + 4 * rows16, id2h, 1);
                             }
+                        }
                     }
                     __syncwarp();
                 }
@@ -938,7 +954,7 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
             Ring xt(2);
             uint32_t ublk = 0;
             for (int t = 0; t < nt; ++t) {
-                const int nb = (t == 0 || (k0 + t) % g.T == 0) ? nbf : nbr;
+                const int nb = (t == 0 || (k0 + t) % g.TH == 0) ? nbf : nbr;
                 for (int blk = 0; blk < nb; ++blk, ++ublk) {
                     if (lane == 0 && blk == 0) LTL(t, 13);
                     const uint32_t ab = ublk & 1, aph = (ublk >> 1) & 1;
@@ -1131,11 +1147,11 @@ tdc_bf_layer_tm_kernel(const __grid_constant__ CUtensorMap mapX, const BfLayerAr
         const int nch = g.N3p / 32;  // 1 or 2
         TileWalk e3w(g, k0);
         for (int t = 0; t < nt; ++t) {
-            const int b = e3w.b, j = e3w.j;
+            const int b = e3w.b, j = e3w.j, ox = e3w.strip * g.sw + xo;
             e3w.next(g);
             const int oy = j * g.R + yo;
-            const bool valid = yo < g.R && oy < g.Ho && xo < g.Wo;
-            const long long orow = ((long long)b * g.Ho + oy) * g.Wo + xo;
+            const bool valid = yo < g.R && oy < g.Ho && xo < g.sw && ox < g.Wo;
+            const long long orow = ((long long)b * g.Ho + oy) * g.Wo + ox;
             float *dst = g.y + orow * g.N;
             const uint32_t sb = t & 1, sph = (t >> 1) & 1;
             const uint32_t a3 = tmem + lane_base + acc2_base + sb * acc2_cols;
