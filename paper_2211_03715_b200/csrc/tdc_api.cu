@@ -867,7 +867,7 @@ tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_
         // streaming, not the MMAs.  TDC_CORE2=0 disables.
         const char *e2 = std::getenv("TDC_CORE2");
         const int mt2 = div_up((int)M2, 128);
-        if (!fuse3 && !(e2 && e2[0] == '0') && KK == 9 && tg == 9 && !resident && ks2 == 1 && gs2 <= 1 &&
+        if (!fuse3 && !(e2 && e2[0] == '0') && KK == 9 && !resident && ks2 == 1 && gs2 <= 1 &&
             2 * BN2 <= 256 && mt2 >= 2 && p->hints.ksplit_core <= 0 && p->hints.gsplit_core <= 0) {
             int ws2 = 0, as2 = 0;
             const char *eas = std::getenv("TDC_CORE2_AS");  // A/B knob: band ring depth (2 or 3)
