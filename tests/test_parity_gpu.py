@@ -255,6 +255,7 @@ def test_3xbf16_variant_names(env, shape, count):
     assert info.variant_name in ("layer_3xbf16_fused", "tc2_3xbf16_core3", "tc3_3xbf16_band", "tc3_3xbf16_pair")
     assert info.launches_per_forward == {"layer_3xbf16_fused": 1, "tc2_3xbf16_core3": 2,
                                          "tc3_3xbf16_band": 3, "tc3_3xbf16_pair": 3}[info.variant_name]
+    assert 0 < info.smem_bytes_per_cta <= 227 * 1024  # the reported footprint of the kernel that runs
     plan.close()
 
 
