@@ -102,7 +102,22 @@ extern "C" int tdc_debug_bfg_span(unsigned long long *host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_tdc_bfg_span, sizeof(unsigned long long) * n);
 }
 #define BFGSPAN(seq, ev) bfgspan((seq), (ev))
+// per-chunk events of CTA 0's first tile of the gemm launches: [seq % 4][chunk < 64][4]:
+// 0 producer issued the chunk's A, 1 converter saw it land, 2 converter done, 3 MMAs issued
+__device__ unsigned long long g_tdc_bfk[4 * 64 * 4];
+__device__ __forceinline__ void bfk(int seq, int tit, int i, int ev) {
+    if (blockIdx.x == 0 && tit == 0 && i < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_tdc_bfk[((seq & 3) * 64 + i) * 4 + ev] = t;
+    }
+}
+extern "C" int tdc_debug_bf_chunks(unsigned long long *host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, g_tdc_bfk, sizeof(unsigned long long) * n);
+}
+#define BFK(seq, it, i, ev) bfk((seq), (it), (i), (ev))
 #else
+#define BFK(seq, it, i, ev) ((void)0)
 #define BFGSPAN(seq, ev) ((void)0)
 #define BFCSPAN(ev) ((void)0)
 #define BFCTAP(i, ev) ((void)0)
@@ -252,6 +267,7 @@ __device__ __forceinline__ void gs_publish(int *flag, bool leader) {
 
 // ============================================================ GEMM (stages 1, 3)
 constexpr int kConvThreads16 = 256;  // 8 converter warps (stage 1 is converter-paced otherwise)
+constexpr int kXT = 2;                // converting GEMMs: X hi/lo TMEM slots (64 columns each)
 
 // KS: 0 plain, 1 cluster split-K, 2 split-K through L2; OB: bf16 planar X' output (stage 1)
 // rather than fp32 -- each instantiation carries only the epilogue code it runs.
@@ -297,11 +313,22 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     uint64_t *red_ready = bempty + SB;  // split-K: all CS partials of the tile written
     uint64_t *red_free = red_ready + 1; // split-K: all CS readers done with this CTA's partial
     uint64_t *rbar = red_free + 1;      // fp32 output: residual block landed in ring buffer [warp][slot]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rbar + 4 * kYRing);
+    uint64_t *xt_full = rbar + 4 * kYRing, *xt_empty = xt_full + kXT;  // CONVERT: TMEM X slots
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xt_empty + kXT);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t ncols = 32;
     while ((int)ncols < BN) ncols *= 2;
+    // CONVERT: the converters write X hi/lo into kXT TMEM slots of 64 columns after the two
+    // accumulators, and stage 1 is a TS-MMA -- the fp32 staging slot is free as soon as it has
+    // been read, and no bf16 X tile goes through shared memory
+    const uint32_t xt_base = 2 * ncols;
+    uint32_t tcols = 2 * ncols + (CONVERT ? 64u * kXT : 0u);
+    {
+        uint32_t p2 = 32;
+        while (p2 < tcols) p2 *= 2;
+        tcols = p2;
+    }
     const int mtiles = (g.M + kBM16 - 1) / kBM16;
     const int num_tiles = mtiles * g.ntiles;
     const int iters = g.taps * g.kchunks;
@@ -326,7 +353,11 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         }
         for (int i = 0; i < SX; ++i) {
             mbar_init(&xfull[i], 1);
-            mbar_init(&xempty[i], 1);  // arrived by the MMA commit
+            mbar_init(&xempty[i], kConvThreads16);  // the converters have read the fp32 slot
+        }
+        for (int i = 0; i < kXT; ++i) {
+            mbar_init(&xt_full[i], kConvThreads16);  // hi/lo written to the TMEM slot
+            mbar_init(&xt_empty[i], 1);             // the MMAs that read it completed
         }
         for (int i = 0; i < SB; ++i) {
             mbar_init(&bfull[i], 1);
@@ -342,7 +373,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         tma_prefetch(&mapB);
     }
     if (threadIdx.x == 0) BFGSPAN(seq, 0);
-    if (warp == 1) tmem_alloc(tmem_slot, 2 * ncols);
+    if (warp == 1) tmem_alloc(tmem_slot, tcols);
     tc_fence_before();
     __syncthreads();
     if (CS > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
@@ -364,6 +395,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                 if (CONVERT) {  // fp32 X: channels [64kc, 64kc+32) and [64kc+32, 64kc+64)
                     mbar_wait(&xempty[r.slot], r.phase ^ 1);
                     if (i == i0 && lane == 0) BFTL(seq, tit, 0);  // producer issues tile
+                    if (lane == 0) BFK(seq, tit, i - i0, 0);
                     if (elect_one()) {
                         uint8_t *dst = xstage + (size_t)r.slot * kStage32;
                         mbar_arrive_expect_tx(&xfull[r.slot], kStage32);
@@ -404,7 +436,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         const uint64_t da = sdesc_kmajor_sw128(smem_u32(ops));
         const uint64_t db = sdesc_kmajor_sw128(smem_u32(CONVERT ? bring : ops + kATile16));
         const uint32_t lo = half >> 4, blo = (CONVERT ? b_tile : half) >> 4;
-        Ring r(S), acc(2), rb(CONVERT ? SB : 1);
+        Ring r(CONVERT ? kXT : S), acc(2), rb(CONVERT ? SB : 1);
         int tit = 0;
         for (int u = cid; u < num_units; u += ncl, acc.next(), ++tit) {
             const int pc = u % GS;
@@ -415,7 +447,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
             const uint32_t d = tmem + acc.slot * ncols;
             for (int i = i0; i < i1; ++i, r.next()) {
                 if (CONVERT) {
-                    mbar_wait(&conv[r.slot], r.phase);
+                    mbar_wait(&xt_full[r.slot], r.phase);
                     mbar_wait(&bfull[rb.slot], rb.phase);
                 } else {
                     mbar_wait(&full[r.slot], r.phase);
@@ -423,22 +455,30 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
                 tc_fence_after();
                 if (i == i0 && lane == 0) BFTL(seq, tit, 2);  // MMA: operands ready
                 if (elect_one()) {
-                    const uint64_t a = da + ((r.slot * slot_bytes) >> 4);
                     const uint64_t b = db + (((CONVERT ? rb.slot * bslot : r.slot * slot_bytes)) >> 4);
+                    if (CONVERT) {  // A = X hi (columns [0, 32)) / lo ([32, 64)) of TMEM slot r
+                        const uint32_t xa = tmem + xt_base + r.slot * 64;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {  // K = 16 bf16 = 32 B per MMA
-                        mma_bf16(d, a + j * 2, b + j * 2, idesc, (i != i0) || (j != 0));
-                        mma_bf16(d, a + j * 2, b + blo + j * 2, idesc, 1);  // hi * lo
-                        mma_bf16(d, a + lo + j * 2, b + j * 2, idesc, 1);   // lo * hi
-                    }
-                    if (CONVERT) {
-                        mma_commit(&xempty[r.slot]);  // staging slot free for the next TMA load
+                        for (int j = 0; j < 4; ++j) {  // K = 16 channels = 8 TMEM columns
+                            mma_bf16_ts(d, xa + j * 8, b + j * 2, idesc, (i != i0) || (j != 0));
+                            mma_bf16_ts(d, xa + j * 8, b + blo + j * 2, idesc, 1);  // hi * lo
+                            mma_bf16_ts(d, xa + 32 + j * 8, b + j * 2, idesc, 1);   // lo * hi
+                        }
+                        mma_commit(&xt_empty[r.slot]);
                         mma_commit(&bempty[rb.slot]);
                     } else {
+                        const uint64_t a = da + ((r.slot * slot_bytes) >> 4);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {  // K = 16 bf16 = 32 B per MMA
+                            mma_bf16(d, a + j * 2, b + j * 2, idesc, (i != i0) || (j != 0));
+                            mma_bf16(d, a + j * 2, b + blo + j * 2, idesc, 1);  // hi * lo
+                            mma_bf16(d, a + lo + j * 2, b + j * 2, idesc, 1);   // lo * hi
+                        }
                         mma_commit(&empty[r.slot]);
                     }
                 }
                 __syncwarp();
+                if (lane == 0) BFK(seq, tit, i - i0, 3);
                 if (CONVERT) rb.next();
             }
             if (elect_one()) mma_commit(&tfull[acc.slot]);
@@ -647,45 +687,48 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
         }
         if (g.tma_y && lane == 0) bulk_wait_group0();  // TMA stores complete before the CTA retires
         (void)res_load;
-    } else if (CONVERT) {  // ----------------- converter: fp32 staging -> bf16 hi/lo A tiles
+    } else if (CONVERT) {  // ----------------- converter: fp32 staging -> bf16 hi/lo in a TMEM slot
+        // thread = (row, 32-channel half): row = this warp's TMEM lane quarter (warp % 4) x 32 +
+        // lane, half = which 4 of the 8 converter warps; reads its 128 B of the fp32 box, writes
+        // 16 hi and 16 lo columns (bf16 pairs) of the row's TMEM lane
         const int tid = threadIdx.x - 192;
-        Ring rx(SX);
+        const int q = warp & 3, hf = tid >> 7, row = q * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        Ring rx(SX), xt(kXT);
         int tit = 0;
         for (int u = cid; u < num_units; u += ncl, ++tit) {
             const int pc = u % GS;
             const int i0 = GS > 1 ? pc * iters / GS : ci0, i1 = GS > 1 ? (pc + 1) * iters / GS : ci1;
-            for (int i = i0; i < i1; ++i, rx.next()) {
+            for (int i = i0; i < i1; ++i, rx.next(), xt.next()) {
                 mbar_wait(&xfull[rx.slot], rx.phase);
                 if (i == i0 && tid == 0) BFTL(seq, tit, 6);  // converter: X landed
-                // thread = (row, 32-channel half): read the row's half from its fp32 box, then
-                // (after every converter thread has read) overwrite the slot in place with the
-                // hi tile [0, 16 KB) and lo tile [16 KB, 32 KB), 128B-swizzled K-major rows
-                const int row = tid & 127, hf = tid >> 7;
-                const uint32_t base = smem_u32(xstage + (size_t)rx.slot * kStage32);
-                const uint32_t box = base + (uint32_t)hf * (kStage32 / 2) + row * 128;
+                if (tid == 0) BFK(seq, tit, i - i0, 1);
+                const uint32_t box = smem_u32(xstage + (size_t)rx.slot * kStage32) + (uint32_t)hf * (kStage32 / 2) +
+                                     row * 128;
                 float v[32];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float4 f = ld_shared_v4(box + ((j ^ (row & 7)) << 4));
                     v[4 * j] = f.x; v[4 * j + 1] = f.y; v[4 * j + 2] = f.z; v[4 * j + 3] = f.w;
                 }
-                uint4 h[4], l[4];
-#pragma unroll
-                for (int g8 = 0; g8 < 4; ++g8) split_bf16x8(v + 8 * g8, h[g8], l[g8]);
-                asm volatile("bar.sync 2, %0;" ::"n"(kConvThreads16) : "memory");  // all reads done
+                mbar_arrive(&xempty[rx.slot]);  // the fp32 slot has been read: the next TMA may land
+                uint32_t h[16], l[16];
 #pragma unroll
                 for (int g8 = 0; g8 < 4; ++g8) {
-                    const int c8 = 4 * hf + g8;
-                    const uint32_t dsto = row * 128 + ((c8 ^ (row & 7)) << 4);
-                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + dsto), "r"(h[g8].x),
-                                 "r"(h[g8].y), "r"(h[g8].z), "r"(h[g8].w)
-                                 : "memory");
-                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + half + dsto),
-                                 "r"(l[g8].x), "r"(l[g8].y), "r"(l[g8].z), "r"(l[g8].w)
-                                 : "memory");
+                    uint4 hh, ll;
+                    split_bf16x8(v + 8 * g8, hh, ll);
+                    h[4 * g8] = hh.x; h[4 * g8 + 1] = hh.y; h[4 * g8 + 2] = hh.z; h[4 * g8 + 3] = hh.w;
+                    l[4 * g8] = ll.x; l[4 * g8 + 1] = ll.y; l[4 * g8 + 2] = ll.z; l[4 * g8 + 3] = ll.w;
                 }
-                fence_proxy_async_smem();
-                mbar_arrive(&conv[rx.slot]);
+                mbar_wait(&xt_empty[xt.slot], xt.phase ^ 1);
+                tc_fence_after();
+                const uint32_t tx = tmem + lane_base + xt_base + xt.slot * 64;
+                tmem_st_32x32b_x16(tx + 16 * hf, h);       // hi: channels 32hf.. -> columns 16hf..
+                tmem_st_32x32b_x16(tx + 32 + 16 * hf, l);  // lo: columns 32 + 16hf..
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&xt_full[xt.slot]);
+                if (tid == 0) BFK(seq, tit, i - i0, 2);
                 if (i == i1 - 1 && tid == 0) BFTL(seq, tit, 7);  // converter: done
             }
         }
@@ -694,7 +737,7 @@ tdc_bf_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
     __syncthreads();
     if (CS > 1) cluster_sync();  // no CTA leaves while a peer may still read its partial
     if (threadIdx.x == 0) BFGSPAN(seq, 2);
-    if (warp == 1) tmem_dealloc(tmem, 2 * ncols);
+    if (warp == 1) tmem_dealloc(tmem, tcols);
 #ifdef TDC_TIMELINE
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_tdc_bf_seq, 1u);
 #endif
@@ -709,7 +752,7 @@ int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages, int 
     const int ops = xstages ? bstages * 2 * b_tile : stages * 2 * (kATile16 + b_tile);
     return 1024 + xstages * kStage32 + ops + bf_epi_bytes(xstages > 0, xstages > 0 && !fp32_out, fp32_out) +
            (ksplit > 1 ? 128 * BN * 4 : 0) +
-           (3 * stages + 4 + 2 * xstages + 2 * bstages + 2 + 4 * kYRing) * 8 + 16;
+           (3 * stages + 4 + 2 * xstages + 2 * bstages + 2 + 4 * kYRing + 2 * kXT) * 8 + 16;
 }
 
 // Ring depths: operand slots (and, for the converting stage 1, the fp32 staging and
