@@ -454,7 +454,7 @@ tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_
         while (b > 64 && div_up((int)mrows, 128) * (long long)div_up(nn, b) < 2 * p->num_sms) b /= 2;
         return b;
     };
-    int BN1 = pick(D1s, M1), BN3 = pick(N, M3);
+    int BN1 = std::min(pick(D1s, M1), 128), BN3 = pick(N, M3);  // stage 1: 2 accumulators + 2 TMEM X slots <= 512 columns
     int BN2 = pick(D2s, M2);
     // few output tiles (deep / strided layers): a narrower core N tile while the grid still
     // fits one wave -- twice the CTAs streaming weight slices (14x14 s2: 26.8 -> 24.6 us,
@@ -500,7 +500,7 @@ tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_
             while (b < v && b < 256) b *= 2;
             return b;
         };
-        if (h.bn_stage1 > 0) BN1 = pow2(h.bn_stage1);
+        if (h.bn_stage1 > 0) BN1 = std::min(pow2(h.bn_stage1), 128);
         if (h.bn_stage3 > 0) BN3 = pow2(h.bn_stage3);
         if (h.ksplit_stage1 > 0) ks1 = std::max(1, std::min({h.ksplit_stage1, 4, C64 / 64}));
         if (h.ksplit_stage3 > 0) ks3 = std::max(1, std::min({h.ksplit_stage3, 4, D2p / 64}));

@@ -777,6 +777,7 @@ cudaError_t bf_gemm_launch(const CUtensorMap &mapA, const CUtensorMap &mapAlo, c
                            const CUtensorMap &mapBlo, const CUtensorMap &mapY, const TcGemmArgs &g, int grid,
                            cudaStream_t st, const CUtensorMap *mapR) {
     if (!mapR) mapR = &mapY;
+    if (g.a_convert && g.BN > 128) return cudaErrorInvalidValue;  // TMEM: 2 accumulators + 2 X slots <= 512 columns
     const int smem = bf_smem_bytes(g.BN, g.stages, g.a_convert ? g.xstages : 0, g.ksplit, g.a_convert ? g.bstages : 0,
                                    g.out_bf16 ? 0 : bf_yring(true, g.yring));
     // the cluster split-K variant is a separate instantiation, so the default kernels carry

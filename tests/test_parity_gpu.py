@@ -458,3 +458,23 @@ def test_paper_weak_vgg_shapes(env, shape):
     got, info = run_layer(env, shape, d, math="3xbf16")
     e = err(got, ref_of(shape, d))
     assert e <= TOL["3xbf16"], (shape.name, info.variant_name, e)
+
+
+def test_wide_rank_stage1_large_batch(env):
+    # Tucker VGG-16 conv4 (28x28, C = N = 512, D = 192) at batch 64: the stage-1 N tile is
+    # capped at 128 (two accumulators + two TMEM X slots in 512 columns); images 0 and 63
+    # against the oracle
+    torch, tdc = env
+    s = LayerShape(64, 512, 512, 28, 28, 192, 192, 3, 1, 1, "vgg_28_512_r192_b64")
+    d = synth.make_layer(s, seed=71, bias=True)
+    plan = tdc.ConvPlan(s, d, math=tdc.TDC_MATH_3XBF16)
+    assert plan.info().bn_stage1 <= 128
+    x = torch.from_numpy(synth.nchw_to_nhwc(d["x"])).cuda()
+    y = torch.empty((s.B, s.Ho, s.Wo, s.N), device="cuda")
+    plan.forward(x, y)
+    torch.cuda.synchronize()
+    got = synth.nhwc_to_nchw(y.cpu().numpy())
+    plan.close()
+    for i in (0, 63):
+        ref = oracle.tkd_stages(d["x"][i:i + 1], d["core"], d["u_in"], d["u_out"], d["bias"], s.stride, s.pad)
+        assert err(got[i:i + 1], ref) <= TOL["3xbf16"], i
