@@ -290,13 +290,16 @@ def impl_tdc(args):
             for r in range(nbuf):
                 L["plan"].forward(xs[r], ys[r], stream=stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for r in range(reps):
-            L["plan"].forward(xs[r % nbuf], ys[r % nbuf], stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        per_shape_ms[s.name] = e0.elapsed_time(e1) / reps
+        trials = []
+        for _ in range(3):  # best of 3: these are plain host launches, a host hiccup starves the GPU
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for r in range(reps):
+                L["plan"].forward(xs[r % nbuf], ys[r % nbuf], stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            trials.append(e0.elapsed_time(e1) / reps)
+        per_shape_ms[s.name] = min(trials)
         del xs, ys
     per_layer_ms = [per_shape_ms[L["shape"].name] for L in layers]
     step_bytes = sum(rl.tkd_bytes(L["shape"]) for L in layers)
@@ -361,7 +364,7 @@ def impl_tdc(args):
                  "peak_source": peak_src,
                  "hbm": {"achieved": row["gbs"], "peak": peaks["hbm_gbs"], "frac": row["hbm_frac"]},
                  "share_of_step": round(dom_share * 1e-3 / sum(per_layer_ms), 3),
-                 "timing": "layer alone, back-to-back forwards between CUDA events on the launching stream, "
+                 "timing": "layer alone, back-to-back forwards between CUDA events on the launching stream (best of 3 trials), "
                            "inputs rotated over > 2x L2"})
 
     # ---- batch-1 latency, the paper's regime (batch 1, averaged over 1000
