@@ -1764,7 +1764,7 @@ tdc_status tdc_conv_plan_query(tdc_conv_plan_t p, tdc_plan_info *info) {
         info->gsplit_core = std::max(1, c.gsplit);
         info->gsplit_stage3 = p->fuse3 ? 1 : std::max(1, p->tc[2].args.gsplit);
         info->tile_w = c.BN;
-        info->threads_per_cta = p->fuse3 ? 320 : 192;
+        info->threads_per_cta = p->fuse3 ? 448 : 192;
         info->smem_bytes_per_cta = p->fuse3   ? tdc::bf_core3_smem_bytes(c)
                                    : p->core2 ? tdc::bf_core2_smem_bytes(c.BN, c.nphase, c.band_rows, c.w_slots, c.a_slots)
                                               : tdc::bf_core_smem_bytes(c.BN, c.nphase, c.band_rows, c.tg, c.w_slots,

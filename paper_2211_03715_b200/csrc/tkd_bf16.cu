@@ -827,9 +827,10 @@ __host__ __device__ inline int bf_pow2_cols(int c) {
 // resident U_out hi|lo panel [BN/8 planes][2*N3p rows][16 B], + 9 barriers.
 __host__ __device__ inline int bf_core3_zbuf(const BfCoreArgs &g) { return (g.BN / 8) * 128 * 16 * 2; }
 __host__ __device__ inline int bf_core3_w3(const BfCoreArgs &g) { return (g.BN / 8) * 2 * g.N3p * 16; }
+// + the second epilogue-3 warp group's transpose scratch (kEpiScratch16)
 int bf_core3_smem_bytes(const BfCoreArgs &g) {
     return bf_core_smem_bytes(g.BN, g.nphase, g.band_rows, g.tg, g.w_slots, 1) + 2 * bf_core3_zbuf(g) +
-           bf_core3_w3(g) + 9 * 8;
+           bf_core3_w3(g) + kEpiScratch16 + 9 * 8;
 }
 __host__ __device__ inline int bf_core3_tmem(const BfCoreArgs &g) {
     const int a2 = bf_pow2_cols(g.ncat ? 2 * g.BN : g.BN), a3 = bf_pow2_cols(g.ncat3 ? 2 * g.N3p : g.N3p);
@@ -845,7 +846,9 @@ int bf_core3_tmem_cols(const BfCoreArgs &g) { return bf_core3_tmem(g); }
 // KS: 0 plain, 1 cluster split-K, 2 split-K through L2 (stage 2 alone); RES: the fused
 // stage-3 epilogue adds a residual (model path) -- compiled only where used.
 template <bool F3, int KS, bool RES>
-__global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const BfCoreArgs g) {
+// F3: 14 warps -- epilogue 3 is split over two groups of four warps (each stores half of the
+// output columns), as the Y stores were the fused kernel's slowest stage
+__global__ void __launch_bounds__(F3 ? 448 : 192, 1) tdc_bf_core_kernel(const BfCoreArgs g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -860,7 +863,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
     uint8_t *a_slots = smem;
     uint8_t *w_slots = smem + 2 * (size_t)a_bytes;
     float *epi_scratch = reinterpret_cast<float *>(w_slots + (size_t)WS * w_slot);
-    uint8_t *zs = reinterpret_cast<uint8_t *>(epi_scratch) + kEpiScratch16;  // F3: 2 Z buffers
+    uint8_t *zs = reinterpret_cast<uint8_t *>(epi_scratch) + (F3 ? 2 : 1) * kEpiScratch16;  // F3: 2 Z buffers
     const int CS = (!F3 && KS == 1 && g.ksplit > 1) ? g.ksplit : 1;           // split-K cluster size
     float *red = reinterpret_cast<float *>(zs);                              // split-K partial [128][BN]
     const uint32_t red_bytes = CS > 1 ? (uint32_t)128 * BN * 4 : 0u;
@@ -904,7 +907,7 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
                 mbar_init(&z_full[i], 128);
                 mbar_init(&z_empty[i], 1);
                 mbar_init(&t3full[i], 1);
-                mbar_init(&t3empty[i], 128);
+                mbar_init(&t3empty[i], 256);  // both epilogue-3 warp groups
             }
         }
         for (int i = 0; i < WS; ++i) {
@@ -1267,9 +1270,10 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             }
             if (warp == 2 && lane == 0) BFCTL(tit, 5);  // epilogue: done
         }
-    } else if (F3) {  // ------------------------- epilogue warps 6..9: acc3 (+bias) -> Y
-        const int q = warp & 3;
-        float *scratch = epi_scratch + q * 1024;
+    } else if (F3) {  // ------------------------- epilogue warps 6..13: acc3 (+bias) -> Y
+        const int q = warp & 3, grp = (warp - 6) >> 2;  // group 0: warps 6-9, group 1: warps 10-13
+        float *scratch = epi_scratch + (warp - 6) * 1024;
+        const int chalf = ((g.N3p / 32 + 1) / 2) * 32;  // output columns per group (whole 32-column chunks)
         Ring a3(2);
         int tit = 0;
         for (int t = TDC_DBG(g, 256) ? num_tiles : cid; t < num_tiles; t += ncl, a3.next(), ++tit) {
@@ -1281,7 +1285,8 @@ __global__ void __launch_bounds__(F3 ? 320 : 192, 1) tdc_bf_core_kernel(const Bf
             const bool valid = out_row(m0 + q * 32 + lane, &dst_row);
             const uint32_t src = tmem + ((uint32_t)(q * 32) << 16) + 2 * ncols + a3.slot * ncols3;
             float *dst = g.y + dst_row * g.N3;
-            for (int c = 0; c < (TDC_DBG(g, 64) ? 0 : g.N3p); c += 32) {  // dbg 64: no E3 TMEM loads
+            const int c_end = (grp + 1) * chalf < g.N3p ? (grp + 1) * chalf : g.N3p;
+            for (int c = grp * chalf; c < (TDC_DBG(g, 64) ? 0 : c_end); c += 32) {  // dbg 64: no E3 TMEM loads
                 uint32_t rr[32];
                 float v[32];
                 tmem_ld_32x32b_x32(src + c, rr);
@@ -1643,7 +1648,7 @@ cudaError_t bf_core3_launch(const BfCoreArgs &g, int grid, cudaStream_t st) {
     auto go = [&](auto kernel) {
         cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        return launch_pdl(kernel, grid, 320, smem, st, g);
+        return launch_pdl(kernel, grid, 448, smem, st, g);
     };
     return g.res ? go(tdc_bf_core_kernel<true, 0, true>) : go(tdc_bf_core_kernel<true, 0, false>);
 }
