@@ -593,7 +593,8 @@ tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_
     int fuse3 = 0;
     {
         const char *ev = std::getenv("TDC_NO_FUSE3");
-        const bool off = (ev && ev[0] && ev[0] != '0') || p->hints.core3 == 0 ||
+        const char *e2f = std::getenv("TDC_CORE2");  // A/B knob: 2 = the CTA-pair core instead of core3
+        const bool off = (ev && ev[0] && ev[0] != '0') || p->hints.core3 == 0 || (e2f && e2f[0] == '2') ||
                          (p->hints.bn_core > 0 && p->hints.bn_core < D2s) || p->hints.ksplit_core > 1;
         int bn = 32;
         while (bn < D2s) bn *= 2;
@@ -867,7 +868,8 @@ tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_
         // streaming, not the MMAs.  TDC_CORE2=0 disables.
         const char *e2 = std::getenv("TDC_CORE2");
         const int mt2 = div_up((int)M2, 128);
-        if (!fuse3 && !(e2 && e2[0] == '0') && KK == 9 && !resident && ks2 == 1 && gs2 <= 1 &&
+        if (!fuse3 && !(e2 && e2[0] == '0') && KK == 9 && (!resident || (e2 && e2[0] == '2')) && ks2 == 1 &&
+            gs2 <= 1 &&
             2 * BN2 <= 256 && mt2 >= 2 && p->hints.ksplit_core <= 0 && p->hints.gsplit_core <= 0) {
             int ws2 = 0, as2 = 0;
             const char *eas = std::getenv("TDC_CORE2_AS");  // A/B knob: band ring depth (2 or 3)
