@@ -873,8 +873,10 @@ tdc_status plan_bf16_impl(tdc_conv_plan_s *p, const float *core, const float *u_
             2 * BN2 <= 256 && mt2 >= 2 && p->hints.ksplit_core <= 0 && p->hints.gsplit_core <= 0) {
             int ws2 = 0, as2 = 0;
             const char *eas = std::getenv("TDC_CORE2_AS");  // A/B knob: band ring depth (2 or 3)
+            const char *ews = std::getenv("TDC_CORE2_WS");  // A/B knob: maximum weight slots
+            const int ws_top = ews ? std::max(3, std::min(6, std::atoi(ews))) : 6;
             for (int as = eas ? std::max(2, std::min(3, std::atoi(eas))) : 3; as >= 2 && !ws2; --as)
-                for (int ws = 6; ws >= 3 && !ws2; --ws)
+                for (int ws = ws_top; ws >= 3 && !ws2; --ws)
                     if (tdc::bf_core2_smem_bytes(BN2, nphase, band_rows, ws, as) <= p->max_smem) {
                         ws2 = ws;
                         as2 = as;

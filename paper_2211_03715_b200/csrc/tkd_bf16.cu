@@ -23,6 +23,8 @@
 #include <type_traits>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 #include "sm100.cuh"
 #include "tkd_common.cuh"
@@ -759,7 +761,8 @@ int bf_smem_bytes(int BN, int stages, int xstages, int ksplit, int bstages, int 
 // weight rings).
 int bf_pick_stages(int BN, int max_smem, int convert, int *xstages, int ksplit, int *bstages, int fp32_out) {
     if (convert) {  // staging (= operand) ring first, then the weight ring
-        int sx = 6, sb = 4;
+        static const int sx_max = std::getenv("TDC_GEMM_SX") ? std::atoi(std::getenv("TDC_GEMM_SX")) : 6;  // A/B knob
+        int sx = sx_max < 2 ? 2 : (sx_max > 6 ? 6 : sx_max), sb = 4;
         while (sb > 2 && bf_smem_bytes(BN, sx, sx, ksplit, sb, fp32_out) > max_smem) --sb;
         while (sx > 2 && bf_smem_bytes(BN, sx, sx, ksplit, sb, fp32_out) > max_smem) --sx;
         if (xstages) *xstages = sx;
